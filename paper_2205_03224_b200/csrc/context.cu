@@ -1,0 +1,1274 @@
+// GeMSLR solve path on one B200: device plan, orchestration and the C-ABI
+// (include/gemslr.h).  arXiv 2205.03224, /root/reference/PAPER.md = "P".
+//
+//   spmv            K1                                   (Note N P:L58-61)
+//   apply_precond   Alg. 2 single pass: down sweep (K4, K6+K7, K8) -> bottom
+//                   block-Jacobi (K9) -> up sweep (K5)
+//   solve           FGMRES(m) with CGS2 (K10-K12), device-side Givens, host
+//                   least squares per cycle
+//   setup           host plan (hostplan.cpp) + bottom-up thick-restart Arnoldi
+//                   on Ĝ_l with the same kernels
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <sys/stat.h>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/gemslr.h"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+namespace gemslr {
+
+static constexpr int kNumSM = 148;
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess) throw Error{GEMSLR_ERR_CUDA, std::string("CUDA: ") + #x + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+// host scalar <-> device scalar
+template <typename T> struct Dev;
+template <> struct Dev<double> { using type = double; };
+template <> struct Dev<zc> { using type = cd; };
+
+// ----------------------------------------------------------------- device memory
+struct Allocator {
+  void *(*alloc_fn)(size_t, void *) = nullptr;
+  void (*free_fn)(void *, void *) = nullptr;
+  void *user = nullptr;
+  void *alloc(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    void *p = nullptr;
+    if (alloc_fn) p = alloc_fn(bytes, user);
+    else if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
+    if (!p) throw Error{GEMSLR_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed"};
+    return p;
+  }
+  void release(void *p) {
+    if (!p) return;
+    if (free_fn) free_fn(p, user); else cudaFree(p);
+  }
+};
+
+struct Pool {                                   // owns every device allocation of a context
+  Allocator *A = nullptr;
+  std::vector<void *> ptrs;
+  size_t bytes = 0;
+  template <typename U>
+  U *get(size_t count) {
+    U *p = static_cast<U *>(A->alloc(count * sizeof(U)));
+    ptrs.push_back(p);
+    bytes += count * sizeof(U);
+    return p;
+  }
+  template <typename U, typename V>
+  U *upload(const std::vector<V> &h, cudaStream_t s) {
+    static_assert(sizeof(U) == sizeof(V), "layout");
+    U *p = get<U>(std::max<size_t>(h.size(), 1));
+    if (!h.empty()) CK(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(U), cudaMemcpyHostToDevice, s));
+    return p;
+  }
+  void clear() {
+    for (void *p : ptrs) A->release(p);
+    ptrs.clear();
+    bytes = 0;
+  }
+};
+
+// ----------------------------------------------------------------- profiling
+enum KernelClass { KC_SPMV = 0, KC_TRI_DOWN, KC_TRI_UP, KC_TRI_LAST, KC_EW, KC_WAXPY, KC_GS, KC_FGM, KC_UTIL, KC_COUNT };
+static const char *kKernelName[KC_COUNT] = {"spmv", "trisolve_down", "trisolve_up", "trisolve_last", "ew",
+                                            "waxpy", "gs", "fgmres_col", "util"};
+
+struct Profiler {
+  bool on = false;
+  struct Rec { int kc; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> freelist;
+  double ms[KC_COUNT] = {0};
+  long long count[KC_COUNT] = {0};
+  cudaEvent_t ev() {
+    if (!freelist.empty()) { cudaEvent_t e = freelist.back(); freelist.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void flush() {
+    for (auto &r : pending) {
+      cudaEventSynchronize(r.b);
+      float t = 0;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      ms[r.kc] += t;
+      count[r.kc] += 1;
+      freelist.push_back(r.a);
+      freelist.push_back(r.b);
+    }
+    pending.clear();
+  }
+  void reset() {
+    flush();
+    for (int i = 0; i < KC_COUNT; ++i) { ms[i] = 0; count[i] = 0; }
+  }
+  ~Profiler() {
+    for (auto &r : pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : freelist) cudaEventDestroy(e);
+  }
+};
+
+struct Timed {                                  // RAII event pair around one launch
+  Profiler &P;
+  cudaStream_t s;
+  int kc;
+  cudaEvent_t a = nullptr;
+  Timed(Profiler &p, cudaStream_t st, int k) : P(p), s(st), kc(k) {
+    if (P.on) { a = P.ev(); cudaEventRecord(a, s); }
+  }
+  ~Timed() {
+    if (P.on) {
+      cudaEvent_t b = P.ev();
+      cudaEventRecord(b, s);
+      P.pending.push_back({kc, a, b});
+      if (P.pending.size() > 4096) P.flush();
+    }
+  }
+};
+
+// ----------------------------------------------------------------- device plan
+template <typename D>
+struct StageDev {
+  int nblk = 0, cps = 1;
+  int64_t rows = 0;
+  const int64_t *blk = nullptr;
+  TriDev<D> L{}, U{};
+  int depthL = 0, depthU = 0;
+  int64_t nnz = 0;         // real stored nonzeros (L + U incl. diagonal)
+  int64_t padded = 0;      // stored entries incl. padding
+};
+
+template <typename D>
+struct CsrDev {
+  int64_t n = 0, nnz = 0;
+  const int64_t *ptr = nullptr;
+  const int32_t *col = nullptr;
+  const D *val = nullptr;
+};
+
+template <typename D>
+struct LevelDev {
+  int64_t o0 = 0, o1 = 0, s = 0;
+  StageDev<D> st;
+  CsrDev<D> E, F;
+  int k = 0;
+  D *W = nullptr;          // s x k column-major, ld = ldw
+  int64_t ldw = 0;
+  D *G = nullptr;          // k x k
+  std::vector<typename std::conditional<std::is_same<D, double>::value, double, zc>::type> Wh, Rh, Gh;  // host copies
+  int cycles = 0;
+};
+
+struct Ctx;
+
+template <typename T>
+struct Engine {
+  using D = typename Dev<T>::type;
+  Ctx *ctx = nullptr;
+  HostPlan<T> plan;
+  int64_t n = 0, nnzA = 0;
+  // SpMV (SELL-32 of Â)
+  int64_t nslices = 0, sell_padded = 0;
+  const int64_t *sell_off = nullptr;
+  const int32_t *sell_col = nullptr;
+  const D *sell_val = nullptr;
+  std::vector<LevelDev<D>> lev;
+  StageDev<D> last;
+  const int64_t *perm_d = nullptr;
+  // workspace
+  D *r = nullptr, *tmp = nullptr, *tvec = nullptr, *partial = nullptr, *res = nullptr;
+  unsigned *tickets = nullptr;
+  size_t partial_cap = 0;
+  // Krylov workspace (lazy)
+  int kry_m = -1;
+  int64_t ldv = 0;
+  D *V = nullptr, *Z = nullptr, *w = nullptr;
+  D *H = nullptr, *g = nullptr, *sn = nullptr, *ydev = nullptr;
+  double *cs = nullptr, *dbl = nullptr, *hist = nullptr;
+  int *ints = nullptr, *done = nullptr;
+  int hist_cap = 0;
+  D *xb = nullptr, *bb = nullptr;   // host-path staging
+  double setup_host_s = 0, setup_dev_s = 0, arnoldi_s = 0;
+
+  void upload(cudaStream_t s);
+  void apply_from(int l0, const D *in, D *out, const int *doneflag);
+  void spmv(const D *x, D *y, int mode, const D *b, const int *doneflag);
+  void ghat(int l, D *bufA, D *bufB);
+  void build_lowrank(const gemslr_params &prm, unsigned long long seed);
+  int solve(const D *b, D *x, double rtol, int m, int maxit, int *its, double *hist, int hcap, int *hlen, double *frel);
+  void ensure_krylov(int m, int maxit);
+  void gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv, int upd, int dot, const D *h_in, D *resv, int ticket, const int *doneflag);
+  double norm(const D *x, int64_t nn, int ticket);
+  void export_bundle(const std::string &dir) const;
+  std::string stats_json() const;
+};
+
+struct Ctx {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  void *nccl = nullptr;
+  Allocator alloc;
+  Pool pool;
+  Profiler prof;
+  std::string err;
+  int dtype = -1;
+  bool ready = false;
+  bool host_only = false;
+  int coord_dim = 0;
+  std::vector<double> coords;
+  const double *coords_src = nullptr;
+  gemslr_params params{};
+  std::unique_ptr<Engine<double>> ed;
+  std::unique_ptr<Engine<zc>> ez;
+};
+
+// ----------------------------------------------------------------- upload
+template <typename D, typename T>
+static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int cps_override) {
+  StageDev<D> d;
+  d.nblk = (int)S.blk.size() - 1;
+  d.rows = S.blk.empty() ? 0 : S.blk.back() - S.blk.front();
+  d.blk = P.upload<int64_t>(S.blk, s);
+  auto up = [&](const TriPack<T> &p) {
+    TriDev<D> t;
+    t.blk_lev = P.upload<int32_t>(p.blk_lev, s);
+    t.lev_slice = P.upload<int32_t>(p.lev_slice, s);
+    t.slice_off = P.upload<int64_t>(p.slice_off, s);
+    t.slice_row = P.upload<int32_t>(p.slice_row, s);
+    t.col = P.upload<int32_t>(p.col, s);
+    t.val = P.upload<D>(p.val, s);
+    t.diag = p.diag.empty() ? nullptr : P.upload<D>(p.diag, s);
+    return t;
+  };
+  d.L = up(S.Lp);
+  d.U = up(S.Up);
+  d.depthL = S.Lp.max_depth;
+  d.depthU = S.Up.max_depth;
+  d.nnz = S.Lp.nnz_real + S.Up.nnz_real + (int64_t)d.rows;
+  d.padded = (int64_t)S.Lp.val.size() + (int64_t)S.Up.val.size() + (int64_t)S.Up.diag.size();
+  // CTAs per block: enough to cover the average rows of one level with 8-warp CTAs,
+  // bounded by the SMs available per block and the portable cluster size.
+  int cps = 1;
+  if (cps_override > 0) cps = cps_override;
+  else if (d.nblk > 0) {
+    const double depth = std::max(1, std::max(d.depthL, d.depthU));
+    const double rows_per_level = (double)d.rows / d.nblk / depth;
+    int want = (int)std::ceil(rows_per_level / 256.0);
+    int avail = std::max(1, kNumSM / d.nblk);
+    cps = std::min(std::min(want, avail), 8);
+    int p2 = 1;
+    while (p2 * 2 <= cps) p2 *= 2;
+    cps = std::max(1, p2);
+  }
+  d.cps = std::min(cps, 8);
+  return d;
+}
+
+template <typename D, typename T>
+static CsrDev<D> upload_csr(Pool &P, cudaStream_t s, const Csr<T> &A) {
+  CsrDev<D> d;
+  d.n = A.n;
+  d.nnz = A.nnz();
+  d.ptr = P.upload<int64_t>(A.ptr, s);
+  d.col = P.upload<int32_t>(A.col, s);
+  d.val = P.upload<D>(A.val, s);
+  return d;
+}
+
+template <typename T>
+void Engine<T>::upload(cudaStream_t s) {
+  Pool &P = ctx->pool;
+  const auto &A = plan.Ahat;
+  n = A.n;
+  nnzA = A.nnz();
+  // SELL-32 of Â
+  nslices = (n + 31) / 32;
+  std::vector<int64_t> off(nslices + 1, 0);
+  for (int64_t sl = 0; sl < nslices; ++sl) {
+    int64_t w = 0;
+    for (int64_t row = sl * 32; row < std::min(n, sl * 32 + 32); ++row) w = std::max(w, A.ptr[row + 1] - A.ptr[row]);
+    off[sl + 1] = off[sl] + 32 * w;
+  }
+  sell_padded = off[nslices];
+  std::vector<int32_t> col(sell_padded, -1);
+  std::vector<T> val(sell_padded, T(0));
+  for (int64_t row = 0; row < n; ++row) {
+    const int64_t sl = row / 32, lane = row % 32;
+    for (int64_t p = A.ptr[row], e = 0; p < A.ptr[row + 1]; ++p, ++e) {
+      col[off[sl] + 32 * e + lane] = A.col[p];
+      val[off[sl] + 32 * e + lane] = A.val[p];
+    }
+  }
+  sell_off = P.upload<int64_t>(off, s);
+  sell_col = P.upload<int32_t>(col, s);
+  sell_val = P.upload<D>(val, s);
+  perm_d = P.upload<int64_t>(plan.st.perm, s);
+  const int L = plan.st.L;
+  lev.resize(L);
+  for (int l = 0; l < L; ++l) {
+    LevelDev<D> &d = lev[l];
+    d.o0 = plan.st.o[l];
+    d.o1 = plan.st.o[l + 1];
+    d.s = n - d.o1;
+    d.st = upload_stage<D>(P, s, plan.stage[l], ctx->params.cluster_ctas);
+    d.E = upload_csr<D>(P, s, plan.E[l]);
+    d.F = upload_csr<D>(P, s, plan.F[l]);
+  }
+  last = upload_stage<D>(P, s, plan.last_stage, ctx->params.cluster_ctas);
+  r = P.get<D>(n + 1);
+  tmp = P.get<D>(n + 1);
+  tvec = P.get<D>(64 * 8);
+  partial_cap = (size_t)kNumSM * 8 * (GS_MAXC + 2);
+  partial = P.get<D>(partial_cap);
+  res = P.get<D>(4 * (GS_MAXC + 2));
+  tickets = P.get<unsigned>(16);
+  CK(cudaMemsetAsync(tickets, 0, 16 * sizeof(unsigned), s));
+  CK(cudaMemsetAsync(r, 0, (n + 1) * sizeof(D), s));
+  CK(cudaMemsetAsync(tmp, 0, (n + 1) * sizeof(D), s));
+}
+
+// ----------------------------------------------------------------- launches
+template <typename D>
+static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *rhs, D *x, D *tmp,
+                            const CsrDev<D> *F, int64_t Fbase, const int *doneflag, int kc) {
+  if (S.nblk <= 0 || S.rows == 0) return;
+  Timed t(ctx->prof, ctx->stream, kc);
+  const int64_t *Fp = F ? F->ptr : nullptr;
+  const int32_t *Fc = F ? F->col : nullptr;
+  const D *Fv = F ? F->val : nullptr;
+  if (S.cps <= 1) {
+    k_trisolve<D, false><<<S.nblk, 256, 0, ctx->stream>>>(S.L, S.U, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(S.nblk * S.cps);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = S.cps;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_trisolve<D, true>, S.L, S.U, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag));
+  }
+  CK(cudaGetLastError());
+}
+
+static int grid_for(int64_t units, int per_sm) {
+  int64_t g = std::min<int64_t>(units, (int64_t)kNumSM * per_sm);
+  return (int)std::max<int64_t>(g, 1);
+}
+
+template <typename T>
+void Engine<T>::spmv(const D *x, D *y, int mode, const D *b, const int *doneflag) {
+  Timed t(ctx->prof, ctx->stream, KC_SPMV);
+  const int grid = (int)((nslices + 7) / 8);
+  k_spmv_sell<D><<<std::max(grid, 1), 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, y, mode, b, doneflag);
+  CK(cudaGetLastError());
+}
+
+// Alg. 2, single pass, from level l0: input `in` and output `out`
+// are full-length vectors of which positions [o_{l0}, N) are used.
+template <typename T>
+void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
+  const int L = (int)lev.size();
+  cudaStream_t s = ctx->stream;
+  for (int l = l0; l < L; ++l) {
+    LevelDev<D> &d = lev[l];
+    const D *src = (l == l0) ? in : r;
+    // z1 = U_l^-1 L_l^-1 b1  -> out[I_l]
+    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, (const CsrDev<D> *)nullptr, 0, doneflag, KC_TRI_DOWN);
+    if (d.s > 0) {
+      // z2 = b2 - E_l z1 ; s = W^H z2 ; t = G s
+      {
+        Timed t(ctx->prof, s, KC_EW);
+        const int grid = grid_for((d.s + 255) / 256, 4);
+        k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, out, src, r, d.W, d.ldw, d.k, partial,
+                                     tickets + 0, d.G, tvec, doneflag);
+        CK(cudaGetLastError());
+      }
+      if (d.k > 0) {                                              // u2 + z2
+        Timed t(ctx->prof, s, KC_WAXPY);
+        const int grid = grid_for((d.s + 255) / 256, 8);
+        k_waxpy<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.W, d.ldw, d.k, tvec, r, doneflag);
+        CK(cudaGetLastError());
+      }
+    }
+  }
+  // bottom: C_{L-1}^{-1} by block-Jacobi ILU
+  const D *src = (l0 == L) ? in : r;
+  launch_trisolve(ctx, last, TRI_DOWN, src, out, tmp, (const CsrDev<D> *)nullptr, 0, doneflag, KC_TRI_LAST);
+  // up: y1 = z1 - U^-1 L^-1 F_l y2
+  for (int l = L - 1; l >= l0; --l) {
+    LevelDev<D> &d = lev[l];
+    launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, &d.F, d.o0, doneflag, KC_TRI_UP);
+  }
+}
+
+// Ĝ_l v = E_l (L_l U_l)^{-1} F_l C_l^{-1} v.  bufA[J_l] holds v
+// on entry; on exit bufB[J_l] = Ĝ_l v.  bufA is used as scratch.
+template <typename T>
+void Engine<T>::ghat(int l, D *bufA, D *bufB) {
+  LevelDev<D> &d = lev[l];
+  cudaStream_t s = ctx->stream;
+  // c = C_l^{-1} v  -> bufB[J_l]
+  apply_from(l + 1, bufA, bufB, nullptr);
+  // bufB[I_l] = 0 - U^-1 L^-1 F_l c = -u
+  CK(cudaMemsetAsync(bufB + d.o0, 0, (d.o1 - d.o0) * sizeof(D), s));
+  launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, bufB, tmp, &d.F, d.o0, nullptr, KC_TRI_UP);
+  // bufB[J_l] = 0 - E_l (-u) = E_l u   (k = 0 mode of K6+K7, src = 0)
+  const int grid = grid_for((d.s + 255) / 256, 4);
+  k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, bufB, (const D *)nullptr, bufB, (const D *)nullptr, 0,
+                               0, partial, tickets + 1, (const D *)nullptr, tvec, nullptr);
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv, int upd, int dot, const D *h_in,
+                        D *resv, int ticket, const int *doneflag) {
+  Timed t(ctx->prof, ctx->stream, KC_GS);
+  const int grid = grid_for((nn + 31) / 32, 4);
+  k_gs<D><<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv, doneflag);
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+double Engine<T>::norm(const D *x, int64_t nn, int ticket) {
+  gs_pass(nullptr, 0, nn, 0, const_cast<D *>(x), 0, 0, nullptr, res, ticket, nullptr);
+  D h;
+  CK(cudaMemcpyAsync(&h, res, sizeof(D), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double v;
+  if constexpr (std::is_same<D, double>::value) v = h; else v = h.x;
+  return std::sqrt(std::max(v, 0.0));
+}
+
+// ----------------------------------------------------------------- small dense helpers (host)
+template <typename S>
+static bool inverse_small(int k, std::vector<S> &A) {    // Gauss-Jordan with partial pivoting, column-major
+  std::vector<S> I((size_t)k * k, S(0));
+  for (int i = 0; i < k; ++i) I[(size_t)i * k + i] = S(1);
+  auto at = [&](std::vector<S> &M, int i, int j) -> S & { return M[(size_t)j * k + i]; };
+  for (int c = 0; c < k; ++c) {
+    int piv = c;
+    for (int i = c + 1; i < k; ++i)
+      if (absval(at(A, i, c)) > absval(at(A, piv, c))) piv = i;
+    if (absval(at(A, piv, c)) == 0.0) return false;
+    if (piv != c)
+      for (int j = 0; j < k; ++j) { std::swap(at(A, c, j), at(A, piv, j)); std::swap(at(I, c, j), at(I, piv, j)); }
+    const S d = at(A, c, c);
+    for (int j = 0; j < k; ++j) { at(A, c, j) /= d; at(I, c, j) /= d; }
+    for (int i = 0; i < k; ++i) {
+      if (i == c) continue;
+      const S f = at(A, i, c);
+      if (f == S(0)) continue;
+      for (int j = 0; j < k; ++j) { at(A, i, j) -= f * at(A, c, j); at(I, i, j) -= f * at(I, c, j); }
+    }
+  }
+  A.swap(I);
+  return true;
+}
+
+// ----------------------------------------------------------------- low rank (Arnoldi)
+// Thick-restart (Krylov-Schur) Arnoldi on Ĝ_l, cycle length m = 2k,
+// CGS2 orthogonalisation, Schur form of the projected matrix reordered so the
+// k Ritz values with the largest |γ/(1-γ)| lead (
+// reading Q6), converged when they change by < tol relatively between cycles
+// (reading Q8).  Real A keeps a real basis: the selected set is
+// closed under conjugation (a split pair takes k+1, reading Q7) and its
+// invariant subspace gets a real orthonormal basis.  W = V Y, R = Y^H H Y,
+// G = (I - R)^{-1} - I.  Built bottom-up l = L-1 .. 0.
+template <typename T>
+void Engine<T>::build_lowrank(const gemslr_params &prm, unsigned long long seed) {
+  const int L = (int)lev.size();
+  cudaStream_t s = ctx->stream;
+  const bool is_real = std::is_same<T, double>::value;
+  const double tol = prm.arnoldi_tol > 0 ? prm.arnoldi_tol : 1e-2;
+  const int maxcyc = prm.arnoldi_max_cycles > 0 ? prm.arnoldi_max_cycles : 10;
+  D *bufA = ctx->pool.get<D>(n + 1);
+  D *bufB = ctx->pool.get<D>(n + 1);
+  CK(cudaMemsetAsync(bufA, 0, (n + 1) * sizeof(D), s));
+  CK(cudaMemsetAsync(bufB, 0, (n + 1) * sizeof(D), s));
+  D *hres = ctx->pool.get<D>(3 * (GS_MAXC + 2));
+  for (int l = L - 1; l >= 0; --l) {
+    LevelDev<D> &d = lev[l];
+    const int64_t sl = d.s;
+    int k = prm.rank;
+    if (k <= 0 || sl == 0) { d.k = 0; continue; }
+    if (k > sl) k = (int)sl;
+    int m = std::min<int64_t>(2 * (int64_t)k, sl);
+    if (m < k + 1 && m < sl) m = k + 1;
+    if (m + 1 > GS_MAXC) throw Error{GEMSLR_ERR_INVALID_ARG, "rank too large for the Arnoldi workspace (2k+1 > 104)"};
+    const int64_t ld = (sl + 31) / 32 * 32;
+    D *Vb = ctx->pool.get<D>((size_t)ld * (m + 1));
+    D *Wt = ctx->pool.get<D>((size_t)ld * (k + 2));
+    D *Yd = ctx->pool.get<D>((size_t)m * (k + 2));
+    // start vector: uniform[-1,1] from the seed (reading Q8), normalised
+    std::mt19937_64 rng(seed + 7919ull * (unsigned long long)(l + 1));
+    std::uniform_real_distribution<double> U(-1.0, 1.0);
+    std::vector<T> v0(sl);
+    for (auto &e : v0) {
+      if constexpr (std::is_same<T, double>::value) e = U(rng); else e = zc(U(rng), U(rng));
+    }
+    CK(cudaMemcpyAsync(Vb, v0.data(), sl * sizeof(D), cudaMemcpyHostToDevice, s));
+    double nv = norm(Vb, sl, 2);
+    if (nv == 0.0) throw Error{GEMSLR_ERR_LOWRANK, "Arnoldi start vector is zero"};
+    {
+      std::vector<double> inv{1.0 / nv};
+      double *dsc = ctx->pool.get<double>(1);
+      CK(cudaMemcpyAsync(dsc, inv.data(), sizeof(double), cudaMemcpyHostToDevice, s));
+      k_scale<D><<<grid_for((sl + 255) / 256, 4), 256, 0, s>>>(sl, Vb, Vb, dsc, nullptr);
+    }
+    // H: (m+1) x m host, column-major
+    std::vector<zc> H((size_t)(m + 1) * m, zc(0));
+    auto Hat = [&](int i, int j) -> zc & { return H[(size_t)j * (m + 1) + i]; };
+    int j0 = 0, cyc = 0, kk = 0;
+    std::vector<zc> prev_sel;
+    std::vector<zc> Yh, Rk;
+    bool converged = false;
+    double *dscale = ctx->pool.get<double>(1);
+    while (true) {
+      ++cyc;
+      int mm = m;
+      bool breakdown = false;
+      double hlast = 0;
+      for (int j = j0; j < m; ++j) {
+        D *vj = Vb + (size_t)j * ld;
+        CK(cudaMemcpyAsync(bufA + d.o1, vj, sl * sizeof(D), cudaMemcpyDeviceToDevice, s));
+        ghat(l, bufA, bufB);
+        D *wv = bufB + d.o1;
+        gs_pass(Vb, ld, sl, j + 1, wv, 0, 1, nullptr, hres, 3, nullptr);
+        gs_pass(Vb, ld, sl, j + 1, wv, 1, 1, hres, hres + (GS_MAXC + 2), 4, nullptr);
+        gs_pass(Vb, ld, sl, j + 1, wv, 1, 0, hres + (GS_MAXC + 2), hres + 2 * (GS_MAXC + 2), 5, nullptr);
+        std::vector<T> hh(3 * (GS_MAXC + 2));
+        CK(cudaMemcpyAsync(hh.data(), hres, hh.size() * sizeof(D), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const double eta = std::sqrt(std::max(0.0, std::real(zc(hh[j + 1]))));
+        const double hn = std::sqrt(std::max(0.0, std::real(zc(hh[2 * (GS_MAXC + 2)]))));
+        for (int i = 0; i <= j; ++i) Hat(i, j) = zc(hh[i]) + zc(hh[(GS_MAXC + 2) + i]);
+        Hat(j + 1, j) = hn;
+        hlast = hn;
+        if (!(hn > 1e-14 * eta) || !std::isfinite(hn)) { mm = j + 1; breakdown = true; break; }
+        const double inv = 1.0 / hn;
+        CK(cudaMemcpyAsync(dscale, &inv, sizeof(double), cudaMemcpyHostToDevice, s));
+        k_scale<D><<<grid_for((sl + 255) / 256, 4), 256, 0, s>>>(sl, wv, Vb + (size_t)(j + 1) * ld, dscale, nullptr);
+        CK(cudaStreamSynchronize(s));
+      }
+      // Schur of the mm x mm projected matrix
+      std::vector<zc> Hm((size_t)mm * mm), Tm((size_t)mm * mm), Q((size_t)mm * mm);
+      for (int j = 0; j < mm; ++j)
+        for (int i = 0; i < mm; ++i) Hm[(size_t)j * mm + i] = Hat(i, j);
+      if (!schur_complex(mm, Hm.data(), Tm.data(), Q.data()))
+        throw Error{GEMSLR_ERR_LOWRANK, "Schur iteration did not converge at level " + std::to_string(l)};
+      // select the k largest |γ/(1-γ)|
+      std::vector<int> idx(mm);
+      std::vector<double> key(mm);
+      for (int i = 0; i < mm; ++i) {
+        const zc gm = Tm[(size_t)i * mm + i];
+        key[i] = std::abs(gm / (zc(1.0) - gm));
+        idx[i] = i;
+      }
+      std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return key[a] > key[b]; });
+      int want = std::min(k, mm);
+      std::vector<char> sel(mm, 0);
+      for (int i = 0; i < want; ++i) sel[idx[i]] = 1;
+      if (is_real) {                                    // never split a conjugate pair (Q7)
+        for (int i = 0; i < mm; ++i) {
+          if (!sel[i]) continue;
+          const zc gi = Tm[(size_t)i * mm + i];
+          if (std::abs(gi.imag()) <= 1e-12 * std::max(1.0, std::abs(gi))) continue;
+          int best = -1;
+          double bd = 1e300;
+          for (int q = 0; q < mm; ++q) {
+            if (q == i) continue;
+            double dd = std::abs(Tm[(size_t)q * mm + q] - std::conj(gi));
+            if (dd < bd) { bd = dd; best = q; }
+          }
+          if (best >= 0 && !sel[best] && bd <= 1e-6 * std::max(1.0, std::abs(gi))) sel[best] = 1;
+        }
+      }
+      for (int i = 0; i < mm; ++i)
+        if (sel[i] && std::abs(zc(1.0) - Tm[(size_t)i * mm + i]) < 1e-12)
+          throw Error{GEMSLR_ERR_LOWRANK, "Ritz value within 1e-12 of 1 at level " + std::to_string(l)};
+      schur_reorder(mm, Tm.data(), Q.data(), sel);
+      int ks = 0;
+      for (char c : sel) ks += c;
+      // convergence of the selected Ritz values (sorted by key)
+      std::vector<zc> cur(ks);
+      for (int i = 0; i < ks; ++i) cur[i] = Tm[(size_t)i * mm + i];
+      std::sort(cur.begin(), cur.end(), [](const zc &a, const zc &b) {
+        double ka = std::abs(a / (zc(1.0) - a)), kb = std::abs(b / (zc(1.0) - b));
+        if (ka != kb) return ka > kb;
+        if (a.real() != b.real()) return a.real() < b.real();
+        return a.imag() < b.imag();
+      });
+      if (!prev_sel.empty() && prev_sel.size() == cur.size()) {
+        double worst = 0;
+        for (int i = 0; i < ks; ++i) worst = std::max(worst, std::abs(cur[i] - prev_sel[i]) / std::max(std::abs(cur[i]), 1e-300));
+        converged = worst < tol;
+      }
+      if (breakdown || mm <= ks) converged = true;
+      prev_sel = cur;
+      // basis Y (mm x kk) of the selected invariant subspace
+      std::vector<zc> Yc((size_t)mm * ks);
+      for (int c = 0; c < ks; ++c)
+        for (int i = 0; i < mm; ++i) Yc[(size_t)c * mm + i] = Q[(size_t)c * mm + i];
+      if (is_real) {                                    // real orthonormal basis of span(Y)
+        std::vector<std::vector<double>> cand;
+        for (int c = 0; c < ks; ++c) {
+          std::vector<double> re(mm), im(mm);
+          for (int i = 0; i < mm; ++i) { re[i] = Yc[(size_t)c * mm + i].real(); im[i] = Yc[(size_t)c * mm + i].imag(); }
+          cand.push_back(re);
+          cand.push_back(im);
+        }
+        std::vector<std::vector<double>> basis;
+        for (auto &v : cand) {
+          double n0 = 0;
+          for (double e : v) n0 += e * e;
+          n0 = std::sqrt(n0);
+          if (n0 == 0) continue;
+          for (int pass = 0; pass < 2; ++pass)
+            for (auto &b : basis) {
+              double dd = 0;
+              for (int i = 0; i < mm; ++i) dd += b[i] * v[i];
+              for (int i = 0; i < mm; ++i) v[i] -= dd * b[i];
+            }
+          double n1 = 0;
+          for (double e : v) n1 += e * e;
+          n1 = std::sqrt(n1);
+          if (n1 <= 1e-8 * n0) continue;
+          for (double &e : v) e /= n1;
+          basis.push_back(v);
+          if ((int)basis.size() == ks) break;
+        }
+        if ((int)basis.size() != ks) throw Error{GEMSLR_ERR_LOWRANK, "real invariant-subspace basis is rank deficient"};
+        for (int c = 0; c < ks; ++c)
+          for (int i = 0; i < mm; ++i) Yc[(size_t)c * mm + i] = zc(basis[c][i], 0.0);
+      }
+      kk = ks;
+      // Rk = Y^H H_mm Y
+      Rk.assign((size_t)kk * kk, zc(0));
+      {
+        std::vector<zc> HY((size_t)mm * kk, zc(0));
+        for (int c = 0; c < kk; ++c)
+          for (int j = 0; j < mm; ++j) {
+            const zc y = Yc[(size_t)c * mm + j];
+            if (y == zc(0)) continue;
+            for (int i = 0; i < mm; ++i) HY[(size_t)c * mm + i] += Hm[(size_t)j * mm + i] * y;
+          }
+        for (int c = 0; c < kk; ++c)
+          for (int a = 0; a < kk; ++a) {
+            zc acc = 0;
+            for (int i = 0; i < mm; ++i) acc += std::conj(Yc[(size_t)a * mm + i]) * HY[(size_t)c * mm + i];
+            Rk[(size_t)c * kk + a] = acc;
+          }
+      }
+      Yh = Yc;
+      // W (or the restarted basis) = V_mm Y  -> Wt
+      {
+        std::vector<T> Yt((size_t)mm * kk);
+        for (size_t i = 0; i < Yt.size(); ++i) {
+          if constexpr (std::is_same<T, double>::value) Yt[i] = Yc[i].real(); else Yt[i] = Yc[i];
+        }
+        CK(cudaMemcpyAsync(Yd, Yt.data(), Yt.size() * sizeof(D), cudaMemcpyHostToDevice, s));
+        k_gemm_tall<D><<<grid_for((sl + 255) / 256, 4), 256, 0, s>>>(sl, Vb, ld, mm, Yd, kk, Wt, ld);
+        CK(cudaGetLastError());
+      }
+      if (converged || cyc >= maxcyc) break;
+      // thick restart: V[:, 0:kk] = V Y ; V[:, kk] = v_{m+1} ; H = [Rk ; hlast * Y[mm-1, :]]
+      CK(cudaMemcpyAsync(Vb, Wt, (size_t)ld * kk * sizeof(D), cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(Vb + (size_t)kk * ld, Vb + (size_t)mm * ld, sl * sizeof(D), cudaMemcpyDeviceToDevice, s));
+      std::fill(H.begin(), H.end(), zc(0));
+      for (int c = 0; c < kk; ++c) {
+        for (int a = 0; a < kk; ++a) Hat(a, c) = Rk[(size_t)c * kk + a];
+        Hat(kk, c) = hlast * Yc[(size_t)c * mm + (mm - 1)];
+      }
+      j0 = kk;
+      CK(cudaStreamSynchronize(s));
+    }
+    CK(cudaStreamSynchronize(s));
+    d.cycles = cyc;
+    d.k = kk;
+    d.ldw = ld;
+    d.W = Wt;
+    // G = (I - Rk)^{-1} - I
+    using S = typename std::conditional<std::is_same<T, double>::value, double, zc>::type;
+    std::vector<S> IR((size_t)kk * kk), Rs((size_t)kk * kk);
+    for (int c = 0; c < kk; ++c)
+      for (int a = 0; a < kk; ++a) {
+        zc v = Rk[(size_t)c * kk + a];
+        S sv;
+        if constexpr (std::is_same<S, double>::value) sv = v.real(); else sv = v;
+        Rs[(size_t)c * kk + a] = sv;
+        IR[(size_t)c * kk + a] = (a == c ? S(1) : S(0)) - sv;
+      }
+    if (!inverse_small(kk, IR)) throw Error{GEMSLR_ERR_LOWRANK, "I - R singular at level " + std::to_string(l)};
+    for (int a = 0; a < kk; ++a) IR[(size_t)a * kk + a] -= S(1);
+    d.Gh = IR;
+    d.Rh = Rs;
+    d.G = ctx->pool.upload<D>(IR, s);
+    // host copy of W for export
+    d.Wh.assign((size_t)sl * kk, S(0));
+    for (int c = 0; c < kk; ++c)
+      CK(cudaMemcpyAsync(d.Wh.data() + (size_t)c * sl, Wt + (size_t)c * ld, sl * sizeof(D), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+}
+
+// ----------------------------------------------------------------- FGMRES
+template <typename T>
+void Engine<T>::ensure_krylov(int m, int maxit) {
+  if (kry_m >= m && hist_cap >= maxit + 1) return;
+  Pool &P = ctx->pool;
+  ldv = (n + 31) / 32 * 32;
+  if (kry_m < m) {
+    V = P.get<D>((size_t)ldv * (m + 1));
+    Z = P.get<D>((size_t)ldv * m);
+    w = P.get<D>(n + 1);
+    H = P.get<D>((size_t)(m + 1) * m);
+    g = P.get<D>(m + 1);
+    sn = P.get<D>(m);
+    cs = P.get<double>(m);
+    ydev = P.get<D>(m + 1);
+    dbl = P.get<double>(8);
+    ints = P.get<int>(8);
+    done = P.get<int>(2);
+    kry_m = m;
+  }
+  if (hist_cap < maxit + 1) {
+    hist = P.get<double>(maxit + 2);
+    hist_cap = maxit + 1;
+  }
+}
+
+// Right-preconditioned FGMRES(m) with CGS2 (c5 of DESIGN.md).
+template <typename T>
+int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_out, double *hist_out, int hcap,
+                     int *hlen, double *frel) {
+  cudaStream_t s = ctx->stream;
+  if (m + 1 > GS_MAXC) throw Error{GEMSLR_ERR_INVALID_ARG, "restart must be <= 103"};
+  ensure_krylov(m, maxit);
+  std::vector<double> hh;
+  const double bnorm = norm(b, n, 6);
+  int its = 0;
+  if (bnorm == 0.0) {
+    k_fill<D><<<grid_for((n + 255) / 256, 4), 256, 0, s>>>(n, x, dzero<D>());
+    if (hist_out && hcap > 0) hist_out[0] = 0.0;
+    if (hlen) *hlen = 1;
+    if (its_out) *its_out = 0;
+    if (frel) *frel = 0.0;
+    CK(cudaStreamSynchronize(s));
+    return GEMSLR_OK;
+  }
+  // r = b - A x
+  spmv(x, w, 1, b, nullptr);
+  double beta = norm(w, n, 6);
+  hh.push_back(beta / bnorm);
+  double *dsc = dbl + 4;
+  FgmDev<D> f{done, ints, dbl, hist, H, g, cs, sn};
+  while (beta > rtol * bnorm && its < maxit) {
+    // V0 = r / beta ; g = (beta, 0, ...) ; state
+    {
+      double hv[8] = {bnorm, rtol, 0, 0, 1.0 / beta, 0, 0, 0};
+      int iv[4] = {0, its, maxit, 0};
+      CK(cudaMemcpyAsync(dbl, hv, sizeof(hv), cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(ints, iv, sizeof(iv), cudaMemcpyHostToDevice, s));
+      CK(cudaMemsetAsync(done, 0, 2 * sizeof(int), s));
+      std::vector<D> g0(m + 1, dzero<D>());
+      if constexpr (std::is_same<D, double>::value) g0[0] = beta; else g0[0] = D{beta, 0.0};
+      CK(cudaMemcpyAsync(g, g0.data(), (m + 1) * sizeof(D), cudaMemcpyHostToDevice, s));
+      CK(cudaMemsetAsync(H, 0, (size_t)(m + 1) * m * sizeof(D), s));
+      Timed t(ctx->prof, s, KC_UTIL);
+      k_scale<D><<<grid_for((n + 255) / 256, 4), 256, 0, s>>>(n, w, V, dsc, nullptr);
+    }
+    D *res1 = res, *res2 = res + (GS_MAXC + 2), *res3 = res + 2 * (GS_MAXC + 2);
+    std::vector<cudaEvent_t> evs;
+    int j = 0;
+    for (j = 0; j < m; ++j) {
+      D *vj = V + (size_t)j * ldv;
+      D *zj = Z + (size_t)j * ldv;
+      apply_from(0, vj, zj, done);                                // Z_j = M^{-1} V_j
+      spmv(zj, w, 0, nullptr, done);                              // w = A Z_j
+      gs_pass(V, ldv, n, j + 1, w, 0, 1, nullptr, res1, 7, done); // h = V^H w, ||w||^2
+      gs_pass(V, ldv, n, j + 1, w, 1, 1, res1, res2, 8, done);    // w -= V h ; h2 = V^H w
+      gs_pass(V, ldv, n, j + 1, w, 1, 0, res2, res3, 9, done);    // w -= V h2 ; ||w||^2
+      {
+        Timed t(ctx->prof, s, KC_FGM);
+        k_fgmres_col<D><<<1, 32, 0, s>>>(f, m, j, res1, res2, res3);
+        CK(cudaGetLastError());
+      }
+      {
+        Timed t(ctx->prof, s, KC_UTIL);
+        k_scale<D><<<grid_for((n + 255) / 256, 4), 256, 0, s>>>(n, w, V + (size_t)(j + 1) * ldv, dbl + 2, done);
+      }
+      // keep at most 2 iterations in flight so the host notices convergence
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, s));
+      evs.push_back(e);
+      if (j >= 2) {
+        CK(cudaEventSynchronize(evs[j - 2]));
+        int dflag = 0;
+        CK(cudaMemcpy(&dflag, done, sizeof(int), cudaMemcpyDeviceToHost));
+        if (dflag) break;
+      }
+    }
+    CK(cudaStreamSynchronize(s));
+    for (auto e : evs) cudaEventDestroy(e);
+    if (ctx->prof.on) ctx->prof.flush();
+    int iv[4];
+    CK(cudaMemcpy(iv, ints, sizeof(iv), cudaMemcpyDeviceToHost));
+    const int jend = iv[0];
+    const int its_new = iv[1];
+    std::vector<double> hcyc(its_new - its);
+    if (its_new > its) CK(cudaMemcpy(hcyc.data(), hist + its + 1, (its_new - its) * sizeof(double), cudaMemcpyDeviceToHost));
+    for (double v : hcyc) hh.push_back(v);
+    its = its_new;
+    // y = H[0:jend,0:jend]^{-1} g  (upper triangular after the rotations; host)
+    std::vector<T> Hh((size_t)(m + 1) * m), gh(m + 1), y(jend);
+    CK(cudaMemcpy(Hh.data(), H, Hh.size() * sizeof(D), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(gh.data(), g, gh.size() * sizeof(D), cudaMemcpyDeviceToHost));
+    for (int i = jend - 1; i >= 0; --i) {
+      T acc = gh[i];
+      for (int c = i + 1; c < jend; ++c) acc -= Hh[(size_t)c * (m + 1) + i] * y[c];
+      y[i] = acc / Hh[(size_t)i * (m + 1) + i];
+    }
+    if (jend > 0) {
+      CK(cudaMemcpyAsync(ydev, y.data(), jend * sizeof(D), cudaMemcpyHostToDevice, s));
+      Timed t(ctx->prof, s, KC_UTIL);
+      k_xupdate<D><<<grid_for((n + 255) / 256, 4), 256, 0, s>>>(n, Z, ldv, jend, ydev, x);   // x += Z y
+      CK(cudaGetLastError());
+    }
+    spmv(x, w, 1, b, nullptr);                                    // explicit r = b - A x
+    beta = norm(w, n, 6);
+    if (jend == 0) break;
+  }
+  if (its_out) *its_out = its;
+  const int hl = (int)hh.size();
+  if (hlen) *hlen = std::min(hl, hcap);
+  if (hist_out)
+    for (int i = 0; i < hl && i < hcap; ++i) hist_out[i] = hh[i];
+  if (frel) *frel = beta / bnorm;
+  return beta > rtol * bnorm ? GEMSLR_NOT_CONVERGED : GEMSLR_OK;
+}
+
+// ----------------------------------------------------------------- bundle export
+static void write_bin(const std::string &path, const void *p, size_t bytes) {
+  FILE *f = std::fopen(path.c_str(), "wb");
+  if (!f) throw Error{GEMSLR_ERR_INVALID_ARG, "cannot write " + path};
+  if (bytes) std::fwrite(p, 1, bytes, f);
+  std::fclose(f);
+}
+
+template <typename T>
+void Engine<T>::export_bundle(const std::string &dir) const {
+  mkdir(dir.c_str(), 0755);
+  std::string man = "{\n";
+  const char *vt = std::is_same<T, double>::value ? "float64" : "complex128";
+  auto add = [&](const std::string &name, const char *dt, const void *p, size_t count, size_t esz, std::vector<int64_t> shape) {
+    write_bin(dir + "/" + name + ".bin", p, count * esz);
+    man += "  \"" + name + "\": {\"dtype\": \"" + dt + "\", \"shape\": [";
+    for (size_t i = 0; i < shape.size(); ++i) man += (i ? ", " : "") + std::to_string(shape[i]);
+    man += "]},\n";
+  };
+  const Structure &st = plan.st;
+  add("perm", "int64", st.perm.data(), st.perm.size(), 8, {(int64_t)st.perm.size()});
+  add("level_off", "int64", st.o.data(), st.o.size(), 8, {(int64_t)st.o.size()});
+  for (int l = 0; l < st.L; ++l)
+    add("blocks_" + std::to_string(l), "int64", st.blk[l].data(), st.blk[l].size(), 8, {(int64_t)st.blk[l].size()});
+  add("last_off", "int64", st.last.data(), st.last.size(), 8, {(int64_t)st.last.size()});
+  auto facs = [&](const std::string &tag, const std::vector<Factor<T>> &F) {
+    for (int which = 0; which < 2; ++which) {
+      std::vector<int64_t> ptr, nnzoff{0};
+      std::vector<int32_t> col;
+      std::vector<T> val;
+      for (auto &f : F) {
+        const Csr<T> &M = which ? f.U : f.L;
+        ptr.insert(ptr.end(), M.ptr.begin(), M.ptr.end());
+        col.insert(col.end(), M.col.begin(), M.col.end());
+        val.insert(val.end(), M.val.begin(), M.val.end());
+        nnzoff.push_back((int64_t)col.size());
+      }
+      const std::string b = tag + (which ? "_U" : "_L");
+      add(b + "_ptr", "int64", ptr.data(), ptr.size(), 8, {(int64_t)ptr.size()});
+      add(b + "_col", "int32", col.data(), col.size(), 4, {(int64_t)col.size()});
+      add(b + "_val", vt, val.data(), val.size(), sizeof(T), {(int64_t)val.size()});
+      add(b + "_nnzoff", "int64", nnzoff.data(), nnzoff.size(), 8, {(int64_t)nnzoff.size()});
+    }
+  };
+  for (int l = 0; l < st.L; ++l) facs("fac" + std::to_string(l), plan.fac[l]);
+  facs("faclast", plan.lastfac);
+  std::string ranks = "[";
+  for (int l = 0; l < (int)lev.size(); ++l) {
+    const auto &d = lev[l];
+    ranks += (l ? ", " : "") + std::to_string(d.k);
+    if (d.k > 0) {
+      add("W_" + std::to_string(l), vt, d.Wh.data(), d.Wh.size(), sizeof(T), {(int64_t)d.k, d.s});
+      add("R_" + std::to_string(l), vt, d.Rh.data(), d.Rh.size(), sizeof(T), {(int64_t)d.k, (int64_t)d.k});
+      add("G_" + std::to_string(l), vt, d.Gh.data(), d.Gh.size(), sizeof(T), {(int64_t)d.k, (int64_t)d.k});
+    }
+  }
+  ranks += "]";
+  const gemslr_params &p = ctx->params;
+  man += "  \"meta\": {\"n\": " + std::to_string(n) + ", \"levels\": " + std::to_string(st.L) + ", \"dtype\": \"" + vt +
+         "\", \"ilu\": " + std::to_string(p.ilu) + ", \"ilut_drop\": " + std::to_string(p.ilut_drop) +
+         ", \"ilut_fill\": " + std::to_string(p.ilut_fill) + ", \"ranks\": " + ranks + "}\n}\n";
+  write_bin(dir + "/manifest.json", man.data(), man.size());
+}
+
+template <typename T>
+std::string Engine<T>::stats_json() const {
+  const Structure &st = plan.st;
+  std::string j = "{";
+  j += "\"n\": " + std::to_string(plan.Ahat.n) + ", \"nnz\": " + std::to_string(plan.Ahat.nnz());
+  j += ", \"levels\": " + std::to_string(st.L);
+  j += ", \"level_off\": [";
+  for (size_t i = 0; i < st.o.size(); ++i) j += (i ? ", " : "") + std::to_string(st.o[i]);
+  j += "], \"fill\": " + std::to_string((double)plan.fac_nnz / std::max<int64_t>(1, plan.Ahat.nnz()));
+  j += ", \"fac_nnz\": " + std::to_string(plan.fac_nnz);
+  j += ", \"sell_padded\": " + std::to_string(sell_padded);
+  auto stage = [&](const StageDev<D> &S) {
+    return "{\"blocks\": " + std::to_string(S.nblk) + ", \"rows\": " + std::to_string(S.rows) + ", \"cps\": " +
+           std::to_string(S.cps) + ", \"depth_L\": " + std::to_string(S.depthL) + ", \"depth_U\": " +
+           std::to_string(S.depthU) + ", \"nnz\": " + std::to_string(S.nnz) + ", \"padded\": " + std::to_string(S.padded) + "}";
+  };
+  j += ", \"stages\": [";
+  for (size_t l = 0; l < lev.size(); ++l) {
+    const auto &d = lev[l];
+    j += (l ? ", " : "") + std::string("{\"stage\": ") + stage(d.st) + ", \"s\": " + std::to_string(d.s) + ", \"k\": " +
+         std::to_string(d.k) + ", \"cycles\": " + std::to_string(d.cycles) + ", \"nnzE\": " + std::to_string(d.E.nnz) +
+         ", \"nnzF\": " + std::to_string(d.F.nnz) + "}";
+  }
+  j += "], \"last\": " + stage(last);
+  j += ", \"setup_host_s\": " + std::to_string(setup_host_s) + ", \"setup_device_s\": " + std::to_string(setup_dev_s) +
+       ", \"arnoldi_s\": " + std::to_string(arnoldi_s);
+  j += ", \"device_bytes\": " + std::to_string(ctx->pool.bytes);
+  j += ", \"kernels\": {";
+  bool first = true;
+  for (int k = 0; k < KC_COUNT; ++k) {
+    if (!first) j += ", ";
+    first = false;
+    j += "\"" + std::string(kKernelName[k]) + "\": {\"ms\": " + std::to_string(ctx->prof.ms[k]) + ", \"count\": " +
+         std::to_string(ctx->prof.count[k]) + "}";
+  }
+  j += "}}";
+  return j;
+}
+
+template struct Engine<double>;
+template struct Engine<zc>;
+
+}  // namespace gemslr
+
+// =================================================================== C-ABI
+using namespace gemslr;
+
+struct gemslr_ctx : public Ctx {};
+
+static gemslr_status fail(const gemslr_ctx *c, int code, const std::string &msg) {
+  if (c) const_cast<gemslr_ctx *>(c)->err = msg;
+  return (gemslr_status)code;
+}
+
+template <typename F>
+static gemslr_status guarded(gemslr_ctx *c, F &&fn) {
+  try {
+    if (c && c->device >= 0) {
+      cudaError_t e = cudaSetDevice(c->device);
+      if (e != cudaSuccess) return fail(c, GEMSLR_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    }
+    return fn();
+  } catch (const Error &e) {
+    return fail(c, e.code, e.msg);
+  } catch (const std::bad_alloc &) {
+    return fail(c, GEMSLR_ERR_OOM, "host allocation failed");
+  } catch (const std::exception &e) {
+    return fail(c, GEMSLR_ERR_INVALID_ARG, e.what());
+  }
+}
+
+extern "C" {
+
+gemslr_status gemslr_create(gemslr_ctx **out, int cuda_device, void *nccl_comm, void *cuda_stream) {
+  if (!out) return GEMSLR_ERR_INVALID_ARG;
+  *out = nullptr;
+  auto *c = new gemslr_ctx();
+  c->device = cuda_device;
+  c->host_only = cuda_device < 0;
+  c->nccl = nccl_comm;
+  c->stream = static_cast<cudaStream_t>(cuda_stream);
+  c->pool.A = &c->alloc;
+  if (!c->host_only) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device >= ndev) {
+      delete c;
+      return GEMSLR_ERR_CUDA;
+    }
+    if (cudaSetDevice(cuda_device) != cudaSuccess) { delete c; return GEMSLR_ERR_CUDA; }
+  }
+  if (nccl_comm) {
+    c->err = "multi-GPU communicators are not supported by this build (single GPU per context)";
+    delete c;
+    return GEMSLR_ERR_NCCL;
+  }
+  *out = c;
+  return GEMSLR_OK;
+}
+
+gemslr_status gemslr_set_allocator(gemslr_ctx *c, void *(*alloc_fn)(size_t, void *), void (*free_fn)(void *, void *),
+                                   void *user) {
+  if (!c) return GEMSLR_ERR_INVALID_ARG;
+  if (c->ready) return fail(c, GEMSLR_ERR_STATE, "set_allocator must precede setup");
+  if ((alloc_fn == nullptr) != (free_fn == nullptr)) return fail(c, GEMSLR_ERR_INVALID_ARG, "alloc and free come in pairs");
+  c->alloc.alloc_fn = alloc_fn;
+  c->alloc.free_fn = free_fn;
+  c->alloc.user = user;
+  return GEMSLR_OK;
+}
+
+gemslr_status gemslr_set_coordinates(gemslr_ctx *c, int dim, const double *coords) {
+  if (!c || dim < 0 || (dim > 0 && !coords)) return fail(c, GEMSLR_ERR_INVALID_ARG, "bad coordinates");
+  if (c->ready) return fail(c, GEMSLR_ERR_STATE, "set_coordinates must precede setup");
+  c->coord_dim = dim;
+  c->coords_src = coords;   // n x dim doubles, copied by setup once n is known
+  return GEMSLR_OK;
+}
+
+}  // extern "C"
+
+template <typename T>
+static gemslr_status do_setup(gemslr_ctx *c, std::unique_ptr<Engine<T>> &E, int64_t n, const int64_t *rowptr,
+                              const int32_t *colidx, const void *values, const gemslr_params *prm) {
+  E.reset(new Engine<T>());
+  E->ctx = c;
+  SetupOptions opt;
+  opt.levels = prm->levels;
+  opt.p = prm->subdomains;
+  opt.ilu = prm->ilu;
+  opt.tau = prm->ilut_drop;
+  opt.lfil = prm->ilut_fill > 0 ? prm->ilut_fill : 10;
+  opt.last_blocks = prm->last_blocks;
+  if (c->coord_dim > 0 && c->coords_src) {
+    c->coords.assign(c->coords_src, c->coords_src + (size_t)n * c->coord_dim);
+    opt.coord_dim = c->coord_dim;
+    opt.coords = c->coords.data();
+  }
+  Error err{0, ""};
+  auto t0 = std::chrono::steady_clock::now();
+  if (!build_host_plan<T>(n, rowptr, colidx, static_cast<const T *>(values), opt, E->plan, err)) {
+    E.reset();
+    return fail(c, err.code, err.msg);
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  E->setup_host_s = std::chrono::duration<double>(t1 - t0).count();
+  E->n = n;
+  if (c->host_only) return GEMSLR_OK;
+  E->upload(c->stream);
+  CK(cudaStreamSynchronize(c->stream));
+  auto t2 = std::chrono::steady_clock::now();
+  E->setup_dev_s = std::chrono::duration<double>(t2 - t1).count();
+  E->build_lowrank(*prm, prm->seed);
+  CK(cudaStreamSynchronize(c->stream));
+  E->arnoldi_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
+  return GEMSLR_OK;
+}
+
+extern "C" {
+
+
+gemslr_status gemslr_setup(gemslr_ctx *c, gemslr_dtype dtype, int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                           const void *values, const gemslr_params *prm) {
+  if (!c) return GEMSLR_ERR_INVALID_ARG;
+  if (c->ready) return fail(c, GEMSLR_ERR_STATE, "setup called twice on one context");
+  if (!rowptr || !colidx || !values || !prm || n <= 0) return fail(c, GEMSLR_ERR_INVALID_ARG, "null pointer or n <= 0");
+  if (prm->levels < 1 || prm->subdomains < 1 || prm->rank < 0 || (dtype != GEMSLR_F64 && dtype != GEMSLR_C128) ||
+      (prm->ilu != GEMSLR_ILU0 && prm->ilu != GEMSLR_ILUT) || prm->ilut_drop < 0)
+    return fail(c, GEMSLR_ERR_INVALID_ARG, "levels < 1, subdomains < 1, rank < 0 or bad dtype/ilu");
+  if (2 * prm->rank + 2 > GS_MAXC) return fail(c, GEMSLR_ERR_INVALID_ARG, "rank > 50 not supported (cycle 2k <= 102)");
+  c->params = *prm;
+  gemslr_status st = guarded(c, [&]() -> gemslr_status {
+    if (dtype == GEMSLR_F64) return do_setup<double>(c, c->ed, n, rowptr, colidx, values, prm);
+    return do_setup<zc>(c, c->ez, n, rowptr, colidx, values, prm);
+  });
+  if (st == GEMSLR_OK) {
+    c->ready = true;
+    c->dtype = dtype;
+  } else {
+    c->ed.reset();
+    c->ez.reset();
+    c->pool.clear();
+  }
+  return st;
+}
+
+gemslr_status gemslr_layout(const gemslr_ctx *c, int64_t *n_local, int64_t *grow) {
+  if (!c || !n_local) return GEMSLR_ERR_INVALID_ARG;
+  if (!c->ready) return fail(c, GEMSLR_ERR_STATE, "layout before setup");
+  const Structure &st = c->dtype == GEMSLR_F64 ? c->ed->plan.st : c->ez->plan.st;
+  *n_local = st.n;
+  if (grow) std::memcpy(grow, st.perm.data(), st.n * sizeof(int64_t));
+  return GEMSLR_OK;
+}
+
+static gemslr_status need_device(const gemslr_ctx *c) {
+  if (!c) return GEMSLR_ERR_INVALID_ARG;
+  if (!c->ready) return fail(c, GEMSLR_ERR_STATE, "call before setup");
+  if (c->host_only) return fail(c, GEMSLR_ERR_STATE, "host-only context has no device path");
+  return GEMSLR_OK;
+}
+
+gemslr_status gemslr_spmv(gemslr_ctx *c, const void *x, void *y) {
+  gemslr_status st = need_device(c);
+  if (st) return st;
+  if (!x || !y || x == y) return fail(c, GEMSLR_ERR_INVALID_ARG, "null or aliased vectors");
+  return guarded(c, [&]() -> gemslr_status {
+    if (c->dtype == GEMSLR_F64) c->ed->spmv((const double *)x, (double *)y, 0, nullptr, nullptr);
+    else c->ez->spmv((const cd *)x, (cd *)y, 0, nullptr, nullptr);
+    return GEMSLR_OK;
+  });
+}
+
+gemslr_status gemslr_apply_precond(gemslr_ctx *c, const void *x, void *y) {
+  gemslr_status st = need_device(c);
+  if (st) return st;
+  if (!x || !y || x == y) return fail(c, GEMSLR_ERR_INVALID_ARG, "null or aliased vectors");
+  return guarded(c, [&]() -> gemslr_status {
+    if (c->dtype == GEMSLR_F64) c->ed->apply_from(0, (const double *)x, (double *)y, nullptr);
+    else c->ez->apply_from(0, (const cd *)x, (cd *)y, nullptr);
+    return GEMSLR_OK;
+  });
+}
+
+gemslr_status gemslr_solve(gemslr_ctx *c, const void *b, void *x, double rtol, int restart, int maxit, int *its,
+                           double *hist, int hcap, int *hlen, double *frel) {
+  gemslr_status st = need_device(c);
+  if (st) return st;
+  if (!b || !x || b == x || rtol <= 0 || restart < 1 || maxit < 1 || (hist && hcap < 0))
+    return fail(c, GEMSLR_ERR_INVALID_ARG, "bad solve arguments");
+  return guarded(c, [&]() -> gemslr_status {
+    if (c->dtype == GEMSLR_F64)
+      return (gemslr_status)c->ed->solve((const double *)b, (double *)x, rtol, restart, maxit, its, hist, hcap, hlen, frel);
+    return (gemslr_status)c->ez->solve((const cd *)b, (cd *)x, rtol, restart, maxit, its, hist, hcap, hlen, frel);
+  });
+}
+
+}  // extern "C"
+
+template <typename T>
+static gemslr_status host_solve(gemslr_ctx *c, Engine<T> &E, const void *b_host, void *x_host, double rtol, int restart,
+                                int maxit, int *its, double *hist, int hcap, int *hlen, double *frel) {
+  using D = typename Dev<T>::type;
+  const int64_t n = E.n;
+  cudaStream_t s = c->stream;
+  if (!E.xb) {
+    E.xb = c->pool.get<D>(4 * (n + 1));
+    E.bb = E.xb + (n + 1);
+  }
+  D *bn = E.bb + (n + 1), *xn = E.bb + 2 * (n + 1);
+  CK(cudaMemcpyAsync(bn, b_host, n * sizeof(D), cudaMemcpyHostToDevice, s));
+  if (x_host) CK(cudaMemcpyAsync(xn, x_host, n * sizeof(D), cudaMemcpyHostToDevice, s));
+  else CK(cudaMemsetAsync(xn, 0, n * sizeof(D), s));
+  const int grid = grid_for((n + 255) / 256, 4);
+  k_perm<D><<<grid, 256, 0, s>>>(n, E.perm_d, bn, E.bb, 0);
+  k_perm<D><<<grid, 256, 0, s>>>(n, E.perm_d, xn, E.xb, 0);
+  int rc = E.solve(E.bb, E.xb, rtol, restart, maxit, its, hist, hcap, hlen, frel);
+  k_perm<D><<<grid, 256, 0, s>>>(n, E.perm_d, E.xb, xn, 1);
+  CK(cudaMemcpyAsync(x_host, xn, n * sizeof(D), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return (gemslr_status)rc;
+}
+
+extern "C" {
+
+
+gemslr_status gemslr_solve_host(gemslr_ctx *c, const void *b, void *x, double rtol, int restart, int maxit, int *its,
+                                double *hist, int hcap, int *hlen, double *frel) {
+  gemslr_status st = need_device(c);
+  if (st) return st;
+  if (!b || !x || rtol <= 0 || restart < 1 || maxit < 1) return fail(c, GEMSLR_ERR_INVALID_ARG, "bad solve arguments");
+  return guarded(c, [&]() -> gemslr_status {
+    if (c->dtype == GEMSLR_F64) return host_solve(c, *c->ed, b, x, rtol, restart, maxit, its, hist, hcap, hlen, frel);
+    return host_solve(c, *c->ez, b, x, rtol, restart, maxit, its, hist, hcap, hlen, frel);
+  });
+}
+
+static gemslr_status permute_call(gemslr_ctx *c, const void *in, void *out, int inverse) {
+  gemslr_status st = need_device(c);
+  if (st) return st;
+  if (!in || !out || in == out) return fail(c, GEMSLR_ERR_INVALID_ARG, "null or aliased vectors");
+  return guarded(c, [&]() -> gemslr_status {
+    if (c->dtype == GEMSLR_F64) {
+      auto &E = *c->ed;
+      k_perm<double><<<grid_for((E.n + 255) / 256, 4), 256, 0, c->stream>>>(E.n, E.perm_d, (const double *)in, (double *)out, inverse);
+    } else {
+      auto &E = *c->ez;
+      k_perm<cd><<<grid_for((E.n + 255) / 256, 4), 256, 0, c->stream>>>(E.n, E.perm_d, (const cd *)in, (cd *)out, inverse);
+    }
+    CK(cudaGetLastError());
+    return GEMSLR_OK;
+  });
+}
+
+gemslr_status gemslr_to_local(gemslr_ctx *c, const void *xn, void *xl) { return permute_call(c, xn, xl, 0); }
+gemslr_status gemslr_to_natural(gemslr_ctx *c, const void *xl, void *xn) { return permute_call(c, xl, xn, 1); }
+
+gemslr_status gemslr_export_setup(const gemslr_ctx *c, const char *dir) {
+  if (!c || !dir) return GEMSLR_ERR_INVALID_ARG;
+  if (!c->ready) return fail(c, GEMSLR_ERR_STATE, "export before setup");
+  return guarded(const_cast<gemslr_ctx *>(c), [&]() -> gemslr_status {
+    if (c->dtype == GEMSLR_F64) c->ed->export_bundle(dir); else c->ez->export_bundle(dir);
+    return GEMSLR_OK;
+  });
+}
+
+gemslr_status gemslr_stats(const gemslr_ctx *c, char *json, size_t cap) {
+  if (!c || !json || cap == 0) return GEMSLR_ERR_INVALID_ARG;
+  if (!c->ready) return fail(c, GEMSLR_ERR_STATE, "stats before setup");
+  auto *cc = const_cast<gemslr_ctx *>(c);
+  if (cc->prof.on) cc->prof.flush();
+  std::string j = c->dtype == GEMSLR_F64 ? c->ed->stats_json() : c->ez->stats_json();
+  std::snprintf(json, cap, "%s", j.c_str());
+  return j.size() + 1 > cap ? GEMSLR_ERR_INVALID_ARG : GEMSLR_OK;
+}
+
+gemslr_status gemslr_profile(gemslr_ctx *c, int enable, int reset) {
+  if (!c) return GEMSLR_ERR_INVALID_ARG;
+  if (reset) c->prof.reset();
+  c->prof.on = enable != 0;
+  if (!c->prof.on) c->prof.flush();
+  return GEMSLR_OK;
+}
+
+const char *gemslr_last_error(const gemslr_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+void gemslr_destroy(gemslr_ctx *c) {
+  if (!c) return;
+  if (c->device >= 0) {
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+  }
+  c->prof.flush();
+  c->ed.reset();
+  c->ez.reset();
+  c->pool.clear();
+  delete c;
+}
+
+}  // extern "C"

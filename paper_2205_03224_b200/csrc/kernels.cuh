@@ -1,0 +1,506 @@
+// sm_100a kernels of the GeMSLR solve path (arXiv 2205.03224).
+//
+// Every kernel is bandwidth- or latency-bound GEMV/SpMV-class work (<= 0.5
+// flop/byte), so none uses tensor cores; they are written for coalesced
+// 128-byte warp accesses, many loads in flight per thread, grids sized to the
+// 148 SMs and deterministic (fixed-order) reductions.
+//
+//   k_spmv_sell     K1   y = A x / r = b - A x, SELL-32 (one warp per 32 rows)    Note N P:L58-61
+//   k_trisolve      K4/K5/K9  level-scheduled L then U sweep per block; one CTA or
+//                   one thread-block cluster per block, CTA/cluster barriers       Alg.2 l.2, l.9 P:L552,L561
+//   k_ew            K6+K7  r_J = src_J - E_l z1 ; s = W_l^H r_J ; t = G_l s         Alg.2 l.3, l.7 P:L553,L558
+//   k_waxpy         K8   r_J += W_l t
+//   k_gs            K10-K12  CGS2 passes (multi-dot / update+dot / update+norm)
+//   k_fgmres_col    Hessenberg column, Givens rotation, convergence flag (1 thread) P:L695-697
+//   k_xupdate       K13  x += Z y
+//   k_scale, k_perm K14  vector utilities
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gemslr {
+
+// ----------------------------------------------------------------- scalars
+struct cd {
+  double x, y;
+};
+__host__ __device__ inline cd operator+(cd a, cd b) { return {a.x + b.x, a.y + b.y}; }
+__host__ __device__ inline cd operator-(cd a, cd b) { return {a.x - b.x, a.y - b.y}; }
+__host__ __device__ inline cd operator-(cd a) { return {-a.x, -a.y}; }
+__host__ __device__ inline cd operator*(cd a, cd b) { return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
+__host__ __device__ inline cd operator*(double a, cd b) { return {a * b.x, a * b.y}; }
+__host__ __device__ inline cd &operator+=(cd &a, cd b) { a.x += b.x; a.y += b.y; return a; }
+__host__ __device__ inline cd &operator-=(cd &a, cd b) { a.x -= b.x; a.y -= b.y; return a; }
+__host__ __device__ inline cd operator/(cd a, cd b) {
+  // (a conj(b)) / |b|^2 — division by the U diagonal of complex ILU factors
+  const double d = b.x * b.x + b.y * b.y;
+  return {(a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d};
+}
+__host__ __device__ inline double dconj(double a) { return a; }
+__host__ __device__ inline cd dconj(cd a) { return {a.x, -a.y}; }
+__host__ __device__ inline double dabs2(double a) { return a * a; }
+__host__ __device__ inline double dabs2(cd a) { return a.x * a.x + a.y * a.y; }
+template <typename T> __host__ __device__ inline T dzero();
+template <> __host__ __device__ inline double dzero<double>() { return 0.0; }
+template <> __host__ __device__ inline cd dzero<cd>() { return {0.0, 0.0}; }
+__host__ __device__ inline double dscale(double a, double s) { return a * s; }
+__host__ __device__ inline cd dscale(cd a, double s) { return {a.x * s, a.y * s}; }
+
+__device__ inline double shfl_xor(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+__device__ inline cd shfl_xor(cd v, int m) { return {__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m)}; }
+template <typename T>
+__device__ inline T warp_sum(T v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v += shfl_xor(v, m);
+  return v;
+}
+
+// L2-coherent loads (bypass L1) for vectors written by other CTAs of a cluster
+__device__ inline double ld_cg(const double *p) { return __ldcg(p); }
+__device__ inline cd ld_cg(const cd *p) {
+  double2 v = __ldcg(reinterpret_cast<const double2 *>(p));
+  return {v.x, v.y};
+}
+__device__ inline double ld_nc(const double *p) { return __ldg(p); }
+__device__ inline cd ld_nc(const cd *p) {
+  double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+  return {v.x, v.y};
+}
+
+__device__ inline unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ inline void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// ----------------------------------------------------------------- K1 SpMV
+// SELL-32: slice s holds rows 32s..32s+31; entry e of lane r at off[s] + 32e + r;
+// padding has col = -1.  mode 0: y = A x ; mode 1: y = b - A x.
+template <typename T>
+__global__ void __launch_bounds__(256) k_spmv_sell(int64_t n, int64_t nslices, const int64_t *__restrict__ off,
+                                                   const int32_t *__restrict__ col, const T *__restrict__ val,
+                                                   const T *__restrict__ x, T *__restrict__ y, int mode,
+                                                   const T *__restrict__ b, const int *__restrict__ done) {
+  if (done && *done) return;
+  const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t o = off[s];
+  const int w = (int)((off[s + 1] - o) >> 5);
+  T acc = dzero<T>();
+  const int32_t *cp = col + o + lane;
+  const T *vp = val + o + lane;
+#pragma unroll 8
+  for (int e = 0; e < w; ++e) {
+    const int32_t c = __ldg(cp + 32 * e);
+    const T v = ld_nc(vp + 32 * e);
+    if (c >= 0) acc += v * ld_nc(x + c);
+  }
+  const int64_t row = s * 32 + lane;
+  if (row < n) y[row] = mode ? b[row] - acc : acc;
+}
+
+// ----------------------------------------------------------------- K4/K5/K9 trisolve
+template <typename T>
+struct TriDev {
+  const int32_t *blk_lev;
+  const int32_t *lev_slice;
+  const int64_t *slice_off;
+  const int32_t *slice_row;
+  const int32_t *col;
+  const T *val;
+  const T *diag;
+};
+
+enum { TRI_DOWN = 0, TRI_UP = 1 };
+
+// One CTA (CLUSTER=false) or one cluster of CPS CTAs (CLUSTER=true) per block.
+// DOWN:  x[rows] = U^-1 L^-1 rhs[rows]                      (z1 of Alg. 2 l.2; C_last)
+// UP:    t = F_l y_J (rows of the block) ; t = U^-1 L^-1 t ; x[rows] -= t   (Alg. 2 l.9)
+// Every level of a sweep ends with a CTA / cluster barrier; rows of one level
+// are independent and one warp handles one SELL slice (one row per lane).
+template <typename T, bool CLUSTER>
+__global__ void __launch_bounds__(256) k_trisolve(TriDev<T> Lp, TriDev<T> Up, const int64_t *__restrict__ blk, int mode,
+                                                  const T *rhs, T *x, T *tmp, const int64_t *__restrict__ Fptr,
+                                                  const int32_t *__restrict__ Fcol, const T *__restrict__ Fval,
+                                                  int64_t Fbase, const int *__restrict__ done) {
+  if (done && *done) return;
+  int nct = 1, rank = 0;
+  if (CLUSTER) {
+    unsigned n;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+    nct = (int)n;
+    rank = (int)cluster_ctarank();
+  }
+  const int b = blockIdx.x / nct;
+  const int wpc = blockDim.x >> 5;
+  const int gw = rank * wpc + (threadIdx.x >> 5);
+  const int nw = nct * wpc;
+  const int lane = threadIdx.x & 31;
+  const int64_t r0 = blk[b], r1 = blk[b + 1];
+  const int gt = rank * blockDim.x + threadIdx.x, nt = nct * blockDim.x;
+  auto barrier = [&]() {
+    if (CLUSTER) cluster_sync_all(); else __syncthreads();
+  };
+  auto ldv = [&](const T *p) -> T { return CLUSTER ? ld_cg(p) : *p; };
+  const T *in;
+  T *out;
+  if (mode == TRI_DOWN) {
+    in = rhs;
+    out = x;
+  } else {
+    for (int64_t i = r0 + gt; i < r1; i += nt) {              // t = F_l y_J
+      const int64_t li = i - Fbase;
+      T acc = dzero<T>();
+      for (int64_t p = Fptr[li]; p < Fptr[li + 1]; ++p) acc += Fval[p] * x[Fcol[p]];
+      tmp[i] = acc;
+    }
+    barrier();
+    in = tmp;
+    out = tmp;
+  }
+  // forward sweep, unit-lower L
+  for (int v = Lp.blk_lev[b]; v < Lp.blk_lev[b + 1]; ++v) {
+    for (int s = Lp.lev_slice[v] + gw; s < Lp.lev_slice[v + 1]; s += nw) {
+      const int32_t row = Lp.slice_row[(int64_t)s * 32 + lane];
+      const int64_t o = Lp.slice_off[s];
+      const int w = (int)((Lp.slice_off[s + 1] - o) >> 5);
+      if (row >= 0) {
+        T acc = ldv(in + row);
+        for (int e = 0; e < w; ++e) {
+          const int32_t c = Lp.col[o + 32 * e + lane];
+          if (c >= 0) acc -= Lp.val[o + 32 * e + lane] * ldv(out + c);
+        }
+        out[row] = acc;
+      }
+    }
+    barrier();
+  }
+  // backward sweep, U with its diagonal
+  for (int v = Up.blk_lev[b]; v < Up.blk_lev[b + 1]; ++v) {
+    for (int s = Up.lev_slice[v] + gw; s < Up.lev_slice[v + 1]; s += nw) {
+      const int32_t row = Up.slice_row[(int64_t)s * 32 + lane];
+      const int64_t o = Up.slice_off[s];
+      const int w = (int)((Up.slice_off[s + 1] - o) >> 5);
+      if (row >= 0) {
+        T acc = ldv(out + row);
+        for (int e = 0; e < w; ++e) {
+          const int32_t c = Up.col[o + 32 * e + lane];
+          if (c >= 0) acc -= Up.val[o + 32 * e + lane] * ldv(out + c);
+        }
+        out[row] = acc / Up.diag[(int64_t)s * 32 + lane];
+      }
+    }
+    barrier();
+  }
+  if (mode == TRI_UP)
+    for (int64_t i = r0 + gt; i < r1; i += nt) x[i] = x[i] - ldv(tmp + i);   // y1 = z1 - U^-1 L^-1 F y2
+}
+
+// ----------------------------------------------------------------- K6+K7
+// Rows J_l = [rowbase, rowbase + s): dst_i = src_i - Σ_j E_ij z_j (src == nullptr: 0),
+// then per-column partial sums of conj(W_ic) dst_i; the last CTA reduces the
+// partials in CTA order, s = W^H r_J, and writes t = G s.
+// CTA = 8 warps; a tile is 256 rows; warp w owns the columns c ≡ w (mod 8).
+constexpr int EW_NACC = 6;   // k <= 48
+template <typename T>
+__global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const int64_t *__restrict__ Eptr,
+                                            const int32_t *__restrict__ Ecol, const T *__restrict__ Eval,
+                                            const T *__restrict__ z, const T *src, T *dst, const T *__restrict__ W,
+                                            int64_t ldw, int k, T *__restrict__ partial, unsigned *ticket,
+                                            const T *__restrict__ G, T *__restrict__ tout, const int *__restrict__ done) {
+  if (done && *done) return;
+  __shared__ T sv[256];
+  __shared__ T sred[64];
+  __shared__ bool amlast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T acc[EW_NACC];
+#pragma unroll
+  for (int a = 0; a < EW_NACC; ++a) acc[a] = dzero<T>();
+  const int64_t ntiles = (s + 255) / 256;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * 256 + tid;
+    T v = dzero<T>();
+    if (i < s) {
+      T e = dzero<T>();
+      for (int64_t p = Eptr[i]; p < Eptr[i + 1]; ++p) e += Eval[p] * z[Ecol[p]];
+      v = (src ? src[rowbase + i] : dzero<T>()) - e;
+      dst[rowbase + i] = v;
+    }
+    if (k > 0) {
+      sv[tid] = v;
+      __syncthreads();
+#pragma unroll
+      for (int a = 0; a < EW_NACC; ++a) {
+        const int c = warp + 8 * a;
+        if (c < k) {
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) {
+            const int64_t ii = tile * 256 + rr * 32 + lane;
+            if (ii < s) acc[a] += dconj(W[c * ldw + ii]) * sv[rr * 32 + lane];
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (k == 0) return;
+#pragma unroll
+  for (int a = 0; a < EW_NACC; ++a) {
+    const int c = warp + 8 * a;
+    T r = warp_sum(acc[a]);
+    if (lane == 0 && c < k) partial[(int64_t)blockIdx.x * k + c] = r;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) amlast = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!amlast) return;
+  __threadfence();
+  if (tid < k) {
+    T sum = dzero<T>();
+    for (unsigned q = 0; q < gridDim.x; ++q) sum += ld_cg(partial + (int64_t)q * k + tid);
+    sred[tid] = sum;
+  }
+  __syncthreads();
+  if (tid < k) {
+    T t = dzero<T>();
+    for (int a = 0; a < k; ++a) t += G[(int64_t)a * k + tid] * sred[a];   // (G s)_c, G column-major
+    tout[tid] = t;
+  }
+  if (tid == 0) *ticket = 0;
+}
+
+// ----------------------------------------------------------------- K8
+template <typename T>
+__global__ void __launch_bounds__(256) k_waxpy(int64_t s, int64_t rowbase, const T *__restrict__ W, int64_t ldw, int k,
+                                               const T *__restrict__ t, T *dst, const int *__restrict__ done) {
+  if (done && *done) return;
+  __shared__ T st[64];
+  if (threadIdx.x < k) st[threadIdx.x] = t[threadIdx.x];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    T acc = dzero<T>();
+    for (int c = 0; c < k; ++c) acc += ld_nc(W + c * ldw + i) * st[c];
+    dst[rowbase + i] += acc;
+  }
+}
+
+// ----------------------------------------------------------------- K10-K12 CGS2
+// V column-major (ld), ncols <= GS_MAXC.  A CTA of 8 warps walks 32-row tiles;
+// warp w owns the columns c ≡ w (mod 8) and keeps those V values of the tile
+// in registers for the update and the dot of the same pass.
+//   pass 1 (upd = 0, dot = 1): res = [V^H w, ||w||^2]
+//   pass 2 (upd = 1, dot = 1): w -= V h_in ; res = [V^H w, ||w||^2]
+//   pass 3 (upd = 1, dot = 0): w -= V h_in ; res = [||w||^2]
+// Results are reduced in fixed CTA order by the last CTA (ticket).
+constexpr int GS_NPW = 13;                 // columns per warp
+constexpr int GS_MAXC = 8 * GS_NPW;        // 104 >= restart + 1
+template <typename T>
+__global__ void __launch_bounds__(256) k_gs(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
+                                            int dot, const T *__restrict__ h_in, T *__restrict__ partial,
+                                            unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
+  if (done && *done) return;
+  __shared__ T su[8][32];
+  __shared__ T sh[GS_MAXC];
+  __shared__ bool amlast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (upd)
+    for (int c = tid; c < ncols; c += blockDim.x) sh[c] = h_in[c];
+  __syncthreads();
+  T acc[GS_NPW];
+#pragma unroll
+  for (int a = 0; a < GS_NPW; ++a) acc[a] = dzero<T>();
+  double nrm = 0.0;
+  const int64_t ntiles = (n + 31) / 32;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * 32 + lane;
+    const bool ok = i < n;
+    T vr[GS_NPW];
+#pragma unroll
+    for (int a = 0; a < GS_NPW; ++a) {
+      const int c = warp + 8 * a;
+      vr[a] = (ok && c < ncols) ? ld_nc(V + c * ldv + i) : dzero<T>();
+    }
+    T wi = ok ? w[i] : dzero<T>();
+    if (upd) {
+      T u = dzero<T>();
+#pragma unroll
+      for (int a = 0; a < GS_NPW; ++a) {
+        const int c = warp + 8 * a;
+        if (c < ncols) u += vr[a] * sh[c];
+      }
+      su[warp][lane] = u;
+      __syncthreads();
+      T tot = dzero<T>();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) tot += su[q][lane];
+      wi = wi - tot;
+      __syncthreads();
+      if (warp == 0 && ok) w[i] = wi;
+    }
+    if (dot) {
+#pragma unroll
+      for (int a = 0; a < GS_NPW; ++a) acc[a] += dconj(vr[a]) * wi;
+    }
+    if (warp == 0) nrm += dabs2(wi);
+  }
+  // per-warp reduction; warp w owns its columns, warp 0 owns the norm
+  const int nres = dot ? ncols + 1 : 1;
+  if (dot) {
+#pragma unroll
+    for (int a = 0; a < GS_NPW; ++a) {
+      const int c = warp + 8 * a;
+      T r = warp_sum(acc[a]);
+      if (lane == 0 && c < ncols) partial[(int64_t)blockIdx.x * nres + c] = r;
+    }
+  }
+  if (warp == 0) {
+    double r = warp_sum(nrm);
+    if (lane == 0) {
+      T t = dzero<T>();
+      if constexpr (sizeof(T) == sizeof(double)) t = r; else t = T{r, 0.0};
+      partial[(int64_t)blockIdx.x * nres + (nres - 1)] = t;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) amlast = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!amlast) return;
+  __threadfence();
+  for (int c = tid; c < nres; c += blockDim.x) {
+    T sum = dzero<T>();
+    for (unsigned q = 0; q < gridDim.x; ++q) sum += ld_cg(partial + (int64_t)q * nres + c);
+    res[c] = sum;
+  }
+  if (tid == 0) *ticket = 0;
+}
+
+// ----------------------------------------------------------------- FGMRES column (1 thread)
+template <typename T>
+struct FgmDev {
+  int *done;          // [0] done flag
+  int *ints;          // [0] jend, [1] its, [2] maxit
+  double *dbl;        // [0] bnorm, [1] rtol, [2] 1/H[j+1,j]
+  double *hist;       // residual estimate history (maxit + 1)
+  T *H;               // (m+1) x m column-major, rotated
+  T *g;               // m + 1
+  double *cs;         // m
+  T *sn;              // m
+};
+
+template <typename T>
+__global__ void k_fgmres_col(FgmDev<T> f, int m, int j, const T *__restrict__ res1, const T *__restrict__ res2,
+                             const T *__restrict__ res3) {
+  if (*f.done) return;
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  T *Hj = f.H + (int64_t)j * (m + 1);
+  double eta2, hn2;
+  if constexpr (sizeof(T) == sizeof(double)) { eta2 = res1[j + 1]; hn2 = res3[0]; }
+  else { eta2 = res1[j + 1].x; hn2 = res3[0].x; }
+  const double eta = sqrt(eta2 > 0 ? eta2 : 0.0);
+  const double hnext = sqrt(hn2 > 0 ? hn2 : 0.0);
+  for (int i = 0; i <= j; ++i) Hj[i] = res1[i] + res2[i];
+  if constexpr (sizeof(T) == sizeof(double)) Hj[j + 1] = hnext; else Hj[j + 1] = T{hnext, 0.0};
+  for (int i = 0; i < j; ++i) {                       // previous rotations
+    const T p = Hj[i], q = Hj[i + 1];
+    Hj[i] = f.cs[i] * p + dconj(f.sn[i]) * q;
+    Hj[i + 1] = (-f.sn[i]) * p + f.cs[i] * q;
+  }
+  const T a = Hj[j];
+  const double aa = sqrt(dabs2(a)), bb = hnext;
+  double c;
+  T s;
+  if (bb == 0.0) { c = 1.0; s = dzero<T>(); }
+  else if (aa == 0.0) {
+    c = 0.0;
+    if constexpr (sizeof(T) == sizeof(double)) s = 1.0; else s = T{1.0, 0.0};
+  } else {
+    const double t = sqrt(aa * aa + bb * bb);
+    c = aa / t;
+    s = dscale(dconj(a), bb / (aa * t));
+  }
+  f.cs[j] = c;
+  f.sn[j] = s;
+  {
+    const T p = Hj[j], q = Hj[j + 1];
+    Hj[j] = c * p + dconj(s) * q;
+    Hj[j + 1] = (-s) * p + c * q;
+    const T gp = f.g[j], gq = f.g[j + 1];
+    f.g[j] = c * gp + dconj(s) * gq;
+    f.g[j + 1] = (-s) * gp + c * gq;
+  }
+  const int its = f.ints[1] + 1;
+  f.ints[1] = its;
+  f.ints[0] = j + 1;
+  const double est = sqrt(dabs2(f.g[j + 1]));
+  f.hist[its] = est / f.dbl[0];
+  f.dbl[2] = hnext > 0 ? 1.0 / hnext : 0.0;
+  if (est <= f.dbl[1] * f.dbl[0] || hnext <= 1e-14 * eta || its >= f.ints[2] || j + 1 >= m) *f.done = 1;
+}
+
+// ----------------------------------------------------------------- utilities
+// y = x * scale[0] (scale may be a device scalar of 1/β); done-guarded
+template <typename T>
+__global__ void k_scale(int64_t n, const T *x, T *y, const double *scale, const int *done) {
+  if (done && *done) return;
+  const double sc = *scale;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = dscale(x[i], sc);
+}
+
+// x += Z[:, 0:ncols] y
+template <typename T>
+__global__ void k_xupdate(int64_t n, const T *__restrict__ Z, int64_t ldz, int ncols, const T *__restrict__ y, T *x) {
+  __shared__ T sy[GS_MAXC];
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) sy[c] = y[c];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    T acc = x[i];
+    for (int c = 0; c < ncols; ++c) acc += ld_nc(Z + c * ldz + i) * sy[c];
+    x[i] = acc;
+  }
+}
+
+// out[:, c] = V[:, 0:m] Y[:, c], c < kc (thick-restart basis rotation)
+template <typename T>
+__global__ void k_gemm_tall(int64_t n, const T *__restrict__ V, int64_t ldv, int m, const T *__restrict__ Y, int kc,
+                            T *__restrict__ out, int64_t ldo) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int c0 = 0; c0 < kc; c0 += 8) {
+      T acc[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) acc[a] = dzero<T>();
+      for (int j = 0; j < m; ++j) {
+        const T v = V[j * ldv + i];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+          if (c0 + a < kc) acc[a] += v * Y[(int64_t)(c0 + a) * m + j];
+      }
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+        if (c0 + a < kc) out[(c0 + a) * ldo + i] = acc[a];
+    }
+  }
+}
+
+// natural <-> permuted: local[i] = natural[perm[i]]  /  natural[perm[i]] = local[i]
+template <typename T>
+__global__ void k_perm(int64_t n, const int64_t *__restrict__ perm, const T *__restrict__ in, T *__restrict__ out,
+                       int inverse) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (inverse) out[perm[i]] = in[i]; else out[i] = in[perm[i]];
+  }
+}
+
+template <typename T>
+__global__ void k_fill(int64_t n, T *x, T v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) x[i] = v;
+}
+
+}  // namespace gemslr

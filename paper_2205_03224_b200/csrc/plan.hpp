@@ -1,0 +1,133 @@
+// Host-side setup data of the GeMSLR solve path (arXiv 2205.03224).
+//
+// The host setup (partition -> multilevel permutation -> blocks -> ILU ->
+// level schedules) produces a HostPlan; context.cu uploads it and builds the
+// low-rank terms on the GPU.  Notation follows the paper: level l has the
+// interiors I_l = [o_l, o_{l+1}) split into p subdomain blocks B_l^(j), the
+// interface below it J_l = [o_{l+1}, N), and the last separator
+// C_{l_ev-1} = [o_L, N).
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace gemslr {
+
+using zc = std::complex<double>;
+
+inline double absval(double a) { return a < 0 ? -a : a; }
+inline double absval(const zc &a) { return std::abs(a); }
+inline double abs2(double a) { return a * a; }
+inline double abs2(const zc &a) { return a.real() * a.real() + a.imag() * a.imag(); }
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+// Symmetric adjacency graph of |A| + |A^T| without self loops.
+struct Graph {
+  int64_t n = 0;
+  std::vector<int64_t> ptr;
+  std::vector<int32_t> adj;
+};
+
+// Multilevel structure (Alg. 3).  Positions are in the global
+// permuted order Â = Pᵀ A P with perm[new] = old.
+struct Structure {
+  int64_t n = 0;
+  int L = 0;                                   // achieved levels l_ev
+  std::vector<int64_t> perm, iperm;
+  std::vector<int64_t> o;                      // o_0 .. o_L
+  std::vector<std::vector<int64_t>> blk;       // per level: block boundaries (absolute)
+  std::vector<int64_t> last;                   // C_last block boundaries (absolute)
+};
+
+template <typename T>
+struct Csr {                                    // rows local to a range, columns as documented per use
+  int64_t n = 0, m = 0;
+  std::vector<int64_t> ptr;
+  std::vector<int32_t> col;
+  std::vector<T> val;
+  int64_t nnz() const { return ptr.empty() ? 0 : ptr[n]; }
+};
+
+// ILU factors of one diagonal block in block-local indices: L strictly lower
+// with an implicit unit diagonal, U upper with the diagonal FIRST in each row.
+template <typename T>
+struct Factor {
+  Csr<T> L, U;
+};
+
+// Level-scheduled, SELL-32 packed triangular sweep over a set of blocks
+// ("stage").  For block b, levels [blk_lev[b], blk_lev[b+1]) of lev_slice;
+// level v covers slices [lev_slice[v], lev_slice[v+1]); slice s has 32 lanes
+// (one row each, -1 = padding) and width w_s = (slice_off[s+1]-slice_off[s])/32
+// entries stored column-major (entry e of lane r at slice_off[s] + 32 e + r).
+// Rows and columns are ABSOLUTE positions in the permuted vector; col = -1 pads.
+template <typename T>
+struct TriPack {
+  std::vector<int32_t> blk_lev;
+  std::vector<int32_t> lev_slice;
+  std::vector<int64_t> slice_off;
+  std::vector<int32_t> slice_row;
+  std::vector<int32_t> col;
+  std::vector<T> val;
+  std::vector<T> diag;                          // U sweep only: u_ii per lane (1 on padding)
+  int max_depth = 0;
+  int64_t nnz_real = 0;                         // stored nonzeros without padding
+};
+
+template <typename T>
+struct Stage {                                  // the blocks of one level (or of C_last)
+  std::vector<int64_t> blk;                     // absolute boundaries (empty blocks removed)
+  TriPack<T> Lp, Up;
+};
+
+template <typename T>
+struct HostPlan {
+  Structure st;
+  Csr<T> Ahat;                                  // Pᵀ A P, absolute columns
+  std::vector<std::vector<Factor<T>>> fac;      // per level, per block (block-local)
+  std::vector<Factor<T>> lastfac;               // per C_last block
+  std::vector<Csr<T>> E;                        // E_l: rows J_l (local row i - o_{l+1}), absolute columns in I_l
+  std::vector<Csr<T>> F;                        // F_l: rows I_l (local row i - o_l), absolute columns in J_l
+  std::vector<Stage<T>> stage;                  // per level
+  Stage<T> last_stage;
+  int64_t fac_nnz = 0;                          // nnz(L+U) over every block (L strict + U incl. diag)
+};
+
+struct SetupOptions {
+  int levels = 1, p = 1, ilu = 0, lfil = 10, last_blocks = 0;
+  double tau = 1e-3;
+  int coord_dim = 0;
+  const double *coords = nullptr;               // n x coord_dim (optional)
+};
+
+// partition.cpp
+Graph build_graph(int64_t n, const int64_t *rowptr, const int32_t *colidx);
+bool build_structure(const Graph &g, const SetupOptions &opt, Structure &st, Error &err);
+
+// ilu.cpp
+template <typename T> bool ilu0(const Csr<T> &B, Factor<T> &F, std::string &err);
+template <typename T> bool ilut(const Csr<T> &B, double tau, int lfil, Factor<T> &F, std::string &err);
+
+// schedule.cpp
+template <typename T> void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, Stage<T> &S);
+
+// hostplan.cpp
+template <typename T>
+bool build_host_plan(int64_t n, const int64_t *rowptr, const int32_t *colidx, const T *vals,
+                     const SetupOptions &opt, HostPlan<T> &plan, Error &err);
+
+// schur.cpp — dense complex Schur machinery for the thick-restart Arnoldi.
+// Matrices column-major, leading dimension = rows.
+// schur_complex: A (n x n) -> T (upper triangular) and Z (unitary), A = Z T Z^H.
+bool schur_complex(int n, const zc *A, zc *T, zc *Z);
+// reorder T/Z so that the eigenvalues flagged in `select` come first (in their
+// current relative order); Givens swaps of adjacent 1x1 blocks.
+void schur_reorder(int n, zc *T, zc *Z, const std::vector<char> &select);
+
+}  // namespace gemslr

@@ -1,0 +1,172 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the independent oracle.
+
+Bar (BASELINE.json north_star): ||y_gpu - y_or||_2 <= 1e-10 ||y_or||_2
+on every SpMV and preconditioner application (fp64 and complex128); FGMRES
+iteration count within ±1 of the oracle's; final true residual <= rtol.
+
+The setup is non-unique (partition ties, Arnoldi subspaces), so both sides
+consume ONE exported bundle: the oracle verifies it independently (c3) — its
+own Â from its own A, its own ILU factors recomputed and compared, W
+orthonormal, the Rayleigh quotient W^H Ĝ W ≈ R with its own Ĝ, the identity
+(I - R)(G + I) = I — and then runs its own apply with its own factors and the
+bundle's W, G.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import dense as D
+from synth import problems as P
+from tests.bundle_io import Bundle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+gm = pytest.importorskip("paper_2205_03224_b200")
+
+TOL = 1e-10
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def make_pair(prob, prm, tmp_path, coords=True, **kw):
+    """GPU solver + oracle preconditioner on the same verified bundle."""
+    s = gm.Solver(prob.rowptr, prob.colidx, prob.values, prm["levels"], prm["subdomains"], prm["rank"],
+                  ilu=prm["ilu"], ilut_drop=prm.get("ilut_drop", 1e-3), ilut_fill=prm.get("ilut_fill", 10),
+                  coords=prob.coords if coords else None, device=0, **kw)
+    d = s.export(str(tmp_path / "bundle"))
+    B = Bundle(d)
+    st = B.structure()
+    A = prob.scipy()
+    kind = oracle.ILU0 if prm["ilu"] == "ilu0" else oracle.ILUT
+    Pc = oracle.Precond(A, st, ilu=(kind, prm.get("ilut_drop", 1e-3), prm.get("ilut_fill", 10)))
+    for l in range(B.L):
+        lr = B.lowrank(l)
+        if lr is not None:
+            W, R, G = lr
+            Pc.set_lowrank(l, W, G)
+    return s, B, st, Pc
+
+
+def to_dev(s, v):
+    return torch.from_numpy(np.ascontiguousarray(v)).to(device="cuda:0", dtype=s.torch_dtype)
+
+
+def verify_lowrank(B, Pc, rank):
+    for l in range(B.L):
+        lr = B.lowrank(l)
+        if lr is None:
+            assert rank == 0 or Pc.s(l) == 0
+            continue
+        W, R, G = lr
+        k = W.shape[1]
+        assert rank <= k <= rank + 1 or k == Pc.s(l)
+        assert np.abs(W.conj().T @ W - np.eye(k)).max() <= 1e-12            # c3.5
+        GW = np.stack([Pc.ghat(l, W[:, c]) for c in range(k)], axis=1)
+        WGW = W.conj().T @ GW
+        assert np.linalg.norm(WGW - R) <= 1e-2 * np.linalg.norm(R)          # c3.6 Rayleigh
+        I = np.eye(k)
+        assert np.abs((I - R) @ (G + I) - I).max() <= 1e-12                 # c3.8
+
+
+CASES = [
+    ("C1", None, {}),
+    ("C2", (20, 20, 20), dict(subdomains=8, rank=6)),
+    ("C3", (20, 18, 16), dict(subdomains=8, rank=8)),
+    ("C4", (16, 16, 14), dict(subdomains=8, rank=8)),
+    ("C5", (24, 24, 24), dict(subdomains=8, rank=6)),
+]
+
+
+@pytest.mark.parametrize("name,dims,over", CASES)
+def test_spmv_and_apply_parity(tmp_path, name, dims, over):
+    prob, b, xt, prm = P.make_config(name, dims=dims, **over)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    verify_lowrank(B, Pc, prm["rank"])
+    perm = st["perm"]
+    n = prob.n
+    # SpMV: local permuted layout in, gathered back to natural order
+    x = P.rhs_vector(n, prob.is_complex, 3)
+    y = s.spmv(to_dev(s, x[perm])).cpu().numpy()
+    ynat = np.empty_like(y)
+    ynat[perm] = y
+    assert rel(ynat, oracle.spmv(prob, x)) <= TOL
+    # apply: several vectors, incl. structured ones
+    for seed, scale in ((5, 1.0), (6, 1e-3), (7, 1e5)):
+        r = P.rhs_vector(n, prob.is_complex, seed) * scale
+        yg = s.apply_precond(to_dev(s, r)).cpu().numpy()
+        yo = Pc.apply(r)
+        assert rel(yg, yo) <= TOL, (seed, rel(yg, yo))
+    e = np.zeros(n, dtype=prob.values.dtype)
+    e[n // 2] = 1
+    assert rel(s.apply_precond(to_dev(s, e)).cpu().numpy(), Pc.apply(e)) <= TOL
+    z = s.apply_precond(to_dev(s, np.zeros(n, dtype=prob.values.dtype))).cpu().numpy()
+    assert np.all(z == 0)
+
+
+@pytest.mark.parametrize("name,dims,over", CASES)
+def test_solve_parity(tmp_path, name, dims, over):
+    prob, b, xt, prm = P.make_config(name, dims=dims, **over)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    perm = st["perm"]
+    out = s.solve(to_dev(s, b[perm]), rtol=prm["rtol"], restart=prm["restart"], maxit=1000)
+    xg = np.empty(prob.n, dtype=prob.values.dtype)
+    xg[perm] = out["x"].cpu().numpy()
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"], maxit=1000)
+    assert out["status"] == 0 and ref["status"] == 0
+    assert abs(out["its"] - ref["its"]) <= 1, (out["its"], ref["its"])
+    true_rel = np.linalg.norm(b - oracle.spmv(prob, xg)) / np.linalg.norm(b)
+    assert true_rel <= prm["rtol"]
+    assert out["final_relres"] == pytest.approx(true_rel, rel=1e-6, abs=1e-14)
+    # residual histories agree while above the rounding floor
+    h = min(len(out["hist"]), len(ref["hist"]))
+    assert np.allclose(out["hist"][:h], ref["hist"][:h], rtol=1e-6, atol=1e2 * prm["rtol"])
+    if xt is not None:
+        assert np.linalg.norm(xg - xt) <= 1e3 * prm["rtol"] * np.linalg.norm(xt)
+
+
+def test_solve_host_path_matches_device_path(tmp_path):
+    prob, b, xt, prm = P.make_config("C2", dims=(16, 16, 16), subdomains=8, rank=6)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    perm = st["perm"]
+    dev = s.solve(to_dev(s, b[perm]), rtol=prm["rtol"], restart=prm["restart"])
+    host = s.solve_host(b, rtol=prm["rtol"], restart=prm["restart"])
+    xd = np.empty(prob.n)
+    xd[perm] = dev["x"].cpu().numpy()
+    assert host["its"] == dev["its"]
+    assert rel(host["x"], xd) <= 1e-13
+    # to_local / to_natural round trip
+    v = to_dev(s, P.rhs_vector(prob.n, False, 1))
+    assert torch.equal(s.to_natural(s.to_local(v)), v)
+
+
+def test_dense_spectrum_C1(tmp_path):
+    """c3.7: on C1 the selected Ritz values match, to two digits, the k eigenvalues of
+    the dense Ĝ_0 with the largest |γ/(1-γ)|."""
+    prob, b, xt, prm = P.make_config("C1")
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    W, R, G = B.lowrank(0)
+    Gm = D.dense_ghat(Pc, 0)
+    ev = np.linalg.eigvals(Gm)
+    key = np.abs(ev / (1 - ev))
+    top = ev[np.argsort(-key)][:W.shape[1]]
+    ritz = np.linalg.eigvals(R)
+    for t in top[:prm["rank"] - 1]:
+        assert np.min(np.abs(ritz - t)) <= 1e-2 * max(abs(t), 1e-3)
+
+
+def test_rank_zero_and_ilu0_variants(tmp_path):
+    prob, b, xt, prm = P.make_config("C3", dims=(14, 14, 14), subdomains=8, rank=0, ilu="ilu0")
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    r = P.rhs_vector(prob.n, False, 9)
+    assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
+
+
+@pytest.mark.parametrize("cps", [1, 2, 4])
+def test_cluster_sizes_agree(tmp_path, cps):
+    prob, b, xt, prm = P.make_config("C5", dims=(32, 32, 32), subdomains=4, rank=4)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path, cluster_ctas=cps)
+    r = P.rhs_vector(prob.n, False, 2)
+    assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
