@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Bench: FGMRES solve-phase ms/iteration of the GeMSLR path on B200 (BASELINE.json metric).
+
+A "step" is one preconditioned FGMRES iteration (the whole hot path: SpMV,
+one GeMSLR apply, CGS2 Gram-Schmidt, Givens update).  Workload: config C5 at
+N=1 — 3D 7-point Laplacian 128^3, l_ev = 3, p = 32, ILUT(1e-3, 10), rank 20,
+restart 50 — the per-GPU problem of the north star's weak-scaling target.
+Timed region: exactly K iterations (solve with maxit = K and an unreachable
+tolerance), inputs resident in HBM; the working set (matrix, factors,
+Krylov basis ~2.4 GB) exceeds the 126 MB L2, so no flush is needed.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+--impl reference times the plain CPU oracle (oracle/) on bounded samples of
+the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import problems as P  # noqa: E402
+
+METRIC = "FGMRES solve-phase ms/iteration (HBM GB/s fraction in roofline)"
+UNIT = "ms/iteration"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path:
+            return None
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(parts[1]), smax=float(parts[2]), hw=parts[5], hwt=parts[6],
+                                 swt=parts[7], pcap=parts[8]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        load = [r for r in rows if r["sm"] > 500] or rows
+        reasons = set()
+        for r in load:
+            for k, nm in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"), ("swt", "sw_thermal_slowdown"),
+                          ("pcap", "sw_power_cap")):
+                if r[k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median([r["sm"] for r in load])), "sm_max_mhz": max(r["smax"] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def algorithmic_bytes(stats, v, ld_iters, n):
+    """Algorithmic bytes per kernel class for the iterations executed.
+
+    trisolve: every stored factor entry once (value v + int32 column 4), the U
+    diagonal once, the right-hand side read and the solution written (2 v per row);
+    the up sweep adds the F_l entries (v + 4) and the read-modify-write of y (2 v
+    per row) plus the temporary (2 v per row).
+    gs: CGS2 pass j reads (j+1) basis columns + w (v per element) and passes 2-3 write w.
+    """
+    per = {}
+    down = up = last = 0
+    for st in stats["stages"]:
+        S = st["stage"]
+        fac = (S["nnz"] - S["rows"]) * (v + 4) + S["rows"] * v
+        down += fac + 2 * S["rows"] * v
+        up += fac + st["nnzF"] * (v + 4) + 5 * S["rows"] * v
+    S = stats["last"]
+    last = (S["nnz"] - S["rows"]) * (v + 4) + S["rows"] * v + 2 * S["rows"] * v
+    per["trisolve_down"] = down
+    per["trisolve_up"] = up
+    per["trisolve_last"] = last
+    nnz = stats["nnz"]
+    per["spmv"] = nnz * (v + 4) + 2 * n * v
+    ew = 0
+    wax = 0
+    for st in stats["stages"]:
+        k = st["k"]
+        ew += st["nnzE"] * (v + 4) + 2 * st["s"] * v + k * st["s"] * v
+        wax += k * st["s"] * v + 2 * st["s"] * v
+    per["ew"] = ew
+    per["waxpy"] = wax
+    gs = 0
+    for j in ld_iters:
+        gs += 3 * (j + 1) * n * v + 3 * n * v + 2 * n * v
+    per["gs_total"] = gs
+    return per
+
+
+def run_ours(args):
+    import torch
+    import paper_2205_03224_b200 as gm
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    name = args.config
+    prob, b, xt, prm = P.make_config(name, gpus=1)      # per-GPU problem (see "parallelism")
+    if args.ilu:
+        prm["ilu"] = args.ilu
+    t0 = time.time()
+    s = gm.Solver(prob.rowptr, prob.colidx, prob.values, prm["levels"], prm["subdomains"], prm["rank"],
+                  ilu=prm["ilu"], ilut_drop=prm["ilut_drop"], ilut_fill=prm["ilut_fill"], coords=prob.coords,
+                  device=local, cluster_ctas=args.cluster_ctas)
+    setup_s = time.time() - t0
+    stream = torch.cuda.current_stream()
+    bd = s.to_local(torch.from_numpy(b).to(f"cuda:{local}", dtype=s.torch_dtype))
+    K, W = args.steps, args.warmup
+    restart = prm["restart"]
+    # warm-up: W iterations (untimed)
+    s.solve(bd, rtol=1e-300, restart=restart, maxit=max(W, 1))
+    torch.cuda.synchronize()
+
+    def timed(profile):
+        if profile:
+            s.profile(True, reset=True)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = s.solve(bd, rtol=1e-300, restart=restart, maxit=K)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if profile:
+            s.profile(False)
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=f"cuda:{local}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, out
+
+    with ClockSampler(local) as clk:
+        ms, out = timed(False)
+    clocks = clk.summary()
+    its = out["its"]
+    assert its == K, (its, K)
+    ms_per = ms / its
+    # per-kernel CUDA-event timing over a second identical timed region
+    ms_prof, out2 = timed(True)
+    stats = s.stats()
+    kern = stats["kernels"]
+    v = 16 if prob.is_complex else 8
+    n = prob.n
+    iters_j = [j % restart for j in range(K)]
+    ab = algorithmic_bytes(stats, v, iters_j, n)
+    gb = {
+        "trisolve_down": ab["trisolve_down"] * K, "trisolve_up": ab["trisolve_up"] * K,
+        "trisolve_last": ab["trisolve_last"] * K, "spmv": ab["spmv"] * (K + 2),
+        "ew": ab["ew"] * K, "waxpy": ab["waxpy"] * K, "gs": ab["gs_total"],
+    }
+    peak, peak_src = peaks()
+    per_kernel = {}
+    for kname, d in kern.items():
+        if d["count"] == 0:
+            continue
+        rec = {"ms_total": round(d["ms"], 4), "launches": d["count"], "us_per_launch": round(1e3 * d["ms"] / d["count"], 2)}
+        if kname in gb and d["ms"] > 0:
+            gbs = gb[kname] / (d["ms"] * 1e-3) / 1e9
+            rec.update(algorithmic_GB=round(gb[kname] / 1e9, 4), GBps=round(gbs, 1), frac=round(gbs / peak, 4))
+        per_kernel[kname] = rec
+    dom = max((k for k in per_kernel if k in gb), key=lambda k: per_kernel[k]["ms_total"])
+    dd = per_kernel[dom]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": dd["GBps"], "peak": peak, "unit": "GB/s",
+                "frac": dd["frac"], "traffic": None, "peak_source": peak_src,
+                "bytes_per_launch": round(gb[dom] / dd["launches"]), "us_per_launch": dd["us_per_launch"]}
+    launches = int(sum(d["count"] for d in kern.values()))
+    # end-to-end: host vectors in natural order through gemslr_solve_host
+    bh = np.ascontiguousarray(b)
+    xh = np.zeros_like(bh)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    oute = s.solve_host(bh, rtol=1e-300, restart=restart, maxit=K, out=xh)
+    e2e_ms = (time.perf_counter() - t1) * 1e3 / oute["its"]
+    e2e = {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": round(bh.nbytes / K),
+           "d2h_bytes_per_step": round(xh.nbytes / K), "h2d_bytes_total": bh.nbytes, "d2h_bytes_total": xh.nbytes}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(prob, prm, s, b, args.cpu_iters)
+    line = {
+        "metric": METRIC, "value": round(ms_per, 4), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": round(ms_per, 4), "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128" if prob.is_complex else "f64", "data": "synthetic (seeded 7-pt Laplacian, b = A x_true)",
+        "config": {"workload": f"{name}: 3D 7-pt Laplacian {prob.dims[0]}x{prob.dims[1]}x{prob.dims[2]} per GPU, "
+                               f"l_ev={prm['levels']}, p={prm['subdomains']}, {prm['ilu'].upper()}(1e-3,10), "
+                               f"rank={prm['rank']}, restart={restart}",
+                   "n": n, "nnz": prob.nnz, "levels": stats["levels"], "fill": round(stats["fill"], 3),
+                   "parallelism": "1 GPU" if world == 1 else f"{world} independent per-GPU replicas (no inter-GPU coupling yet)",
+                   "l2": "working set (~2.4 GB) > 126 MB L2; no flush",
+                   "setup_s": round(setup_s, 2), "timed_region": f"{K} FGMRES iterations (maxit=K, unreachable rtol)"},
+        "roofline": roofline, "kernels": per_kernel, "ms_per_step_profiled": round(ms_prof / out2["its"], 4),
+        "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_baseline(prob, prm, s, b, iters):
+    """The oracle as it stands (single-threaded C++), bounded sample: `iters` FGMRES
+    iterations of the same workload on the same exported setup bundle."""
+    import oracle
+    from tests.bundle_io import Bundle
+    with tempfile.TemporaryDirectory() as d:
+        s.export(d)
+        B = Bundle(d)
+        st = B.structure()
+        t0 = time.perf_counter()
+        kind = oracle.ILU0 if prm["ilu"] == "ilu0" else oracle.ILUT
+        Pc = oracle.Precond(prob, st, ilu=(kind, prm["ilut_drop"], prm["ilut_fill"]))
+        for l in range(B.L):
+            lr = B.lowrank(l)
+            if lr is not None:
+                Pc.set_lowrank(l, lr[0], lr[2])
+        t_setup = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        out = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=iters)
+        dt = time.perf_counter() - t1
+    return {"value": round(1e3 * dt / out["its"], 2), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{out['its']} FGMRES iterations of the same {prob.n}-row workload (oracle factor setup "
+                      f"{t_setup:.1f}s excluded)", "threads": 1}
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from oracle import dense as D
+    name = args.config
+    prob, b, xt, prm = P.make_config(name, gpus=1)
+    t0 = time.perf_counter()
+    st = D.rcb_structure(prob.scipy(), prob.coords, prm["levels"], prm["subdomains"])
+    kind = oracle.ILU0 if prm["ilu"] == "ilu0" else oracle.ILUT
+    Pc = oracle.Precond(prob, st, ilu=(kind, prm["ilut_drop"], prm["ilut_fill"]))
+    D.arnoldi_lowrank(Pc, prm["rank"], seed=0)
+    setup = time.perf_counter() - t0
+    K, W = args.steps, args.warmup
+    oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=max(1, min(W, 1)))
+    t1 = time.perf_counter()
+    out = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=K)
+    dt = time.perf_counter() - t1
+    val = 1e3 * dt / out["its"]
+    line = {"impl": "reference", "metric": METRIC, "value": round(val, 2), "unit": UNIT, "n_gpus": 0, "steps": out["its"],
+            "warmup": W, "ms_per_step": round(val, 2), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded 7-pt Laplacian, b = A x_true)",
+            "config": {"workload": f"{name} per-GPU problem {prob.dims}", "n": prob.n, "setup_s": round(setup, 1)},
+            "cpu_baseline": {"value": round(val, 2), "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{out['its']} FGMRES iterations, oracle's own RCB structure, ILU and "
+                                       f"one-cycle Arnoldi low rank (setup {setup:.0f}s excluded)"},
+            "e2e": {"value": round(val, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--ilu", default=None)
+    ap.add_argument("--cluster-ctas", type=int, default=0)
+    ap.add_argument("--cpu-iters", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

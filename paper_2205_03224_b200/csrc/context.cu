@@ -27,6 +27,8 @@
 namespace gemslr {
 
 static constexpr int kNumSM = 148;
+long long *g_tri_dbg = nullptr;   // debug: per-chunk clock64 trace of block 0 (gemslr_debug_trace)
+static_assert(PIPE_SB == PIPE_SB_DEV && PIPE_NW == PIPE_NW_DEV, "pipeline constants");
 
 #define CK(x)                                                                          \
   do {                                                                                 \
@@ -84,9 +86,9 @@ struct Pool {                                   // owns every device allocation 
 };
 
 // ----------------------------------------------------------------- profiling
-enum KernelClass { KC_SPMV = 0, KC_TRI_DOWN, KC_TRI_UP, KC_TRI_LAST, KC_EW, KC_WAXPY, KC_GS, KC_FGM, KC_UTIL, KC_COUNT };
+enum KernelClass { KC_SPMV = 0, KC_TRI_DOWN, KC_TRI_UP, KC_TRI_LAST, KC_EW, KC_WAXPY, KC_GS, KC_FGM, KC_UTIL, KC_PACK, KC_COUNT };
 static const char *kKernelName[KC_COUNT] = {"spmv", "trisolve_down", "trisolve_up", "trisolve_last", "ew",
-                                            "waxpy", "gs", "fgmres_col", "util"};
+                                            "waxpy", "gs", "fgmres_col", "util", "pack_rhs"};
 
 struct Profiler {
   bool on = false;
@@ -149,6 +151,9 @@ struct StageDev {
   const int64_t *blk = nullptr;
   TriDev<D> L{}, U{};
   int depthL = 0, depthU = 0;
+  bool pipe = false;       // TMA-pipelined kernel (k_tri_pipe) instead of the level kernel
+  PipeDev<D> P{};
+  int64_t nchunks = 0, far = 0, nearc = 0;
   int64_t nnz = 0;         // real stored nonzeros (L + U incl. diagonal)
   int64_t padded = 0;      // stored entries incl. padding
 };
@@ -259,6 +264,22 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
   d.U = up(S.Up);
   d.depthL = S.Lp.max_depth;
   d.depthU = S.Up.max_depth;
+  if (S.pipe.ok && cps_override <= 0 && d.nblk > 0) {
+    static_assert(sizeof(ChunkDesc) == sizeof(ChunkDev), "chunk descriptor layout");
+    d.pipe = true;
+    d.P.blob = P.upload<unsigned char>(S.pipe.blob, s);
+    d.P.chunks = P.upload<ChunkDev>(S.pipe.chunks, s);
+    d.P.blk_chunk = P.upload<int>(S.pipe.blk_chunk, s);
+    d.P.blk_nl = P.upload<int>(S.pipe.blk_nl, s);
+    d.P.lpos = P.upload<int>(S.pipe.lpos, s);
+    d.P.row0 = S.blk.front();
+    d.P.rhsL = P.get<D>(std::max<int64_t>(S.pipe.lslices * 32, 1));
+    d.P.rhsU = P.get<D>(std::max<int64_t>(S.pipe.uslices * 32, 1));
+    d.P.ring = S.pipe.ring;
+    d.nchunks = (int64_t)S.pipe.chunks.size();
+    d.far = S.pipe.far;
+    d.nearc = S.pipe.near;
+  }
   d.nnz = S.Lp.nnz_real + S.Up.nnz_real + (int64_t)d.rows;
   d.padded = (int64_t)S.Lp.val.size() + (int64_t)S.Up.val.size() + (int64_t)S.Up.diag.size();
   // CTAs per block: enough to cover the average rows of one level with 8-warp CTAs,
@@ -343,17 +364,43 @@ void Engine<T>::upload(cudaStream_t s) {
 }
 
 // ----------------------------------------------------------------- launches
+static int grid_for(int64_t units, int per_sm) {
+  int64_t g = std::min<int64_t>(units, (int64_t)kNumSM * per_sm);
+  return (int)std::max<int64_t>(g, 1);
+}
+
 template <typename D>
 static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *rhs, D *x, D *tmp,
                             const CsrDev<D> *F, int64_t Fbase, const int *doneflag, int kc) {
   if (S.nblk <= 0 || S.rows == 0) return;
-  Timed t(ctx->prof, ctx->stream, kc);
   const int64_t *Fp = F ? F->ptr : nullptr;
   const int32_t *Fc = F ? F->col : nullptr;
   const D *Fv = F ? F->val : nullptr;
-  if (S.cps <= 1) {
+  if (S.pipe) {
+    const size_t smem = pipe_smem_bytes<D>(S.P.ring);
+    static bool attr_set = false;
+    if (!attr_set) {
+      CK(cudaFuncSetAttribute(k_tri_pipe<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK(cudaFuncSetAttribute(k_tri_pipe<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_set = true;
+    }
+    {
+      Timed tp(ctx->prof, ctx->stream, KC_PACK);
+      const int grid = grid_for((S.rows + 255) / 256, 4);
+      k_pack_rhs<D><<<grid, 256, 0, ctx->stream>>>(S.rows, S.P.row0, S.P.lpos, S.P.rhsL, mode == TRI_DOWN ? rhs : nullptr,
+                                                   Fp, Fc, Fv, Fbase, x, doneflag);
+    }
+    Timed t(ctx->prof, ctx->stream, kc);
+    long long *dbg = kc == KC_TRI_DOWN ? g_tri_dbg : nullptr;
+    if (S.far > 0)
+      k_tri_pipe<D, true><<<S.nblk, 32 * (PIPE_NW_DEV + 1), smem, ctx->stream>>>(S.P, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag, dbg);
+    else
+      k_tri_pipe<D, false><<<S.nblk, 32 * (PIPE_NW_DEV + 1), smem, ctx->stream>>>(S.P, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag, dbg);
+  } else if (S.cps <= 1) {
+    Timed t(ctx->prof, ctx->stream, kc);
     k_trisolve<D, false><<<S.nblk, 256, 0, ctx->stream>>>(S.L, S.U, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag);
   } else {
+    Timed t(ctx->prof, ctx->stream, kc);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(S.nblk * S.cps);
     cfg.blockDim = dim3(256);
@@ -369,11 +416,6 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
     CK(cudaLaunchKernelEx(&cfg, k_trisolve<D, true>, S.L, S.U, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag));
   }
   CK(cudaGetLastError());
-}
-
-static int grid_for(int64_t units, int per_sm) {
-  int64_t g = std::min<int64_t>(units, (int64_t)kNumSM * per_sm);
-  return (int)std::max<int64_t>(g, 1);
 }
 
 template <typename T>
@@ -947,7 +989,9 @@ std::string Engine<T>::stats_json() const {
   auto stage = [&](const StageDev<D> &S) {
     return "{\"blocks\": " + std::to_string(S.nblk) + ", \"rows\": " + std::to_string(S.rows) + ", \"cps\": " +
            std::to_string(S.cps) + ", \"depth_L\": " + std::to_string(S.depthL) + ", \"depth_U\": " +
-           std::to_string(S.depthU) + ", \"nnz\": " + std::to_string(S.nnz) + ", \"padded\": " + std::to_string(S.padded) + "}";
+           std::to_string(S.depthU) + ", \"nnz\": " + std::to_string(S.nnz) + ", \"padded\": " + std::to_string(S.padded) +
+           ", \"pipe\": " + (S.pipe ? "true" : "false") + ", \"chunks\": " + std::to_string(S.nchunks) +
+           ", \"far\": " + std::to_string(S.far) + ", \"near\": " + std::to_string(S.nearc) + "}";
   };
   j += ", \"stages\": [";
   for (size_t l = 0; l < lev.size(); ++l) {
@@ -1247,6 +1291,10 @@ gemslr_status gemslr_stats(const gemslr_ctx *c, char *json, size_t cap) {
   std::snprintf(json, cap, "%s", j.c_str());
   return j.size() + 1 > cap ? GEMSLR_ERR_INVALID_ARG : GEMSLR_OK;
 }
+
+// Debug hook (not in gemslr.h): record a clock64 trace of block 0 of the down-sweep
+// trisolve launches into a device buffer of 4 * 4096 int64.
+extern "C" void gemslr_debug_trace(void *dev_buf) { g_tri_dbg = static_cast<long long *>(dev_buf); }
 
 gemslr_status gemslr_profile(gemslr_ctx *c, int enable, int reset) {
   if (!c) return GEMSLR_ERR_INVALID_ARG;

@@ -21,6 +21,9 @@
 
 namespace gemslr {
 
+constexpr int PIPE_SB_DEV = 16 * 1024;    // = PIPE_SB
+constexpr int PIPE_NW_DEV = 8;            // = PIPE_NW
+
 // ----------------------------------------------------------------- scalars
 struct cd {
   double x, y;
@@ -199,6 +202,253 @@ __global__ void __launch_bounds__(256) k_trisolve(TriDev<T> Lp, TriDev<T> Up, co
   }
   if (mode == TRI_UP)
     for (int64_t i = r0 + gt; i < r1; i += nt) x[i] = x[i] - ldv(tmp + i);   // y1 = z1 - U^-1 L^-1 F y2
+}
+
+// ----------------------------------------------------------------- K4/K5/K9 pipelined
+// One CTA per block.  The factor data of the block's two sweeps is streamed
+// chunk by chunk (<= 8 slices of one level) by 1D bulk copies (TMA,
+// cp.async.bulk -> UBLKCP) into a pipe_stages<T>()-deep shared-memory ring
+// with mbarrier completion, issued that many chunks ahead of the consumers; the
+// solution values of the last `ring` packed positions stay in shared memory
+// so a dependency costs a shared-memory load instead of an L2 round trip.
+// One __syncthreads per chunk orders the levels and frees the stage.
+struct ChunkDev {
+  long long blob_off, rhs_off;
+  int bytes, ns, flags, pad;
+};
+template <typename T>
+struct PipeDev {
+  const unsigned char *blob;
+  const ChunkDev *chunks;
+  const int *blk_chunk;
+  const int *blk_nl;
+  const int *lpos;       // per stage row: packed L right-hand-side index
+  long long row0;        // first row of the stage
+  T *rhsL, *rhsU;        // packed right-hand sides of the L and U sweeps
+  int ring;
+};
+
+__device__ inline unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ inline void mbar_init(unsigned long long *b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ inline void mbar_expect_tx(unsigned long long *b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ inline void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+__device__ inline void mbar_wait(unsigned long long *b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n"
+      "DONE:\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ inline void mbar_arrive(unsigned long long *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ inline bool mbar_test(unsigned long long *b, unsigned parity) {
+  unsigned r;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(r)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return r != 0;
+}
+__device__ inline void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"r"(32 * PIPE_NW_DEV) : "memory"); }
+
+__device__ inline void cp_async_8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ inline void cp_async_16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ inline void cp_async_arrive_noinc(unsigned long long *b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+template <typename T> __host__ __device__ constexpr int pipe_stages() { return sizeof(T) == 8 ? 8 : 7; }
+template <typename T> __host__ __device__ constexpr size_t pipe_smem_bytes(int ring) {
+  return (size_t)ring * sizeof(T) + (size_t)pipe_stages<T>() * (PIPE_SB_DEV + 32 * PIPE_NW_DEV * sizeof(T)) +
+         (size_t)(2 * pipe_stages<T>() + 2) * 8;
+}
+__device__ inline void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Warp-specialised: warps 0..PIPE_NW-1 consume (one SELL slice of the chunk
+// each); warp PIPE_NW produces.  Per stage s:
+//   full[s]  the chunk's blob AND its packed right-hand sides landed (two bulk
+//            copies, one complete_tx barrier);
+//   empty[s] every consumer warp is done with stage s.
+// The right-hand sides are packed in chunk order: the L sweep's by k_pack_rhs
+// (a full-GPU kernel launched just before), the U sweep's (= the L results)
+// by the consumers as they compute them (gate[1] after the last L chunk,
+// crossed with fence.proxy.async so the bulk copies (async proxy) see the
+// generic-proxy stores).  Consumers order the levels with a named
+// barrier among themselves only.
+template <typename T, bool FAR>
+__global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<T> P, const int64_t *__restrict__ blk, int mode,
+                                                                     const T *rhs, T *x, T *tmp,
+                                                                     const int64_t *__restrict__ Fptr,
+                                                                     const int32_t *__restrict__ Fcol,
+                                                                     const T *__restrict__ Fval, int64_t Fbase,
+                                                                     const int *__restrict__ done, long long *dbg) {
+  if (done && *done) return;
+  constexpr int NS = pipe_stages<T>();
+  constexpr int NCONS = 32 * PIPE_NW_DEV;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int R = P.ring;
+  T *ring = reinterpret_cast<T *>(smem);
+  unsigned char *stages = smem + (size_t)R * sizeof(T);
+  T *rslot = reinterpret_cast<T *>(stages + (size_t)NS * PIPE_SB_DEV);
+  unsigned long long *full = reinterpret_cast<unsigned long long *>(rslot + (size_t)NS * NCONS);
+  unsigned long long *empty = full + NS;
+  unsigned long long *gate = empty + NS;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c0 = P.blk_chunk[b], nc = P.blk_chunk[b + 1] - c0;
+  const int64_t r0 = blk[b], r1 = blk[b + 1];
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], PIPE_NW_DEV);
+    }
+    mbar_init(&gate[1], PIPE_NW_DEV);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < R; i += blockDim.x) ring[i] = dzero<T>();
+  __syncthreads();
+  T *out = (mode == TRI_DOWN) ? x : tmp;
+  if (warp == PIPE_NW_DEV) {                                       // ---- producer warp
+    // descriptors are loaded 32 at a time (one per lane, next batch prefetched)
+    // and broadcast with shuffles, so the issue loop never waits on memory
+    bool g1 = false;
+    ChunkDev cur{}, nxt{};
+    if (lane < nc) cur = P.chunks[c0 + lane];
+    for (int base = 0; base < nc; base += 32) {
+      if (base + 32 + lane < nc) nxt = P.chunks[c0 + base + 32 + lane];
+      const int cnt = min(32, nc - base);
+      for (int j = 0; j < cnt; ++j) {
+        const int k = base + j;
+        const long long boff = __shfl_sync(0xffffffffu, cur.blob_off, j);
+        const long long roff = __shfl_sync(0xffffffffu, cur.rhs_off, j);
+        const int bytes = __shfl_sync(0xffffffffu, cur.bytes, j);
+        const int ns = __shfl_sync(0xffffffffu, cur.ns, j);
+        const int flags = __shfl_sync(0xffffffffu, cur.flags, j);
+        if (lane == 0) {
+          const int st = k % NS;
+          const bool upper = flags & 1;
+          if (upper && !g1) { mbar_wait(&gate[1], 0); g1 = true; }
+          if (k >= NS) mbar_wait(&empty[st], (unsigned)(((k / NS) - 1) & 1));
+          const unsigned rb = (unsigned)(ns * 32 * sizeof(T));
+          mbar_expect_tx(&full[st], (unsigned)bytes + rb);
+          bulk_g2s(stages + (size_t)st * PIPE_SB_DEV, P.blob + boff, (unsigned)bytes, &full[st]);
+          bulk_g2s(rslot + (size_t)st * NCONS, (upper ? P.rhsU : P.rhsL) + roff, rb, &full[st]);
+          if (dbg && b == 0 && k < 4096) dbg[4 * k + 3] = clock64();
+        }
+        __syncwarp();
+      }
+      cur = nxt;
+    }
+    return;
+  }
+  // ---- consumer warps (the L right-hand sides were packed by k_pack_rhs)
+  const int nL = P.blk_nl[b];
+  for (int k = 0; k < nc; ++k) {
+    const int st = k % NS;
+    if (dbg && b == 0 && tid == 0 && k < 4096) dbg[4 * k] = clock64();
+    mbar_wait(&full[st], (unsigned)((k / NS) & 1));
+    if (dbg && b == 0 && tid == 0 && k < 4096) dbg[4 * k + 1] = clock64();
+    const unsigned char *blob = stages + (size_t)st * PIPE_SB_DEV;
+    const int *hdr = reinterpret_cast<const int *>(blob);
+    const int ns = hdr[0], s0 = hdr[1], ne = hdr[2];
+    const bool upper = hdr[3] & 1;
+    const int H = (ns + 5 + 3) & ~3;
+    const int *rows = hdr + H;
+    const int *aux = rows + ns * 32;
+    const T *diag = reinterpret_cast<const T *>(aux + ns * 32);
+    const int *col = reinterpret_cast<const int *>(diag + ns * 32);
+    const T *val = reinterpret_cast<const T *>(col + ne);
+    if (warp < ns) {
+      const int row = rows[warp * 32 + lane];
+      if (row >= 0) {
+        T acc = rslot[(size_t)st * NCONS + warp * 32 + lane];
+        const int e0 = hdr[4 + warp], w = (hdr[5 + warp] - e0) >> 5;
+        const int *cp = col + e0 + lane;
+        const T *vp = val + e0 + lane;
+        if (FAR) {
+          for (int e = 0; e < w; ++e) {
+            const int c = cp[32 * e];
+            const T v = vp[32 * e];
+            if (c >= 0) acc -= v * ring[c & (R - 1)];
+            else if (c <= -2) acc -= v * out[-c - 2];
+          }
+        } else {
+          // branch-free: padding has value 0 and column -1 (ring slot R-1, finite
+          // because the ring is zero-initialised); two partial sums shorten the
+          // dependent DFMA chain
+          T acc1 = dzero<T>();
+          int e = 0;
+#pragma unroll 4
+          for (; e + 2 <= w; e += 2) {
+            const int ca = cp[32 * e], cb = cp[32 * (e + 1)];
+            const T va = vp[32 * e], vb = vp[32 * (e + 1)];
+            acc -= va * ring[ca & (R - 1)];
+            acc1 -= vb * ring[cb & (R - 1)];
+          }
+          if (e < w) acc -= vp[32 * e] * ring[cp[32 * e] & (R - 1)];
+          acc += acc1;
+        }
+        if (upper) acc = acc * diag[warp * 32 + lane];             // diag holds 1 / u_ii
+        else P.rhsU[aux[warp * 32 + lane]] = acc;              // right-hand side of the U sweep
+        ring[((s0 + warp) * 32 + lane) & (R - 1)] = acc;
+        out[row] = acc;
+      }
+    }
+    __syncwarp();
+    if (dbg && b == 0 && tid == 0 && k < 4096) dbg[4 * k + 2] = clock64();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (k == nL - 1) {                                             // L sweep done: release the U right-hand sides
+      fence_proxy_async_global();
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&gate[1]);
+    }
+    consumer_sync();
+  }
+  if (mode == TRI_UP)
+    for (int64_t i = r0 + tid; i < r1; i += NCONS) x[i] = x[i] - tmp[i];   // y1 = z1 - U^-1 L^-1 F y2
+}
+
+// Packs the L-sweep right-hand sides of a stage in chunk order:
+// DOWN: dst[lpos[i]] = src[row0 + i];  UP: dst[lpos[i]] = (F_l y_J)_{row0 + i}.
+template <typename T>
+__global__ void __launch_bounds__(256) k_pack_rhs(int64_t nrows, int64_t row0, const int *__restrict__ lpos, T *__restrict__ dst,
+                                                  const T *__restrict__ src, const int64_t *__restrict__ Fptr,
+                                                  const int32_t *__restrict__ Fcol, const T *__restrict__ Fval,
+                                                  int64_t Fbase, const T *__restrict__ y, const int *__restrict__ done) {
+  if (done && *done) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    T v;
+    if (src) {
+      v = src[row0 + i];
+    } else {
+      const int64_t li = row0 + i - Fbase;
+      v = dzero<T>();
+      for (int64_t p = Fptr[li]; p < Fptr[li + 1]; ++p) v += Fval[p] * y[Fcol[p]];
+    }
+    dst[lpos[i]] = v;
+  }
 }
 
 // ----------------------------------------------------------------- K6+K7

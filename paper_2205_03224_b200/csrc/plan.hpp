@@ -80,10 +80,46 @@ struct TriPack {
   int64_t nnz_real = 0;                         // stored nonzeros without padding
 };
 
+// TMA-pipelined form of a stage's two sweeps (k_tri_pipe): per block, the L
+// chunks then the U chunks; a chunk is <= PIPE_NW slices of ONE level whose
+// static data is one contiguous, 128-byte aligned blob of <= PIPE_SB bytes:
+//   int32 header: ns, s0 (block-relative first slice), ne, flags (bit0 = U
+//     sweep), ns + 1 relative entry offsets, padded to 16 bytes;
+//   int32 rows[ns*32]; int32 aux[ns*32] (L chunks: packed U index of the row);
+//   T diag[ns*32] (U sweep: 1/u_ii; 1 in L chunks); int32 col[ne]; T val[ne].
+// The right-hand sides of a chunk are contiguous in a packed per-sweep vector
+// (index = stage slice * 32 + lane) and arrive by a second bulk copy.
+// Column encoding: c >= 0 block-relative position (slice * 32 + lane) of the
+// dependency, read from the shared-memory ring of the last `ring` solution
+// values; c == -1 padding; c <= -2 "far" dependency read from global memory
+// at row -c - 2.
+struct ChunkDesc {
+  int64_t blob_off;
+  int64_t rhs_off;                          // first packed right-hand-side index
+  int32_t bytes, ns, flags, pad;            // flags bit0: U sweep
+};
+constexpr int PIPE_NW = 8;                  // consumer warps per CTA = max slices per chunk
+constexpr int PIPE_SB = 16 * 1024;          // blob bytes per pipeline stage
+constexpr int PIPE_RING_BYTES = 64 * 1024;  // solution window
+
+template <typename T>
+struct PipePack {
+  bool ok = false;
+  int ring = 0;                             // entries (power of two)
+  std::vector<uint8_t> blob;
+  std::vector<ChunkDesc> chunks;
+  std::vector<int32_t> blk_chunk;           // per block: [blk_chunk[b], blk_chunk[b+1])
+  std::vector<int32_t> blk_nl;              // per block: number of L chunks
+  std::vector<int32_t> lpos;                // per stage row: packed L index
+  int64_t lslices = 0, uslices = 0;
+  int64_t near = 0, far = 0;
+};
+
 template <typename T>
 struct Stage {                                  // the blocks of one level (or of C_last)
   std::vector<int64_t> blk;                     // absolute boundaries (empty blocks removed)
   TriPack<T> Lp, Up;
+  PipePack<T> pipe;
 };
 
 template <typename T>

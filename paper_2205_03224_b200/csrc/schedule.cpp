@@ -90,6 +90,118 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
   }
 }
 
+// Chunk the level-scheduled sweeps of every block into TMA blobs (PipePack).
+template <typename T>
+void pack_pipe(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPack<T> &Up, PipePack<T> &P) {
+  P = PipePack<T>();
+  P.ring = PIPE_RING_BYTES / (int)sizeof(T);
+  const int R = P.ring;
+  const size_t nb = blk.size() - 1;
+  const int64_t R0 = blk.front(), NR = blk.back() - blk.front();
+  P.blk_chunk.push_back(0);
+  P.lslices = (int64_t)Lp.slice_row.size() / 32;
+  P.uslices = (int64_t)Up.slice_row.size() / 32;
+  // packed index (slice * 32 + lane, stage-global) of every row in each sweep
+  std::vector<int32_t> upos(NR, -1);
+  P.lpos.assign(NR, -1);
+  for (int64_t s = 0; s < P.lslices; ++s)
+    for (int lane = 0; lane < 32; ++lane) {
+      const int32_t row = Lp.slice_row[s * 32 + lane];
+      if (row >= 0) P.lpos[row - R0] = (int32_t)(s * 32 + lane);
+    }
+  for (int64_t s = 0; s < P.uslices; ++s)
+    for (int lane = 0; lane < 32; ++lane) {
+      const int32_t row = Up.slice_row[s * 32 + lane];
+      if (row >= 0) upos[row - R0] = (int32_t)(s * 32 + lane);
+    }
+  auto align = [](size_t v, size_t a) { return (v + a - 1) / a * a; };
+  auto blob_bytes = [&](int32_t ns, size_t ne) {
+    return align((size_t)(ns + 5), 4) * 4 + (size_t)ns * 32 * 4 * 2 + (size_t)ns * 32 * sizeof(T) + ne * (4 + sizeof(T));
+  };
+  for (size_t b = 0; b < nb; ++b) {
+    int32_t nL = 0;
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      const TriPack<T> &S = sweep ? Up : Lp;
+      const bool upper = sweep == 1;
+      const int32_t lv0 = S.blk_lev[b], lv1 = S.blk_lev[b + 1];
+      if (lv1 <= lv0) continue;
+      const int32_t sb0 = S.lev_slice[lv0];
+      // chunk boundaries: <= PIPE_NW slices of one level, blob <= PIPE_SB bytes
+      struct Ch { int32_t s0, s1; };
+      std::vector<Ch> ch;
+      for (int32_t v = lv0; v < lv1; ++v) {
+        int32_t s = S.lev_slice[v];
+        while (s < S.lev_slice[v + 1]) {
+          Ch c{s, s};
+          size_t ne = 0;
+          while (c.s1 < S.lev_slice[v + 1] && c.s1 - c.s0 < PIPE_NW) {
+            const size_t e2 = ne + (size_t)(S.slice_off[c.s1 + 1] - S.slice_off[c.s1]);
+            if (blob_bytes(c.s1 + 1 - c.s0, e2) > (size_t)PIPE_SB) {
+              if (c.s1 == c.s0) return;             // one slice does not fit: no pipelined form
+              break;
+            }
+            ne = e2;
+            c.s1++;
+          }
+          ch.push_back(c);
+          s = c.s1;
+        }
+      }
+      for (const Ch &c : ch) {
+        const int32_t ns = c.s1 - c.s0;
+        const int64_t e0 = S.slice_off[c.s0], e1 = S.slice_off[c.s1];
+        const int32_t ne = (int32_t)(e1 - e0);
+        const size_t H = align((size_t)(ns + 5), 4);
+        const size_t bytes = blob_bytes(ns, (size_t)ne);
+        const size_t off = align(P.blob.size(), 128);
+        P.blob.resize(off + bytes, 0);
+        uint8_t *base = P.blob.data() + off;
+        int32_t *hdr = reinterpret_cast<int32_t *>(base);
+        int32_t *rows = hdr + H;
+        int32_t *aux = rows + ns * 32;
+        T *diag = reinterpret_cast<T *>(aux + ns * 32);
+        int32_t *col = reinterpret_cast<int32_t *>(diag + ns * 32);
+        T *val = reinterpret_cast<T *>(col + ne);
+        const int32_t send = c.s1 - sb0;              // chunk end (block-relative slice)
+        hdr[0] = ns;
+        hdr[1] = c.s0 - sb0;
+        hdr[2] = ne;
+        hdr[3] = upper ? 1 : 0;
+        for (int32_t i = 0; i < ns; ++i) {
+          const int32_t s = c.s0 + i;
+          hdr[4 + i] = (int32_t)(S.slice_off[s] - e0);
+          for (int lane = 0; lane < 32; ++lane) {
+            const int32_t row = S.slice_row[(int64_t)s * 32 + lane];
+            rows[i * 32 + lane] = row;
+            aux[i * 32 + lane] = (!upper && row >= 0) ? upos[row - R0] : -1;
+            diag[i * 32 + lane] = upper ? T(1) / S.diag[(int64_t)s * 32 + lane] : T(1);   // reciprocal
+          }
+          const int w = (int)((S.slice_off[s + 1] - S.slice_off[s]) / 32);
+          for (int e = 0; e < w; ++e)
+            for (int lane = 0; lane < 32; ++lane) {
+              const int64_t g = S.slice_off[s] + 32 * e + lane;
+              const int64_t l = g - e0;
+              const int32_t dep = S.col[g];
+              val[l] = S.val[g];
+              if (dep < 0) { col[l] = -1; continue; }
+              const int32_t pd = sweep ? upos[dep - R0] : P.lpos[dep - R0];
+              const int32_t q = pd - sb0 * 32;          // block-relative position
+              if ((int64_t)send * 32 - 1 - q < R) { col[l] = q; P.near++; }
+              else { col[l] = -dep - 2; P.far++; }
+            }
+        }
+        hdr[4 + ns] = ne;
+        P.chunks.push_back(ChunkDesc{(int64_t)off, (int64_t)c.s0 * 32, (int32_t)bytes, ns, upper ? 1 : 0, 0});
+        if (!upper) nL++;
+      }
+    }
+    P.blk_chunk.push_back((int32_t)P.chunks.size());
+    P.blk_nl.push_back(nL);
+  }
+  P.blob.resize(align(P.blob.size(), 128), 0);
+  P.ok = true;
+}
+
 }  // namespace
 
 template <typename T>
@@ -97,6 +209,7 @@ void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
   S.blk = blk;
   pack_sweep(blk, fac, false, S.Lp);
   pack_sweep(blk, fac, true, S.Up);
+  pack_pipe(blk, S.Lp, S.Up, S.pipe);
 }
 
 template void pack_stage<double>(const std::vector<int64_t> &, const std::vector<Factor<double>> &, Stage<double> &);
