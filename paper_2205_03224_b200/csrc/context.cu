@@ -486,8 +486,15 @@ template <typename T>
 void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv, int upd, int dot, const D *h_in,
                         D *resv, int ticket, const int *doneflag) {
   Timed t(ctx->prof, ctx->stream, KC_GS);
-  const int grid = grid_for((nn + 31) / 32, 4);
-  k_gs<D><<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv, doneflag);
+  // 13 values of V in flight per thread whatever the number of columns
+  auto go = [&](auto kern, int tr) {
+    const int grid = grid_for((nn + 32 * tr - 1) / (32 * tr), 3);
+    kern<<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv, doneflag);
+  };
+  if (ncols <= 8) go(k_gs<D, 8, 1>, 8);
+  else if (ncols <= 24) go(k_gs<D, 4, 3>, 4);
+  else if (ncols <= 48) go(k_gs<D, 2, 6>, 2);
+  else go(k_gs<D, 1, 13>, 1);
   CK(cudaGetLastError());
 }
 

@@ -548,62 +548,82 @@ __global__ void __launch_bounds__(256) k_waxpy(int64_t s, int64_t rowbase, const
 //   pass 2 (upd = 1, dot = 1): w -= V h_in ; res = [V^H w, ||w||^2]
 //   pass 3 (upd = 1, dot = 0): w -= V h_in ; res = [||w||^2]
 // Results are reduced in fixed CTA order by the last CTA (ticket).
-constexpr int GS_NPW = 13;                 // columns per warp
-constexpr int GS_MAXC = 8 * GS_NPW;        // 104 >= restart + 1
-template <typename T>
+// A step covers TR 32-row tiles; warp w owns the columns w + 8a, a < NPW, with
+// TR * NPW <= 13 values of V in registers (instances chosen by ncols so the
+// loads in flight per thread stay ~13 however many columns there are).
+constexpr int GS_MAXC = 104;               // >= restart + 1
+template <typename T, int TR, int NPW>
 __global__ void __launch_bounds__(256) k_gs(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
                                             int dot, const T *__restrict__ h_in, T *__restrict__ partial,
                                             unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
   if (done && *done) return;
-  __shared__ T su[8][32];
+  __shared__ T su[8][32 * TR];
   __shared__ T sh[GS_MAXC];
   __shared__ bool amlast;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (upd)
     for (int c = tid; c < ncols; c += blockDim.x) sh[c] = h_in[c];
   __syncthreads();
-  T acc[GS_NPW];
+  T acc[NPW];
 #pragma unroll
-  for (int a = 0; a < GS_NPW; ++a) acc[a] = dzero<T>();
+  for (int a = 0; a < NPW; ++a) acc[a] = dzero<T>();
   double nrm = 0.0;
-  const int64_t ntiles = (n + 31) / 32;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t i = tile * 32 + lane;
-    const bool ok = i < n;
-    T vr[GS_NPW];
+  const int64_t nsteps = (n + 32 * TR - 1) / (32 * TR);
+  for (int64_t step = blockIdx.x; step < nsteps; step += gridDim.x) {
+    const int64_t base = step * 32 * TR + lane;
+    T vr[TR][NPW];
+    T wi[TR];
 #pragma unroll
-    for (int a = 0; a < GS_NPW; ++a) {
-      const int c = warp + 8 * a;
-      vr[a] = (ok && c < ncols) ? ld_nc(V + c * ldv + i) : dzero<T>();
-    }
-    T wi = ok ? w[i] : dzero<T>();
-    if (upd) {
-      T u = dzero<T>();
+    for (int r = 0; r < TR; ++r) {
+      const int64_t i = base + 32 * r;
+      const bool ok = i < n;
 #pragma unroll
-      for (int a = 0; a < GS_NPW; ++a) {
+      for (int a = 0; a < NPW; ++a) {
         const int c = warp + 8 * a;
-        if (c < ncols) u += vr[a] * sh[c];
+        vr[r][a] = (ok && c < ncols) ? ld_nc(V + c * ldv + i) : dzero<T>();
       }
-      su[warp][lane] = u;
-      __syncthreads();
-      T tot = dzero<T>();
+      wi[r] = ok ? w[i] : dzero<T>();
+    }
+    if (upd) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) tot += su[q][lane];
-      wi = wi - tot;
+      for (int r = 0; r < TR; ++r) {
+        T u = dzero<T>();
+#pragma unroll
+        for (int a = 0; a < NPW; ++a) {
+          const int c = warp + 8 * a;
+          if (c < ncols) u += vr[r][a] * sh[c];
+        }
+        su[warp][r * 32 + lane] = u;
+      }
       __syncthreads();
-      if (warp == 0 && ok) w[i] = wi;
+#pragma unroll
+      for (int r = 0; r < TR; ++r) {
+        T tot = dzero<T>();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tot += su[q][r * 32 + lane];
+        wi[r] = wi[r] - tot;
+      }
+      __syncthreads();
+      if (warp == 0)
+#pragma unroll
+        for (int r = 0; r < TR; ++r)
+          if (base + 32 * r < n) w[base + 32 * r] = wi[r];
     }
     if (dot) {
 #pragma unroll
-      for (int a = 0; a < GS_NPW; ++a) acc[a] += dconj(vr[a]) * wi;
+      for (int r = 0; r < TR; ++r)
+#pragma unroll
+        for (int a = 0; a < NPW; ++a) acc[a] += dconj(vr[r][a]) * wi[r];
     }
-    if (warp == 0) nrm += dabs2(wi);
+    if (warp == 0)
+#pragma unroll
+      for (int r = 0; r < TR; ++r) nrm += dabs2(wi[r]);
   }
   // per-warp reduction; warp w owns its columns, warp 0 owns the norm
   const int nres = dot ? ncols + 1 : 1;
   if (dot) {
 #pragma unroll
-    for (int a = 0; a < GS_NPW; ++a) {
+    for (int a = 0; a < NPW; ++a) {
       const int c = warp + 8 * a;
       T r = warp_sum(acc[a]);
       if (lane == 0 && c < ncols) partial[(int64_t)blockIdx.x * nres + c] = r;
