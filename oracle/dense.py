@@ -188,3 +188,97 @@ def pattern_equal(A, Bm):
     A.sort_indices()
     Bm.sort_indices()
     return np.array_equal(A.indptr, Bm.indptr) and np.array_equal(A.indices, Bm.indices)
+
+
+# ---------------------------------------------------------------------------
+# vectorised setup for the bench reference arm (oracle-only; timing, not parity)
+# ---------------------------------------------------------------------------
+def rcb_structure(A, coords, levels, p, nlast=None):
+    """Multilevel p-way vertex separators (Alg. 3) by recursive
+    coordinate bisection, vectorised for large grids.  Same rules as
+    tiny_structure: a vertex joins the separator when it has a neighbour of
+    higher part id; stop when the separator has < 2p vertices."""
+    A = sp.csr_matrix(A)
+    G = _sym_graph(A).tocoo()
+    n = A.shape[0]
+    current = np.arange(n)
+    perm_parts, level_off, blocks = [], [0], []
+    pos = 0
+
+    def bisect(verts, q, first, part):
+        if q == 1:
+            part[verts] = first
+            return
+        qa = q // 2
+        c = coords[verts]
+        ax = int(np.argmax(c.max(axis=0) - c.min(axis=0)))
+        order = verts[np.lexsort((verts, c[:, ax]))]
+        na = len(verts) * qa // q
+        bisect(np.sort(order[:na]), qa, first, part)
+        bisect(np.sort(order[na:]), q - qa, first + qa, part)
+
+    for l in range(levels):
+        if len(current) < 2 * p and l > 0:
+            break
+        part = -np.ones(n, dtype=np.int64)
+        bisect(current, p, 0, part)
+        u, v = G.row, G.col
+        m = (part[u] >= 0) & (part[v] >= 0) & (part[v] > part[u])
+        insep = np.zeros(n, dtype=bool)
+        insep[u[m]] = True
+        sep = current[insep[current]]
+        bl = [pos]
+        inner_all = current[~insep[current]]
+        pa = part[inner_all]
+        order = np.lexsort((inner_all, pa))
+        inner_sorted = inner_all[order]
+        counts = np.bincount(pa, minlength=p)
+        perm_parts.append(inner_sorted)
+        for q in range(p):
+            pos += int(counts[q])
+            bl.append(pos)
+        blocks.append(np.array(bl, dtype=np.int64))
+        level_off.append(pos)
+        current = np.sort(sep)
+    perm_parts.append(current)
+    perm = np.concatenate(perm_parts).astype(np.int64)
+    s = len(current)
+    nlast = nlast or p
+    nlast = max(1, min(nlast, s))
+    last = level_off[-1] + np.array([s * q // nlast for q in range(nlast + 1)], dtype=np.int64)
+    return dict(perm=perm, level_off=np.array(level_off, dtype=np.int64), blocks=blocks, last_off=last)
+
+
+def arnoldi_lowrank(P, k, seed=0):
+    """Rank-k terms bottom-up from ONE Arnoldi cycle of length
+    m = 2k on Ĝ_l with CGS2, Schur of H_m sorted by
+    |γ/(1-γ)| (real Schur for real problems, pairs kept).  Installs W_l, G_l
+    into the oracle preconditioner.  (Reference-arm setup: no thick restart.)"""
+    if k <= 0:
+        return
+    rng = np.random.default_rng(seed)
+    L = len(P.o) - 1
+    for l in range(L - 1, -1, -1):
+        s = P.s(l)
+        if s == 0:
+            continue
+        m = min(2 * k, s)
+        V = np.zeros((s, m + 1), dtype=P.dtype)
+        H = np.zeros((m + 1, m), dtype=P.dtype)
+        v0 = rng.uniform(-1, 1, s).astype(P.dtype)
+        V[:, 0] = v0 / np.linalg.norm(v0)
+        mm = m
+        for j in range(m):
+            w = P.ghat(l, V[:, j])
+            h = V[:, :j + 1].conj().T @ w
+            w = w - V[:, :j + 1] @ h
+            h2 = V[:, :j + 1].conj().T @ w
+            w = w - V[:, :j + 1] @ h2
+            H[:j + 1, j] = h + h2
+            H[j + 1, j] = np.linalg.norm(w)
+            if H[j + 1, j] <= 1e-14 * np.linalg.norm(h):
+                mm = j + 1
+                break
+            V[:, j + 1] = w / H[j + 1, j]
+        W, R, G = lowrank_from_dense(H[:mm, :mm], k=min(k, mm))
+        P.set_lowrank(l, V[:, :mm] @ W, G)

@@ -212,9 +212,8 @@ __global__ void __launch_bounds__(256) k_trisolve(TriDev<T> Lp, TriDev<T> Up, co
 // solution values of the last `ring` packed positions stay in shared memory
 // so a dependency costs a shared-memory load instead of an L2 round trip.
 // One __syncthreads per chunk orders the levels and frees the stage.
-struct ChunkDev {
-  long long blob_off, rhs_off;
-  int bytes, ns, flags, pad;
+struct ChunkDev {          // = ChunkDesc: blob offset / 128, blob bytes, first slice, ns << 1 | U flag
+  int blob128, bytes, slice, nsflags;
 };
 template <typename T>
 struct PipeDev {
@@ -329,102 +328,129 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
   for (int i = tid; i < R; i += blockDim.x) ring[i] = dzero<T>();
   __syncthreads();
   T *out = (mode == TRI_DOWN) ? x : tmp;
-  if (warp == PIPE_NW_DEV) {                                       // ---- producer warp
-    // descriptors are loaded 32 at a time (one per lane, next batch prefetched)
-    // and broadcast with shuffles, so the issue loop never waits on memory
+  if (warp == PIPE_NW_DEV) {                                       // ---- producer (one lane)
+    if (lane != 0) return;
     bool g1 = false;
-    ChunkDev cur{}, nxt{};
-    if (lane < nc) cur = P.chunks[c0 + lane];
-    for (int base = 0; base < nc; base += 32) {
-      if (base + 32 + lane < nc) nxt = P.chunks[c0 + base + 32 + lane];
-      const int cnt = min(32, nc - base);
-      for (int j = 0; j < cnt; ++j) {
-        const int k = base + j;
-        const long long boff = __shfl_sync(0xffffffffu, cur.blob_off, j);
-        const long long roff = __shfl_sync(0xffffffffu, cur.rhs_off, j);
-        const int bytes = __shfl_sync(0xffffffffu, cur.bytes, j);
-        const int ns = __shfl_sync(0xffffffffu, cur.ns, j);
-        const int flags = __shfl_sync(0xffffffffu, cur.flags, j);
-        if (lane == 0) {
-          const int st = k % NS;
-          const bool upper = flags & 1;
-          if (upper && !g1) { mbar_wait(&gate[1], 0); g1 = true; }
-          if (k >= NS) mbar_wait(&empty[st], (unsigned)(((k / NS) - 1) & 1));
-          const unsigned rb = (unsigned)(ns * 32 * sizeof(T));
-          mbar_expect_tx(&full[st], (unsigned)bytes + rb);
-          bulk_g2s(stages + (size_t)st * PIPE_SB_DEV, P.blob + boff, (unsigned)bytes, &full[st]);
-          bulk_g2s(rslot + (size_t)st * NCONS, (upper ? P.rhsU : P.rhsL) + roff, rb, &full[st]);
-          if (dbg && b == 0 && k < 4096) dbg[4 * k + 3] = clock64();
-        }
-        __syncwarp();
-      }
-      cur = nxt;
+    // 16-byte descriptors, prefetched 4 chunks ahead in registers
+    const int4 *dsc = reinterpret_cast<const int4 *>(P.chunks) + c0;
+    int4 q0 = nc > 0 ? dsc[0] : make_int4(0, 0, 0, 0), q1 = nc > 1 ? dsc[1] : q0, q2 = nc > 2 ? dsc[2] : q0,
+         q3 = nc > 3 ? dsc[3] : q0;
+    for (int k = 0; k < nc; ++k) {
+      const int4 d = q0;
+      q0 = q1;
+      q1 = q2;
+      q2 = q3;
+      if (k + 4 < nc) q3 = dsc[k + 4];
+      const int st = k % NS;
+      const int ns = d.w >> 1;
+      const bool upper = d.w & 1;
+      if (upper && !g1) { mbar_wait(&gate[1], 0); g1 = true; }
+      if (k >= NS) mbar_wait(&empty[st], (unsigned)(((k / NS) - 1) & 1));
+      const unsigned rb = (unsigned)(ns * 32 * sizeof(T));
+      mbar_expect_tx(&full[st], (unsigned)d.y + rb);
+      bulk_g2s(stages + (size_t)st * PIPE_SB_DEV, P.blob + (size_t)(unsigned)d.x * 128, (unsigned)d.y, &full[st]);
+      bulk_g2s(rslot + (size_t)st * NCONS, (upper ? P.rhsU : P.rhsL) + (size_t)(unsigned)d.z * 32, rb, &full[st]);
+      if (dbg && b == 0 && k < 4096) dbg[4 * k + 3] = clock64();
     }
     return;
   }
   // ---- consumer warps (the L right-hand sides were packed by k_pack_rhs)
-  const int nL = P.blk_nl[b];
-  for (int k = 0; k < nc; ++k) {
-    const int st = k % NS;
-    if (dbg && b == 0 && tid == 0 && k < 4096) dbg[4 * k] = clock64();
-    mbar_wait(&full[st], (unsigned)((k / NS) & 1));
-    if (dbg && b == 0 && tid == 0 && k < 4096) dbg[4 * k + 1] = clock64();
-    const unsigned char *blob = stages + (size_t)st * PIPE_SB_DEV;
-    const int *hdr = reinterpret_cast<const int *>(blob);
-    const int ns = hdr[0], s0 = hdr[1], ne = hdr[2];
-    const bool upper = hdr[3] & 1;
+  // The static per-chunk values of this lane (row, slice offsets, diagonal,
+  // right-hand side) are fetched for chunk k+1 while chunk k is finishing, so
+  // after the level barrier only the column/value and solution loads remain.
+  struct Pre {
+    const int *cp;
+    const T *vp;
+    T rhs, dg;
+    int row, w, auxv, s0, flags, ok;
+  };
+  auto fetch = [&](int kk, Pre &p) {
+    const int st = kk % NS;
+    const int *hdr = reinterpret_cast<const int *>(stages + (size_t)st * PIPE_SB_DEV);
+    const int4 h4 = *reinterpret_cast<const int4 *>(hdr);       // ns, s0, ne, flags
+    const int ns = h4.x, ne = h4.z;
     const int H = (ns + 5 + 3) & ~3;
     const int *rows = hdr + H;
     const int *aux = rows + ns * 32;
     const T *diag = reinterpret_cast<const T *>(aux + ns * 32);
     const int *col = reinterpret_cast<const int *>(diag + ns * 32);
     const T *val = reinterpret_cast<const T *>(col + ne);
+    p.s0 = h4.y;
+    p.flags = h4.w;
+    p.ok = 1;
+    p.row = -1;
     if (warp < ns) {
-      const int row = rows[warp * 32 + lane];
-      if (row >= 0) {
-        T acc = rslot[(size_t)st * NCONS + warp * 32 + lane];
-        const int e0 = hdr[4 + warp], w = (hdr[5 + warp] - e0) >> 5;
-        const int *cp = col + e0 + lane;
-        const T *vp = val + e0 + lane;
-        if (FAR) {
-          for (int e = 0; e < w; ++e) {
-            const int c = cp[32 * e];
-            const T v = vp[32 * e];
-            if (c >= 0) acc -= v * ring[c & (R - 1)];
-            else if (c <= -2) acc -= v * out[-c - 2];
-          }
-        } else {
-          // branch-free: padding has value 0 and column -1 (ring slot R-1, finite
-          // because the ring is zero-initialised); two partial sums shorten the
-          // dependent DFMA chain
-          T acc1 = dzero<T>();
-          int e = 0;
-#pragma unroll 4
-          for (; e + 2 <= w; e += 2) {
-            const int ca = cp[32 * e], cb = cp[32 * (e + 1)];
-            const T va = vp[32 * e], vb = vp[32 * (e + 1)];
-            acc -= va * ring[ca & (R - 1)];
-            acc1 -= vb * ring[cb & (R - 1)];
-          }
-          if (e < w) acc -= vp[32 * e] * ring[cp[32 * e] & (R - 1)];
-          acc += acc1;
-        }
-        if (upper) acc = acc * diag[warp * 32 + lane];             // diag holds 1 / u_ii
-        else P.rhsU[aux[warp * 32 + lane]] = acc;              // right-hand side of the U sweep
-        ring[((s0 + warp) * 32 + lane) & (R - 1)] = acc;
-        out[row] = acc;
-      }
+      p.row = rows[warp * 32 + lane];
+      const int e0 = hdr[4 + warp];
+      p.w = (hdr[5 + warp] - e0) >> 5;
+      p.cp = col + e0 + lane;
+      p.vp = val + e0 + lane;
+      p.rhs = rslot[(size_t)st * NCONS + warp * 32 + lane];
+      p.dg = diag[warp * 32 + lane];
+      p.auxv = aux[warp * 32 + lane];
     }
+  };
+  const int nL = P.blk_nl[b];
+  Pre cur;
+  cur.ok = 0;
+  for (int k = 0; k < nc; ++k) {
+    const int st = k % NS;
+    if (dbg && b == 0 && tid == 0 && k < 4096) dbg[4 * k] = clock64();
+    if (!cur.ok) {
+      mbar_wait(&full[st], (unsigned)((k / NS) & 1));
+      fetch(k, cur);
+    }
+    if (dbg && b == 0 && tid == 0 && k < 4096) dbg[4 * k + 1] = clock64();
+    const bool upper = cur.flags & 1;
+    if (cur.row >= 0) {
+      T acc = cur.rhs;
+      const int w = cur.w;
+      const int *cp = cur.cp;
+      const T *vp = cur.vp;
+      if (FAR) {
+        for (int e = 0; e < w; ++e) {
+          const int c = cp[32 * e];
+          const T v = vp[32 * e];
+          if (c >= 0) acc -= v * ring[c & (R - 1)];
+          else if (c <= -2) acc -= v * out[-c - 2];
+        }
+      } else {
+        // branch-free: padding has value 0 and column -1 (ring slot R-1, finite
+        // because the ring is zero-initialised); two partial sums shorten the
+        // dependent DFMA chain
+        T acc1 = dzero<T>();
+        int e = 0;
+#pragma unroll 4
+        for (; e + 2 <= w; e += 2) {
+          const int ca = cp[32 * e], cb = cp[32 * (e + 1)];
+          const T va = vp[32 * e], vb = vp[32 * (e + 1)];
+          acc -= va * ring[ca & (R - 1)];
+          acc1 -= vb * ring[cb & (R - 1)];
+        }
+        if (e < w) acc -= vp[32 * e] * ring[cp[32 * e] & (R - 1)];
+        acc += acc1;
+      }
+      if (upper) acc = acc * cur.dg;                              // diag holds 1 / u_ii
+      else P.rhsU[cur.auxv] = acc;                                 // right-hand side of the U sweep
+      ring[((cur.s0 + warp) * 32 + lane) & (R - 1)] = acc;
+      out[cur.row] = acc;
+    }
+    const bool level_end = cur.flags & 2;
     __syncwarp();
     if (dbg && b == 0 && tid == 0 && k < 4096) dbg[4 * k + 2] = clock64();
     if (lane == 0) mbar_arrive(&empty[st]);
+    cur.ok = 0;
+    if (k + 1 < nc) {
+      const int st1 = (k + 1) % NS;
+      if (mbar_test(&full[st1], (unsigned)(((k + 1) / NS) & 1))) fetch(k + 1, cur);
+    }
     if (k == nL - 1) {                                             // L sweep done: release the U right-hand sides
       fence_proxy_async_global();
       __threadfence();
       __syncwarp();
       if (lane == 0) mbar_arrive(&gate[1]);
     }
-    consumer_sync();
+    if (level_end) consumer_sync();                                // rows of one level are independent
   }
   if (mode == TRI_UP)
     for (int64_t i = r0 + tid; i < r1; i += NCONS) x[i] = x[i] - tmp[i];   // y1 = z1 - U^-1 L^-1 F y2

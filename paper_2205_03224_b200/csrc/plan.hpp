@@ -93,10 +93,11 @@ struct TriPack {
 // dependency, read from the shared-memory ring of the last `ring` solution
 // values; c == -1 padding; c <= -2 "far" dependency read from global memory
 // at row -c - 2.
-struct ChunkDesc {
-  int64_t blob_off;
-  int64_t rhs_off;                          // first packed right-hand-side index
-  int32_t bytes, ns, flags, pad;            // flags bit0: U sweep
+struct ChunkDesc {                          // 16 bytes, one vector load in the producer
+  int32_t blob128;                          // blob offset / 128
+  int32_t bytes;                            // blob bytes
+  int32_t slice;                            // first stage slice (packed right-hand sides at slice * 32)
+  int32_t nsflags;                          // ns << 1 | (1 if U sweep)
 };
 constexpr int PIPE_NW = 8;                  // consumer warps per CTA = max slices per chunk
 constexpr int PIPE_SB = 16 * 1024;          // blob bytes per pipeline stage

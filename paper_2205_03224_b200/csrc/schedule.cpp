@@ -127,12 +127,12 @@ void pack_pipe(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriP
       if (lv1 <= lv0) continue;
       const int32_t sb0 = S.lev_slice[lv0];
       // chunk boundaries: <= PIPE_NW slices of one level, blob <= PIPE_SB bytes
-      struct Ch { int32_t s0, s1; };
+      struct Ch { int32_t s0, s1, lev_end; };
       std::vector<Ch> ch;
       for (int32_t v = lv0; v < lv1; ++v) {
         int32_t s = S.lev_slice[v];
         while (s < S.lev_slice[v + 1]) {
-          Ch c{s, s};
+          Ch c{s, s, S.lev_slice[v + 1]};
           size_t ne = 0;
           while (c.s1 < S.lev_slice[v + 1] && c.s1 - c.s0 < PIPE_NW) {
             const size_t e2 = ne + (size_t)(S.slice_off[c.s1 + 1] - S.slice_off[c.s1]);
@@ -162,11 +162,13 @@ void pack_pipe(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriP
         T *diag = reinterpret_cast<T *>(aux + ns * 32);
         int32_t *col = reinterpret_cast<int32_t *>(diag + ns * 32);
         T *val = reinterpret_cast<T *>(col + ne);
-        const int32_t send = c.s1 - sb0;              // chunk end (block-relative slice)
+        // chunks of one level run without a barrier between them, so a dependency
+        // stays in the ring only if no write of the whole level can overwrite it
+        const int32_t send = c.lev_end - sb0;         // level end (block-relative slice)
         hdr[0] = ns;
         hdr[1] = c.s0 - sb0;
         hdr[2] = ne;
-        hdr[3] = upper ? 1 : 0;
+        hdr[3] = (upper ? 1 : 0) | (c.s1 == c.lev_end ? 2 : 0);
         for (int32_t i = 0; i < ns; ++i) {
           const int32_t s = c.s0 + i;
           hdr[4 + i] = (int32_t)(S.slice_off[s] - e0);
@@ -191,7 +193,7 @@ void pack_pipe(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriP
             }
         }
         hdr[4 + ns] = ne;
-        P.chunks.push_back(ChunkDesc{(int64_t)off, (int64_t)c.s0 * 32, (int32_t)bytes, ns, upper ? 1 : 0, 0});
+        P.chunks.push_back(ChunkDesc{(int32_t)(off / 128), (int32_t)bytes, c.s0, (ns << 1) | (upper ? 1 : 0)});
         if (!upper) nL++;
       }
     }
