@@ -307,7 +307,7 @@ def run_reference(args):
     out = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=K)
     dt = time.perf_counter() - t1
     val = 1e3 * dt / out["its"]
-    line = {"impl": "reference", "metric": METRIC, "value": round(val, 2), "unit": UNIT, "n_gpus": 0, "steps": out["its"],
+    line = {"impl": "reference", "metric": METRIC, "value": round(val, 2), "unit": UNIT, "n_gpus": args.gpus, "steps": out["its"],
             "warmup": W, "ms_per_step": round(val, 2), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded 7-pt Laplacian, b = A x_true)",
             "config": {"workload": f"{name} per-GPU problem {prob.dims}", "n": prob.n, "setup_s": round(setup, 1)},

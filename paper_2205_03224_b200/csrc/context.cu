@@ -20,6 +20,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/gemslr.h"
 #include "kernels.cuh"
 #include "plan.hpp"
@@ -813,6 +815,10 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
                      int *hlen, double *frel) {
   cudaStream_t s = ctx->stream;
   if (m + 1 > GS_MAXC) throw Error{GEMSLR_ERR_INVALID_ARG, "restart must be <= 103"};
+  struct Range {                                              // NVTX range for ncu --nvtx filtering
+    Range() { nvtxRangePushA("gemslr_solve"); }
+    ~Range() { nvtxRangePop(); }
+  } nvtx_range;
   ensure_krylov(m, maxit);
   std::vector<double> hh;
   const double bnorm = norm(b, n, 6);

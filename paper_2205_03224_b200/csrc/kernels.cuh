@@ -477,6 +477,22 @@ __global__ void __launch_bounds__(256) k_pack_rhs(int64_t nrows, int64_t row0, c
   }
 }
 
+// Deterministic last-CTA reduction of per-CTA partials stored column-major
+// (partial[c * G + q], q = CTA): warp w sums the columns w, w+8, ...; lane l
+// adds the CTAs l, l+32, ... (coalesced, fixed order), then a fixed shuffle tree.
+template <typename T>
+__device__ inline void reduce_partials(const T *partial, int G, int ncol, T *out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = warp; c < ncol; c += nw) {
+    T s = dzero<T>();
+    const T *p = partial + (int64_t)c * G;
+#pragma unroll 4
+    for (int q = lane; q < G; q += 32) s += ld_cg(p + q);
+    s = warp_sum(s);
+    if (lane == 0) out[c] = s;
+  }
+}
+
 // ----------------------------------------------------------------- K6+K7
 // Rows J_l = [rowbase, rowbase + s): dst_i = src_i - Σ_j E_ij z_j (src == nullptr: 0),
 // then per-column partial sums of conj(W_ic) dst_i; the last CTA reduces the
@@ -529,7 +545,7 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
   for (int a = 0; a < EW_NACC; ++a) {
     const int c = warp + 8 * a;
     T r = warp_sum(acc[a]);
-    if (lane == 0 && c < k) partial[(int64_t)blockIdx.x * k + c] = r;
+    if (lane == 0 && c < k) partial[(int64_t)c * gridDim.x + blockIdx.x] = r;
   }
   __threadfence();
   __syncthreads();
@@ -537,11 +553,7 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
   __syncthreads();
   if (!amlast) return;
   __threadfence();
-  if (tid < k) {
-    T sum = dzero<T>();
-    for (unsigned q = 0; q < gridDim.x; ++q) sum += ld_cg(partial + (int64_t)q * k + tid);
-    sred[tid] = sum;
-  }
+  reduce_partials(partial, (int)gridDim.x, k, sred);
   __syncthreads();
   if (tid < k) {
     T t = dzero<T>();
@@ -652,7 +664,7 @@ __global__ void __launch_bounds__(256) k_gs(int64_t n, const T *__restrict__ V, 
     for (int a = 0; a < NPW; ++a) {
       const int c = warp + 8 * a;
       T r = warp_sum(acc[a]);
-      if (lane == 0 && c < ncols) partial[(int64_t)blockIdx.x * nres + c] = r;
+      if (lane == 0 && c < ncols) partial[(int64_t)c * gridDim.x + blockIdx.x] = r;
     }
   }
   if (warp == 0) {
@@ -660,7 +672,7 @@ __global__ void __launch_bounds__(256) k_gs(int64_t n, const T *__restrict__ V, 
     if (lane == 0) {
       T t = dzero<T>();
       if constexpr (sizeof(T) == sizeof(double)) t = r; else t = T{r, 0.0};
-      partial[(int64_t)blockIdx.x * nres + (nres - 1)] = t;
+      partial[(int64_t)(nres - 1) * gridDim.x + blockIdx.x] = t;
     }
   }
   __threadfence();
@@ -669,11 +681,7 @@ __global__ void __launch_bounds__(256) k_gs(int64_t n, const T *__restrict__ V, 
   __syncthreads();
   if (!amlast) return;
   __threadfence();
-  for (int c = tid; c < nres; c += blockDim.x) {
-    T sum = dzero<T>();
-    for (unsigned q = 0; q < gridDim.x; ++q) sum += ld_cg(partial + (int64_t)q * nres + c);
-    res[c] = sum;
-  }
+  reduce_partials(partial, (int)gridDim.x, nres, res);
   if (tid == 0) *ticket = 0;
 }
 
