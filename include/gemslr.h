@@ -13,7 +13,7 @@
  *    except gemslr_last_error / gemslr_destroy.  After an error the context
  *    stays usable for a new call; gemslr_last_error() gives a message.
  *  - Collective: with a communicator (nranks > 1) every rank makes the same
- *    sequence of calls.  (This release: nranks == 1.)
+ *    sequence of calls.
  *  - Ownership: every input is borrowed.  setup() copies A.  Device buffers
  *    passed to spmv / apply_precond / solve belong to the caller and must not
  *    alias each other.  The context owns factors, low-rank bases, Krylov
@@ -80,6 +80,30 @@ typedef struct gemslr_ctx gemslr_ctx;
  * cudaStream_t or NULL (legacy default stream). */
 gemslr_status gemslr_create(gemslr_ctx **out, int cuda_device, void *nccl_comm, void *cuda_stream);
 
+/* Multi-GPU (one process per GPU).  gemslr_nccl_unique_id: rank 0
+ * creates an NCCL unique id (128 bytes) that the caller broadcasts (e.g. with
+ * torch.distributed); nccl_lib = path of libnccl.so.2 to load (NULL: the one
+ * already loaded in the process).  gemslr_create_dist: like gemslr_create for
+ * rank `rank` of `nranks`; the library owns an NCCL communicator built from
+ * nccl_id.  cuda_device = -1 gives a host-only planning context of that rank
+ * (no NCCL; used to test ownership and halo plans without GPUs).  With
+ * nranks > 1 the matrix is row-partitioned by subdomain: level-0 parts in
+ * contiguous rank ranges (p must be a multiple of nranks), later parts
+ * and C_last rows to the rank owning most of their earlier-level neighbours;
+ * exterior values move by grouped ncclSend/ncclRecv, W^H products, Gram-Schmidt
+ * dots and the last separator by ncclAllReduce; the last-separator solve is
+ * replicated. */
+gemslr_status gemslr_nccl_unique_id(const char *nccl_lib, void *id128);
+gemslr_status gemslr_create_dist(gemslr_ctx **out, int cuda_device, void *cuda_stream, int nranks, int rank,
+                                 const void *nccl_id, const char *nccl_lib);
+
+/* Halo plan of this rank (inspection/tests): which = 0 SpMV, 1 E_l, 2 F_l (level
+ * `level`).  counts (host, 2*nranks): values sent to / received from each rank;
+ * sglob, rglob (host, may be NULL): global permuted positions of the values,
+ * concatenated by peer in rank order. */
+gemslr_status gemslr_halo_plan(const gemslr_ctx *ctx, int which, int level, int64_t *counts, int64_t *sglob,
+                               int64_t *rglob);
+
 /* Optional device allocator (e.g. torch's caching allocator).  NULL resets to cudaMalloc/cudaFree. */
 gemslr_status gemslr_set_allocator(gemslr_ctx *ctx, void *(*alloc_fn)(size_t bytes, void *user),
                                    void (*free_fn)(void *ptr, void *user), void *user);
@@ -102,7 +126,7 @@ gemslr_status gemslr_setup(gemslr_ctx *ctx, gemslr_dtype dtype, int64_t n, const
                            const int32_t *colidx, const void *values, const gemslr_params *params);
 
 /* Local layout: n_local rows on this rank; global_row_of_local[i] (host,
- * caller-allocated, may be NULL) = original row of local row i. */
+ * caller-allocated, may be NULL) = original (natural) row of local row i. */
 gemslr_status gemslr_layout(const gemslr_ctx *ctx, int64_t *n_local, int64_t *global_row_of_local);
 
 /* y = A x (Note N P:L58-61): diagonal block + off-diagonal block over the halo.
@@ -127,9 +151,10 @@ gemslr_status gemslr_solve(gemslr_ctx *ctx, const void *b_dev, void *x_dev, doub
                            double *final_true_relres);
 
 /* The same solve with HOST vectors in the ORIGINAL (natural) global order,
- * length n: the host->device copy, the permutation into the local layout, the
- * solve, the inverse permutation and the device->host copy all happen inside
- * the call (the end-to-end path).  x_host: in x0 (may be NULL = 0), out x. */
+ * length n (global): the host->device copy, the permutation into the local
+ * layout, the solve, the inverse permutation and the device->host copy all
+ * happen inside the call (the end-to-end path).  x_host: in x0, out x; with
+ * nranks > 1 only the entries this rank owns are written. */
 gemslr_status gemslr_solve_host(gemslr_ctx *ctx, const void *b_host, void *x_host, double rtol, int restart,
                                 int maxit, int *iterations, double *res_hist, int hist_cap, int *hist_len,
                                 double *final_true_relres);

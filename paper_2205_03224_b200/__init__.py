@@ -21,7 +21,7 @@ _lib = None
 GEMSLR_OK, GEMSLR_NOT_CONVERGED = 0, 1
 STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "INVALID_ARG", -2: "BAD_CSR", -3: "PARTITION", -4: "ZERO_PIVOT",
           -5: "LOWRANK", -6: "STATE", -7: "CUDA", -8: "NCCL", -9: "OOM"}
-ABI_FUNCTIONS = ["gemslr_create", "gemslr_set_allocator", "gemslr_set_coordinates", "gemslr_setup", "gemslr_layout",
+ABI_FUNCTIONS = ["gemslr_create", "gemslr_nccl_unique_id", "gemslr_create_dist", "gemslr_halo_plan", "gemslr_set_allocator", "gemslr_set_coordinates", "gemslr_setup", "gemslr_layout",
                  "gemslr_spmv", "gemslr_apply_precond", "gemslr_solve", "gemslr_solve_host", "gemslr_to_local",
                  "gemslr_to_natural", "gemslr_export_setup", "gemslr_stats", "gemslr_profile", "gemslr_last_error",
                  "gemslr_destroy"]
@@ -50,6 +50,9 @@ def lib():
         L = C.CDLL(LIB_PATH)
         vp, i64 = C.c_void_p, C.c_int64
         L.gemslr_create.argtypes = [C.POINTER(vp), C.c_int, vp, vp]
+        L.gemslr_nccl_unique_id.argtypes = [C.c_char_p, vp]
+        L.gemslr_create_dist.argtypes = [C.POINTER(vp), C.c_int, vp, C.c_int, C.c_int, vp, C.c_char_p]
+        L.gemslr_halo_plan.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp]
         L.gemslr_set_coordinates.argtypes = [vp, C.c_int, vp]
         L.gemslr_setup.argtypes = [vp, C.c_int, i64, vp, vp, vp, C.POINTER(Params)]
         L.gemslr_layout.argtypes = [vp, C.POINTER(i64), vp]
@@ -75,6 +78,16 @@ def lib():
     return _lib
 
 
+def nccl_lib_path():
+    """libnccl.so.2 of the torch wheel (the one torch itself loads)."""
+    try:
+        import nvidia.nccl
+        p = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        return p if os.path.exists(p) else None
+    except Exception:
+        return None
+
+
 def _ptr(a):
     if a is None:
         return None
@@ -92,7 +105,11 @@ class Solver:
 
     def __init__(self, rowptr, colidx, values, levels, subdomains, rank, ilu="ilut", ilut_drop=1e-3,
                  ilut_fill=10, last_blocks=0, coords=None, device=0, stream=None, seed=0, arnoldi_tol=1e-2,
-                 arnoldi_max_cycles=10, cluster_ctas=0):
+                 arnoldi_max_cycles=10, cluster_ctas=0, nranks=None, my_rank=None):
+        """nranks/my_rank: None = single GPU, or taken from an initialised
+        torch.distributed world (one process per GPU; the NCCL id is broadcast
+        with torch.distributed).  device = -1 with explicit nranks/my_rank builds
+        the host-only plan of that rank (no GPU, no NCCL)."""
         L = lib()
         self.rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
         self.colidx = np.ascontiguousarray(colidx, dtype=np.int32)
@@ -104,7 +121,28 @@ class Solver:
         if stream is None and device >= 0:
             import torch
             stream = torch.cuda.current_stream(device).cuda_stream
-        self._check(L.gemslr_create(C.byref(self.h), int(device), None, C.c_void_p(stream or 0)), "create")
+        if nranks is None and device >= 0:
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+                nranks, my_rank = dist.get_world_size(), dist.get_rank()
+        self.nranks = nranks or 1
+        self.my_rank = my_rank or 0
+        if self.nranks == 1:
+            self._check(L.gemslr_create(C.byref(self.h), int(device), None, C.c_void_p(stream or 0)), "create")
+        else:
+            libp = nccl_lib_path()
+            idb = C.create_string_buffer(128)
+            if device >= 0:
+                import torch
+                import torch.distributed as dist
+                if self.my_rank == 0:
+                    self._check(L.gemslr_nccl_unique_id(libp.encode() if libp else None, idb), "nccl_unique_id")
+                obj = [bytes(idb.raw)]
+                dist.broadcast_object_list(obj, src=0)
+                C.memmove(idb, obj[0], 128)
+            self._check(L.gemslr_create_dist(C.byref(self.h), int(device), C.c_void_p(stream or 0), self.nranks,
+                                             self.my_rank, idb if device >= 0 else None,
+                                             libp.encode() if libp else None), "create_dist")
         if coords is not None:
             self.coords = np.ascontiguousarray(coords, dtype=np.float64)
             self._check(L.gemslr_set_coordinates(self.h, self.coords.shape[1], _ptr(self.coords)), "coordinates")
@@ -114,7 +152,9 @@ class Solver:
         self._check(L.gemslr_setup(self.h, 1 if self.is_complex else 0, self.n, _ptr(self.rowptr), _ptr(self.colidx),
                                    _ptr(self.values), C.byref(p)), "setup")
         nl = C.c_int64(0)
-        self.perm = np.empty(self.n, dtype=np.int64)
+        self._check(L.gemslr_layout(self.h, C.byref(nl), None), "layout")
+        self.n_local = nl.value
+        self.perm = np.empty(self.n_local, dtype=np.int64)      # natural row of every local row
         self._check(L.gemslr_layout(self.h, C.byref(nl), _ptr(self.perm)), "layout")
 
     # ------------------------------------------------------------------ helpers
@@ -129,14 +169,14 @@ class Solver:
         import torch
         return torch.complex128 if self.is_complex else torch.float64
 
-    def _vec(self, like=None):
+    def _vec(self, n=None):
         import torch
-        return torch.empty(self.n, dtype=self.torch_dtype, device=f"cuda:{self.device}")
+        return torch.empty(self.n_local if n is None else n, dtype=self.torch_dtype, device=f"cuda:{self.device}")
 
-    def _dev(self, x):
-        import torch
-        assert x.is_cuda and x.dtype == self.torch_dtype and x.is_contiguous() and x.numel() == self.n, \
-            "device vectors must be contiguous CUDA tensors of the solver dtype and length n"
+    def _dev(self, x, n=None):
+        n = self.n_local if n is None else n
+        assert x.is_cuda and x.dtype == self.torch_dtype and x.is_contiguous() and x.numel() == n, \
+            "device vectors must be contiguous CUDA tensors of the solver dtype and length n_local"
         return x
 
     # ------------------------------------------------------------------ the path
@@ -175,14 +215,27 @@ class Solver:
         return dict(x=x, its=its.value, hist=hist[:hl.value].copy(), final_relres=fr.value, status=rc)
 
     def to_local(self, x_nat, out=None):
+        """natural-order global vector (length n) -> this rank's local vector"""
         out = self._vec() if out is None else out
-        self._check(lib().gemslr_to_local(self.h, _ptr(self._dev(x_nat)), _ptr(out)), "to_local")
+        self._check(lib().gemslr_to_local(self.h, _ptr(self._dev(x_nat, self.n)), _ptr(out)), "to_local")
         return out
 
     def to_natural(self, x_loc, out=None):
-        out = self._vec() if out is None else out
+        """local vector -> natural-order global vector (only owned entries written)"""
+        out = self._vec(self.n).zero_() if out is None else out
         self._check(lib().gemslr_to_natural(self.h, _ptr(self._dev(x_loc)), _ptr(out)), "to_natural")
         return out
+
+    def halo_plan(self, which, level=0):
+        """which: 'A' (SpMV), 'E' or 'F' (level). Returns dict(send_counts, recv_counts, sglob, rglob)."""
+        w = {"A": 0, "E": 1, "F": 2}[which]
+        cnt = np.zeros(2 * self.nranks, dtype=np.int64)
+        self._check(lib().gemslr_halo_plan(self.h, w, level, _ptr(cnt), None, None), "halo_plan")
+        sg = np.zeros(max(int(cnt[:self.nranks].sum()), 1), dtype=np.int64)
+        rg = np.zeros(max(int(cnt[self.nranks:].sum()), 1), dtype=np.int64)
+        self._check(lib().gemslr_halo_plan(self.h, w, level, _ptr(cnt), _ptr(sg), _ptr(rg)), "halo_plan")
+        return dict(send_counts=cnt[:self.nranks].copy(), recv_counts=cnt[self.nranks:].copy(),
+                    sglob=sg[:int(cnt[:self.nranks].sum())], rglob=rg[:int(cnt[self.nranks:].sum())])
 
     def export(self, directory):
         self._check(lib().gemslr_export_setup(self.h, os.fsencode(directory)), "export")

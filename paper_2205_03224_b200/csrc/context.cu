@@ -16,6 +16,7 @@
 #include <memory>
 #include <random>
 #include <string>
+#include <dlfcn.h>
 #include <sys/stat.h>
 #include <type_traits>
 #include <vector>
@@ -145,11 +146,94 @@ struct Timed {                                  // RAII event pair around one la
   }
 };
 
+// ----------------------------------------------------------------- NCCL (dlopen)
+// The library loads NCCL at run time (the torch wheel's libnccl.so.2, or the
+// one already loaded in the process) so it links against no NCCL at build time.
+struct Comm {
+  void *lib = nullptr;
+  void *comm = nullptr;
+  bool owned = false;
+  int nranks = 1, rank = 0;
+  typedef int (*fn_uid)(void *);
+  typedef int (*fn_init)(void **, int, const void *, int);   // id passed by value: see init()
+  typedef int (*fn_destroy)(void *);
+  typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+  typedef int (*fn_p2p)(const void *, size_t, int, int, void *, cudaStream_t);
+  typedef int (*fn_recv)(void *, size_t, int, int, void *, cudaStream_t);
+  typedef int (*fn_group)();
+  typedef const char *(*fn_err)(int);
+  typedef int (*fn_count)(void *, int *);
+  fn_allreduce allreduce_ = nullptr;
+  fn_p2p send_ = nullptr;
+  fn_recv recv_ = nullptr;
+  fn_group gstart_ = nullptr, gend_ = nullptr;
+  fn_err errstr_ = nullptr;
+  fn_destroy destroy_ = nullptr;
+  long long allreduces = 0, exchanges = 0;
+
+  static void *open_lib(const char *path) {
+    void *h = nullptr;
+    if (path && *path) h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw Error{GEMSLR_ERR_NCCL, "cannot load libnccl.so.2"};
+    return h;
+  }
+  template <typename F> F sym(const char *name) {
+    F f = reinterpret_cast<F>(dlsym(lib, name));
+    if (!f) throw Error{GEMSLR_ERR_NCCL, std::string("NCCL symbol missing: ") + name};
+    return f;
+  }
+  void bind() {
+    allreduce_ = sym<fn_allreduce>("ncclAllReduce");
+    send_ = sym<fn_p2p>("ncclSend");
+    recv_ = sym<fn_recv>("ncclRecv");
+    gstart_ = sym<fn_group>("ncclGroupStart");
+    gend_ = sym<fn_group>("ncclGroupEnd");
+    errstr_ = sym<fn_err>("ncclGetErrorString");
+    destroy_ = sym<fn_destroy>("ncclCommDestroy");
+  }
+  void check(int rc, const char *what) {
+    if (rc != 0) throw Error{GEMSLR_ERR_NCCL, std::string("NCCL ") + what + ": " + (errstr_ ? errstr_(rc) : "error")};
+  }
+  void borrow(void *c, const char *path) {
+    lib = open_lib(path);
+    bind();
+    comm = c;
+    int n = 1, r = 0;
+    check(sym<fn_count>("ncclCommCount")(c, &n), "CommCount");
+    check(sym<fn_count>("ncclCommUserRank")(c, &r), "CommUserRank");
+    nranks = n;
+    rank = r;
+  }
+  void init(const char *path, int n, int r, const void *id128) {
+    lib = open_lib(path);
+    bind();
+    // ncclCommInitRank(ncclComm_t*, int, ncclUniqueId (128 bytes by value), int)
+    struct Id { char b[128]; } id;
+    std::memcpy(id.b, id128, 128);
+    typedef int (*fn_init_v)(void **, int, Id, int);
+    check(sym<fn_init_v>("ncclCommInitRank")(&comm, n, id, r), "CommInitRank");
+    owned = true;
+    nranks = n;
+    rank = r;
+  }
+  // sum over ranks in place; count in doubles (complex = 2 doubles each)
+  void allreduce(void *buf, size_t ndouble, cudaStream_t s) {
+    if (nranks == 1 || ndouble == 0) return;
+    check(allreduce_(buf, buf, ndouble, 8 /*ncclFloat64*/, 0 /*ncclSum*/, comm, s), "AllReduce");
+    allreduces++;
+  }
+  ~Comm() {
+    if (owned && comm && destroy_) destroy_(comm);
+  }
+};
+
 // ----------------------------------------------------------------- device plan
 template <typename D>
 struct StageDev {
   int nblk = 0, cps = 1;
-  int64_t rows = 0;
+  int64_t rows = 0, row0 = 0;
   const int64_t *blk = nullptr;
   TriDev<D> L{}, U{};
   int depthL = 0, depthU = 0;
@@ -183,6 +267,15 @@ struct LevelDev {
 
 struct Ctx;
 
+template <typename D>
+struct HaloDev {                  // device side of a HaloPlan
+  std::vector<int32_t> peer;
+  std::vector<int64_t> soff, roff;
+  const int *sidx = nullptr;
+  D *sbuf = nullptr, *rbuf = nullptr;
+  int64_t nsend = 0, nrecv = 0;
+};
+
 template <typename T>
 struct Engine {
   using D = typename Dev<T>::type;
@@ -196,7 +289,12 @@ struct Engine {
   const D *sell_val = nullptr;
   std::vector<LevelDev<D>> lev;
   StageDev<D> last;
-  const int64_t *perm_d = nullptr;
+  const int64_t *perm_d = nullptr;   // natural (original) row of every local row
+  HaloDev<D> hA;
+  std::vector<HaloDev<D>> hE, hF;
+  D *rl_full = nullptr, *yl_full = nullptr;   // replicated last separator (nranks > 1)
+  const int *last_idx_d = nullptr;
+  int64_t nglob = 0, o_last = 0;
   // workspace
   D *r = nullptr, *tmp = nullptr, *tvec = nullptr, *partial = nullptr, *res = nullptr;
   unsigned *tickets = nullptr;
@@ -213,6 +311,8 @@ struct Engine {
   double setup_host_s = 0, setup_dev_s = 0, arnoldi_s = 0;
 
   void upload(cudaStream_t s);
+  void exchange(HaloDev<D> &h, const D *src, const int *doneflag);
+  void allreduce(D *buf, size_t count);
   void apply_from(int l0, const D *in, D *out, const int *doneflag);
   void spmv(const D *x, D *y, int mode, const D *b, const int *doneflag);
   void ghat(int l, D *bufA, D *bufB);
@@ -228,7 +328,7 @@ struct Engine {
 struct Ctx {
   int device = -1;
   cudaStream_t stream = nullptr;
-  void *nccl = nullptr;
+  Comm comm;
   Allocator alloc;
   Pool pool;
   Profiler prof;
@@ -250,6 +350,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
   StageDev<D> d;
   d.nblk = (int)S.blk.size() - 1;
   d.rows = S.blk.empty() ? 0 : S.blk.back() - S.blk.front();
+  d.row0 = S.blk.empty() ? 0 : S.blk.front();
   d.blk = P.upload<int64_t>(S.blk, s);
   auto up = [&](const TriPack<T> &p) {
     TriDev<D> t;
@@ -313,13 +414,29 @@ static CsrDev<D> upload_csr(Pool &P, cudaStream_t s, const Csr<T> &A) {
   return d;
 }
 
+template <typename D>
+static HaloDev<D> upload_halo(Pool &P, cudaStream_t s, const HaloPlan &h) {
+  HaloDev<D> d;
+  d.peer = h.peer;
+  d.soff = h.soff;
+  d.roff = h.roff;
+  d.nsend = h.nsend();
+  d.nrecv = h.nrecv();
+  d.sidx = P.upload<int>(h.sidx, s);
+  d.sbuf = P.get<D>(std::max<int64_t>(d.nsend, 1));
+  d.rbuf = P.get<D>(std::max<int64_t>(d.nrecv, 1));
+  return d;
+}
+
 template <typename T>
 void Engine<T>::upload(cudaStream_t s) {
   Pool &P = ctx->pool;
-  const auto &A = plan.Ahat;
-  n = A.n;
+  const auto &A = plan.Aloc;                   // owned rows of Â, local / halo columns
+  n = plan.nloc;
+  nglob = plan.st.n;
+  o_last = plan.st.o[plan.st.L];
   nnzA = A.nnz();
-  // SELL-32 of Â
+  // SELL-32 of the owned rows
   nslices = (n + 31) / 32;
   std::vector<int64_t> off(nslices + 1, 0);
   for (int64_t sl = 0; sl < nslices; ++sl) {
@@ -340,19 +457,31 @@ void Engine<T>::upload(cudaStream_t s) {
   sell_off = P.upload<int64_t>(off, s);
   sell_col = P.upload<int32_t>(col, s);
   sell_val = P.upload<D>(val, s);
-  perm_d = P.upload<int64_t>(plan.st.perm, s);
+  std::vector<int64_t> nat(n);
+  for (int64_t i = 0; i < n; ++i) nat[i] = plan.st.perm[plan.gpos[i]];
+  perm_d = P.upload<int64_t>(nat, s);
   const int L = plan.st.L;
   lev.resize(L);
+  hE.resize(L);
+  hF.resize(L);
   for (int l = 0; l < L; ++l) {
     LevelDev<D> &d = lev[l];
-    d.o0 = plan.st.o[l];
-    d.o1 = plan.st.o[l + 1];
+    d.o0 = plan.lo[l];
+    d.o1 = plan.lo[l + 1];
     d.s = n - d.o1;
     d.st = upload_stage<D>(P, s, plan.stage[l], ctx->params.cluster_ctas);
     d.E = upload_csr<D>(P, s, plan.E[l]);
     d.F = upload_csr<D>(P, s, plan.F[l]);
+    hE[l] = upload_halo<D>(P, s, plan.hE[l]);
+    hF[l] = upload_halo<D>(P, s, plan.hF[l]);
   }
+  hA = upload_halo<D>(P, s, plan.hA);
   last = upload_stage<D>(P, s, plan.last_stage, ctx->params.cluster_ctas);
+  if (plan.nranks > 1) {
+    rl_full = P.get<D>(plan.slast + 1);
+    yl_full = P.get<D>(plan.slast + 1);
+    last_idx_d = P.upload<int>(plan.last_idx, s);
+  }
   r = P.get<D>(n + 1);
   tmp = P.get<D>(n + 1);
   tvec = P.get<D>(64 * 8);
@@ -365,19 +494,58 @@ void Engine<T>::upload(cudaStream_t s) {
   CK(cudaMemsetAsync(tmp, 0, (n + 1) * sizeof(D), s));
 }
 
+// Neighbour exchange: pack src[sidx] and send/receive with every
+// peer in one NCCL group on the solver stream.  No-op on one GPU.
+template <typename T>
+void Engine<T>::exchange(HaloDev<D> &h, const D *src, const int *doneflag) {
+  if (h.peer.empty()) return;
+  Comm &C = ctx->comm;
+  const int w = (int)(sizeof(D) / sizeof(double));
+  if (h.nsend > 0) {
+    const int grid = (int)std::min<int64_t>((h.nsend + 255) / 256, 4 * kNumSM);
+    k_gather_idx<D><<<grid, 256, 0, ctx->stream>>>(h.nsend, h.sidx, src, h.sbuf, doneflag);
+    CK(cudaGetLastError());
+  }
+  C.check(C.gstart_(), "GroupStart");
+  for (size_t i = 0; i < h.peer.size(); ++i) {
+    const int64_t ns = h.soff[i + 1] - h.soff[i], nr = h.roff[i + 1] - h.roff[i];
+    if (ns > 0) C.check(C.send_(h.sbuf + h.soff[i], (size_t)ns * w, 8, h.peer[i], C.comm, ctx->stream), "Send");
+    if (nr > 0) C.check(C.recv_(h.rbuf + h.roff[i], (size_t)nr * w, 8, h.peer[i], C.comm, ctx->stream), "Recv");
+  }
+  C.check(C.gend_(), "GroupEnd");
+  C.exchanges++;
+}
+
+template <typename T>
+void Engine<T>::allreduce(D *buf, size_t count) {
+  ctx->comm.allreduce(buf, count * (sizeof(D) / sizeof(double)), ctx->stream);
+}
+
 // ----------------------------------------------------------------- launches
 static int grid_for(int64_t units, int per_sm) {
   int64_t g = std::min<int64_t>(units, (int64_t)kNumSM * per_sm);
   return (int)std::max<int64_t>(g, 1);
 }
 
+// F_l product arguments of an UP launch: y_J from the local vector, the halo
+// and (nranks > 1) the replicated last separator.
+template <typename D>
+struct FArgs {
+  const CsrDev<D> *F = nullptr;
+  int64_t Fbase = 0, nloc = 0, nh = 0;
+  const D *yh = nullptr, *yl = nullptr;
+};
+
 template <typename D>
 static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *rhs, D *x, D *tmp,
-                            const CsrDev<D> *F, int64_t Fbase, const int *doneflag, int kc) {
+                            const FArgs<D> &fa, const int *doneflag, int kc) {
   if (S.nblk <= 0 || S.rows == 0) return;
+  const CsrDev<D> *F = fa.F;
+  const int64_t Fbase = fa.Fbase;
   const int64_t *Fp = F ? F->ptr : nullptr;
   const int32_t *Fc = F ? F->col : nullptr;
   const D *Fv = F ? F->val : nullptr;
+  const int pgrid = grid_for((S.rows + 255) / 256, 4);
   if (S.pipe) {
     const size_t smem = pipe_smem_bytes<D>(S.P.ring);
     static bool attr_set = false;
@@ -388,9 +556,8 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
     }
     {
       Timed tp(ctx->prof, ctx->stream, KC_PACK);
-      const int grid = grid_for((S.rows + 255) / 256, 4);
-      k_pack_rhs<D><<<grid, 256, 0, ctx->stream>>>(S.rows, S.P.row0, S.P.lpos, S.P.rhsL, mode == TRI_DOWN ? rhs : nullptr,
-                                                   Fp, Fc, Fv, Fbase, x, doneflag);
+      k_pack_rhs<D><<<pgrid, 256, 0, ctx->stream>>>(S.rows, S.row0, S.P.lpos, S.P.rhsL, mode == TRI_DOWN ? rhs : nullptr,
+                                                    Fp, Fc, Fv, Fbase, x, fa.nloc, fa.yh, fa.nh, fa.yl, doneflag);
     }
     Timed t(ctx->prof, ctx->stream, kc);
     long long *dbg = kc == KC_TRI_DOWN ? g_tri_dbg : nullptr;
@@ -398,11 +565,20 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
       k_tri_pipe<D, true><<<S.nblk, 32 * (PIPE_NW_DEV + 1), smem, ctx->stream>>>(S.P, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag, dbg);
     else
       k_tri_pipe<D, false><<<S.nblk, 32 * (PIPE_NW_DEV + 1), smem, ctx->stream>>>(S.P, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag, dbg);
-  } else if (S.cps <= 1) {
-    Timed t(ctx->prof, ctx->stream, kc);
+    CK(cudaGetLastError());
+    return;
+  }
+  // level-per-barrier kernel (blobs that do not fit a pipeline stage; cluster option)
+  if (mode == TRI_UP) {                                       // t = F_l y_J into tmp first
+    Timed tp(ctx->prof, ctx->stream, KC_PACK);
+    k_pack_rhs<D><<<pgrid, 256, 0, ctx->stream>>>(S.rows, S.row0, nullptr, tmp, nullptr, Fp, Fc, Fv, Fbase, x, fa.nloc,
+                                                  fa.yh, fa.nh, fa.yl, doneflag);
+    Fp = nullptr;
+  }
+  Timed t(ctx->prof, ctx->stream, kc);
+  if (S.cps <= 1) {
     k_trisolve<D, false><<<S.nblk, 256, 0, ctx->stream>>>(S.L, S.U, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag);
   } else {
-    Timed t(ctx->prof, ctx->stream, kc);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(S.nblk * S.cps);
     cfg.blockDim = dim3(256);
@@ -422,47 +598,78 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
 
 template <typename T>
 void Engine<T>::spmv(const D *x, D *y, int mode, const D *b, const int *doneflag) {
+  exchange(hA, x, doneflag);                                     // exterior columns (Note N P:L59-61)
   Timed t(ctx->prof, ctx->stream, KC_SPMV);
   const int grid = (int)((nslices + 7) / 8);
-  k_spmv_sell<D><<<std::max(grid, 1), 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, y, mode, b, doneflag);
+  if (hA.nrecv > 0)
+    k_spmv_sell<D, true><<<std::max(grid, 1), 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, hA.rbuf,
+                                                                    y, mode, b, doneflag);
+  else
+    k_spmv_sell<D, false><<<std::max(grid, 1), 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, hA.rbuf,
+                                                                     y, mode, b, doneflag);
   CK(cudaGetLastError());
 }
 
 // Alg. 2, single pass, from level l0: input `in` and output `out`
-// are full-length vectors of which positions [o_{l0}, N) are used.
+// are local vectors of which the local positions [lo_{l0}, n) are used.
 template <typename T>
 void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
   const int L = (int)lev.size();
   cudaStream_t s = ctx->stream;
+  const bool dist = plan.nranks > 1;
   for (int l = l0; l < L; ++l) {
     LevelDev<D> &d = lev[l];
     const D *src = (l == l0) ? in : r;
     // z1 = U_l^-1 L_l^-1 b1  -> out[I_l]
-    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, (const CsrDev<D> *)nullptr, 0, doneflag, KC_TRI_DOWN);
-    if (d.s > 0) {
-      // z2 = b2 - E_l z1 ; s = W^H z2 ; t = G s
+    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN);
+    if (d.s > 0 || dist) {
+      exchange(hE[l], out, doneflag);                              // z1 entries of E_l's exterior columns
+      // z2 = b2 - E_l z1 ; this rank's part of s = W^H z2
       {
         Timed t(ctx->prof, s, KC_EW);
-        const int grid = grid_for((d.s + 255) / 256, 4);
-        k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, out, src, r, d.W, d.ldw, d.k, partial,
-                                     tickets + 0, d.G, tvec, doneflag);
+        const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 4);
+        k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, out, hE[l].rbuf, n, src, r, d.W, d.ldw, d.k,
+                                     partial, tickets + 0, tvec, doneflag);
         CK(cudaGetLastError());
       }
-      if (d.k > 0) {                                              // u2 + z2
+      if (d.k > 0) {                                              // u2 + z2, G s formed in every CTA
+        if (dist) {
+          if (d.s == 0) CK(cudaMemsetAsync(tvec, 0, d.k * sizeof(D), s));
+          allreduce(tvec, d.k);                                   // W^H all-reduce
+        }
         Timed t(ctx->prof, s, KC_WAXPY);
-        const int grid = grid_for((d.s + 255) / 256, 8);
-        k_waxpy<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.W, d.ldw, d.k, tvec, r, doneflag);
+        const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 8);
+        k_waxpy<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.W, d.ldw, d.k, d.G, tvec, r, doneflag);
         CK(cudaGetLastError());
       }
     }
   }
-  // bottom: C_{L-1}^{-1} by block-Jacobi ILU
+  // bottom: C_{L-1}^{-1} by block-Jacobi ILU, replicated on every rank
   const D *src = (l0 == L) ? in : r;
-  launch_trisolve(ctx, last, TRI_DOWN, src, out, tmp, (const CsrDev<D> *)nullptr, 0, doneflag, KC_TRI_LAST);
+  const int64_t lL = plan.lo[L], nown = n - lL;
+  if (!dist) {
+    launch_trisolve(ctx, last, TRI_DOWN, src + lL, out + lL, tmp, FArgs<D>{}, doneflag, KC_TRI_LAST);
+  } else {
+    CK(cudaMemsetAsync(rl_full, 0, plan.slast * sizeof(D), s));
+    if (nown > 0)
+      k_scatter_idx<D><<<grid_for((nown + 255) / 256, 2), 256, 0, s>>>(nown, last_idx_d, src + lL, rl_full, doneflag);
+    allreduce(rl_full, plan.slast);                               // gather r_last (zeros elsewhere)
+    launch_trisolve(ctx, last, TRI_DOWN, rl_full, yl_full, tmp, FArgs<D>{}, doneflag, KC_TRI_LAST);
+    if (nown > 0)
+      k_gather_idx<D><<<grid_for((nown + 255) / 256, 2), 256, 0, s>>>(nown, last_idx_d, yl_full, out + lL, doneflag);
+  }
   // up: y1 = z1 - U^-1 L^-1 F_l y2
   for (int l = L - 1; l >= l0; --l) {
     LevelDev<D> &d = lev[l];
-    launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, &d.F, d.o0, doneflag, KC_TRI_UP);
+    exchange(hF[l], out, doneflag);                               // y entries of F_l's exterior columns
+    FArgs<D> fa;
+    fa.F = &d.F;
+    fa.Fbase = d.o0;
+    fa.nloc = n;
+    fa.yh = hF[l].rbuf;
+    fa.nh = hF[l].nrecv;
+    fa.yl = yl_full;
+    launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP);
   }
 }
 
@@ -476,11 +683,20 @@ void Engine<T>::ghat(int l, D *bufA, D *bufB) {
   apply_from(l + 1, bufA, bufB, nullptr);
   // bufB[I_l] = 0 - U^-1 L^-1 F_l c = -u
   CK(cudaMemsetAsync(bufB + d.o0, 0, (d.o1 - d.o0) * sizeof(D), s));
-  launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, bufB, tmp, &d.F, d.o0, nullptr, KC_TRI_UP);
-  // bufB[J_l] = 0 - E_l (-u) = E_l u   (k = 0 mode of K6+K7, src = 0)
-  const int grid = grid_for((d.s + 255) / 256, 4);
-  k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, bufB, (const D *)nullptr, bufB, (const D *)nullptr, 0,
-                               0, partial, tickets + 1, (const D *)nullptr, tvec, nullptr);
+  exchange(hF[l], bufB, nullptr);
+  FArgs<D> fa;
+  fa.F = &d.F;
+  fa.Fbase = d.o0;
+  fa.nloc = n;
+  fa.yh = hF[l].rbuf;
+  fa.nh = hF[l].nrecv;
+  fa.yl = yl_full;
+  launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, bufB, tmp, fa, nullptr, KC_TRI_UP);
+  // bufB[J_l] = 0 - E_l (-u) = E_l u   (K6+K7 with k = 0, src = 0)
+  exchange(hE[l], bufB, nullptr);
+  const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 4);
+  k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, bufB, hE[l].rbuf, n, (const D *)nullptr, bufB,
+                               (const D *)nullptr, 0, 0, partial, tickets + 1, tvec, nullptr);
   CK(cudaGetLastError());
 }
 
@@ -497,6 +713,8 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
   else if (ncols <= 24) go(k_gs<D, 4, 3>, 4);
   else if (ncols <= 48) go(k_gs<D, 2, 6>, 2);
   else go(k_gs<D, 1, 13>, 1);
+  CK(cudaGetLastError());
+  allreduce(resv, dot ? ncols + 1 : 1);                          // dots and norms over ranks
   CK(cudaGetLastError());
 }
 
@@ -560,25 +778,29 @@ void Engine<T>::build_lowrank(const gemslr_params &prm, unsigned long long seed)
   D *hres = ctx->pool.get<D>(3 * (GS_MAXC + 2));
   for (int l = L - 1; l >= 0; --l) {
     LevelDev<D> &d = lev[l];
-    const int64_t sl = d.s;
+    const int64_t sl = d.s;                                       // rows of J_l on this rank
+    const int64_t sg = nglob - plan.st.o[l + 1];                  // rows of J_l on all ranks
     int k = prm.rank;
-    if (k <= 0 || sl == 0) { d.k = 0; continue; }
-    if (k > sl) k = (int)sl;
-    int m = std::min<int64_t>(2 * (int64_t)k, sl);
-    if (m < k + 1 && m < sl) m = k + 1;
+    if (k <= 0 || sg == 0) { d.k = 0; continue; }
+    if (k > sg) k = (int)sg;
+    int m = std::min<int64_t>(2 * (int64_t)k, sg);
+    if (m < k + 1 && m < sg) m = k + 1;
     if (m + 1 > GS_MAXC) throw Error{GEMSLR_ERR_INVALID_ARG, "rank too large for the Arnoldi workspace (2k+1 > 104)"};
-    const int64_t ld = (sl + 31) / 32 * 32;
+    const int64_t ld = (std::max<int64_t>(sl, 1) + 31) / 32 * 32;
     D *Vb = ctx->pool.get<D>((size_t)ld * (m + 1));
     D *Wt = ctx->pool.get<D>((size_t)ld * (k + 2));
     D *Yd = ctx->pool.get<D>((size_t)m * (k + 2));
-    // start vector: uniform[-1,1] from the seed (reading Q8), normalised
+    // start vector: uniform[-1,1] from the seed over the GLOBAL rows of J_l
+    // (reading Q8), this rank's rows taken from it, normalised
     std::mt19937_64 rng(seed + 7919ull * (unsigned long long)(l + 1));
     std::uniform_real_distribution<double> U(-1.0, 1.0);
-    std::vector<T> v0(sl);
-    for (auto &e : v0) {
+    std::vector<T> vg(sg);
+    for (auto &e : vg) {
       if constexpr (std::is_same<T, double>::value) e = U(rng); else e = zc(U(rng), U(rng));
     }
-    CK(cudaMemcpyAsync(Vb, v0.data(), sl * sizeof(D), cudaMemcpyHostToDevice, s));
+    std::vector<T> v0(sl);
+    for (int64_t i = 0; i < sl; ++i) v0[i] = vg[plan.gpos[d.o1 + i] - plan.st.o[l + 1]];
+    if (sl > 0) CK(cudaMemcpyAsync(Vb, v0.data(), sl * sizeof(D), cudaMemcpyHostToDevice, s));
     double nv = norm(Vb, sl, 2);
     if (nv == 0.0) throw Error{GEMSLR_ERR_LOWRANK, "Arnoldi start vector is zero"};
     {
@@ -993,6 +1215,7 @@ std::string Engine<T>::stats_json() const {
   const Structure &st = plan.st;
   std::string j = "{";
   j += "\"n\": " + std::to_string(plan.Ahat.n) + ", \"nnz\": " + std::to_string(plan.Ahat.nnz());
+  j += ", \"nnz_local\": " + std::to_string(plan.Aloc.nnz());
   j += ", \"levels\": " + std::to_string(st.L);
   j += ", \"level_off\": [";
   for (size_t i = 0; i < st.o.size(); ++i) j += (i ? ", " : "") + std::to_string(st.o[i]);
@@ -1017,6 +1240,15 @@ std::string Engine<T>::stats_json() const {
   j += ", \"setup_host_s\": " + std::to_string(setup_host_s) + ", \"setup_device_s\": " + std::to_string(setup_dev_s) +
        ", \"arnoldi_s\": " + std::to_string(arnoldi_s);
   j += ", \"device_bytes\": " + std::to_string(ctx->pool.bytes);
+  int64_t hsend = plan.hA.nsend(), hrecv = plan.hA.nrecv();
+  for (size_t l = 0; l < plan.hE.size(); ++l) {
+    hsend += plan.hE[l].nsend() + plan.hF[l].nsend();
+    hrecv += plan.hE[l].nrecv() + plan.hF[l].nrecv();
+  }
+  j += ", \"nranks\": " + std::to_string(plan.nranks) + ", \"rank\": " + std::to_string(plan.rank) +
+       ", \"n_local\": " + std::to_string(plan.nloc) + ", \"halo_send\": " + std::to_string(hsend) +
+       ", \"halo_recv\": " + std::to_string(hrecv) + ", \"allreduces\": " + std::to_string(ctx->comm.allreduces) +
+       ", \"exchanges\": " + std::to_string(ctx->comm.exchanges);
   j += ", \"kernels\": {";
   bool first = true;
   for (int k = 0; k < KC_COUNT; ++k) {
@@ -1063,27 +1295,70 @@ static gemslr_status guarded(gemslr_ctx *c, F &&fn) {
 
 extern "C" {
 
-gemslr_status gemslr_create(gemslr_ctx **out, int cuda_device, void *nccl_comm, void *cuda_stream) {
+static gemslr_status create_common(gemslr_ctx **out, int cuda_device, void *cuda_stream, gemslr_ctx **made) {
   if (!out) return GEMSLR_ERR_INVALID_ARG;
   *out = nullptr;
   auto *c = new gemslr_ctx();
   c->device = cuda_device;
   c->host_only = cuda_device < 0;
-  c->nccl = nccl_comm;
   c->stream = static_cast<cudaStream_t>(cuda_stream);
   c->pool.A = &c->alloc;
   if (!c->host_only) {
     int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device >= ndev) {
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device >= ndev || cudaSetDevice(cuda_device) != cudaSuccess) {
       delete c;
       return GEMSLR_ERR_CUDA;
     }
-    if (cudaSetDevice(cuda_device) != cudaSuccess) { delete c; return GEMSLR_ERR_CUDA; }
   }
+  *made = c;
+  return GEMSLR_OK;
+}
+
+gemslr_status gemslr_create(gemslr_ctx **out, int cuda_device, void *nccl_comm, void *cuda_stream) {
+  gemslr_ctx *c = nullptr;
+  gemslr_status st = create_common(out, cuda_device, cuda_stream, &c);
+  if (st) return st;
   if (nccl_comm) {
-    c->err = "multi-GPU communicators are not supported by this build (single GPU per context)";
-    delete c;
-    return GEMSLR_ERR_NCCL;
+    if (c->host_only) { delete c; return GEMSLR_ERR_INVALID_ARG; }
+    try {
+      c->comm.borrow(nccl_comm, nullptr);
+    } catch (const Error &e) {
+      delete c;
+      return (gemslr_status)e.code;
+    }
+  }
+  *out = c;
+  return GEMSLR_OK;
+}
+
+gemslr_status gemslr_nccl_unique_id(const char *nccl_lib, void *id128) {
+  if (!id128) return GEMSLR_ERR_INVALID_ARG;
+  try {
+    void *h = Comm::open_lib(nccl_lib);
+    auto f = reinterpret_cast<int (*)(void *)>(dlsym(h, "ncclGetUniqueId"));
+    if (!f || f(id128) != 0) return GEMSLR_ERR_NCCL;
+  } catch (const Error &e) {
+    return (gemslr_status)e.code;
+  }
+  return GEMSLR_OK;
+}
+
+gemslr_status gemslr_create_dist(gemslr_ctx **out, int cuda_device, void *cuda_stream, int nranks, int rank,
+                                 const void *nccl_id, const char *nccl_lib) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return GEMSLR_ERR_INVALID_ARG;
+  gemslr_ctx *c = nullptr;
+  gemslr_status st = create_common(out, cuda_device, cuda_stream, &c);
+  if (st) return st;
+  c->comm.nranks = nranks;
+  c->comm.rank = rank;
+  if (!c->host_only && nranks > 1) {
+    if (!nccl_id) { delete c; return GEMSLR_ERR_INVALID_ARG; }
+    try {
+      c->comm.init(nccl_lib, nranks, rank, nccl_id);
+    } catch (const Error &e) {
+      delete c;
+      return (gemslr_status)e.code;
+    }
   }
   *out = c;
   return GEMSLR_OK;
@@ -1122,6 +1397,8 @@ static gemslr_status do_setup(gemslr_ctx *c, std::unique_ptr<Engine<T>> &E, int6
   opt.tau = prm->ilut_drop;
   opt.lfil = prm->ilut_fill > 0 ? prm->ilut_fill : 10;
   opt.last_blocks = prm->last_blocks;
+  opt.nranks = c->comm.nranks;
+  opt.rank = c->comm.rank;
   if (c->coord_dim > 0 && c->coords_src) {
     c->coords.assign(c->coords_src, c->coords_src + (size_t)n * c->coord_dim);
     opt.coord_dim = c->coord_dim;
@@ -1178,10 +1455,35 @@ gemslr_status gemslr_setup(gemslr_ctx *c, gemslr_dtype dtype, int64_t n, const i
 gemslr_status gemslr_layout(const gemslr_ctx *c, int64_t *n_local, int64_t *grow) {
   if (!c || !n_local) return GEMSLR_ERR_INVALID_ARG;
   if (!c->ready) return fail(c, GEMSLR_ERR_STATE, "layout before setup");
-  const Structure &st = c->dtype == GEMSLR_F64 ? c->ed->plan.st : c->ez->plan.st;
-  *n_local = st.n;
-  if (grow) std::memcpy(grow, st.perm.data(), st.n * sizeof(int64_t));
+  auto go = [&](const auto &pl) {
+    *n_local = pl.nloc;
+    if (grow)
+      for (int64_t i = 0; i < pl.nloc; ++i) grow[i] = pl.st.perm[pl.gpos[i]];
+  };
+  if (c->dtype == GEMSLR_F64) go(c->ed->plan); else go(c->ez->plan);
   return GEMSLR_OK;
+}
+
+// Halo plan of this rank (tests): which = 0 SpMV, 1 E_l, 2 F_l.  counts[2*nranks]:
+// values sent to / received from each rank; sglob / rglob (may be NULL):
+// global permuted positions, concatenated by peer in rank order.
+gemslr_status gemslr_halo_plan(const gemslr_ctx *c, int which, int level, int64_t *counts, int64_t *sglob,
+                               int64_t *rglob) {
+  if (!c || !counts || which < 0 || which > 2) return GEMSLR_ERR_INVALID_ARG;
+  if (!c->ready) return fail(c, GEMSLR_ERR_STATE, "halo_plan before setup");
+  auto go = [&](const auto &pl) -> gemslr_status {
+    if (which > 0 && (level < 0 || level >= pl.st.L)) return GEMSLR_ERR_INVALID_ARG;
+    const HaloPlan &h = which == 0 ? pl.hA : (which == 1 ? pl.hE[level] : pl.hF[level]);
+    for (int r = 0; r < 2 * pl.nranks; ++r) counts[r] = 0;
+    for (size_t i = 0; i < h.peer.size(); ++i) {
+      counts[h.peer[i]] = h.soff[i + 1] - h.soff[i];
+      counts[pl.nranks + h.peer[i]] = h.roff[i + 1] - h.roff[i];
+    }
+    if (sglob) std::copy(h.sglob.begin(), h.sglob.end(), sglob);
+    if (rglob) std::copy(h.rglob.begin(), h.rglob.end(), rglob);
+    return GEMSLR_OK;
+  };
+  return c->dtype == GEMSLR_F64 ? go(c->ed->plan) : go(c->ez->plan);
 }
 
 static gemslr_status need_device(const gemslr_ctx *c) {
@@ -1232,22 +1534,22 @@ template <typename T>
 static gemslr_status host_solve(gemslr_ctx *c, Engine<T> &E, const void *b_host, void *x_host, double rtol, int restart,
                                 int maxit, int *its, double *hist, int hcap, int *hlen, double *frel) {
   using D = typename Dev<T>::type;
-  const int64_t n = E.n;
+  const int64_t n = E.n, ng = E.nglob;            // local rows, global rows
   cudaStream_t s = c->stream;
   if (!E.xb) {
-    E.xb = c->pool.get<D>(4 * (n + 1));
+    E.xb = c->pool.get<D>(2 * (n + 1) + 2 * (ng + 1));
     E.bb = E.xb + (n + 1);
   }
-  D *bn = E.bb + (n + 1), *xn = E.bb + 2 * (n + 1);
-  CK(cudaMemcpyAsync(bn, b_host, n * sizeof(D), cudaMemcpyHostToDevice, s));
-  if (x_host) CK(cudaMemcpyAsync(xn, x_host, n * sizeof(D), cudaMemcpyHostToDevice, s));
-  else CK(cudaMemsetAsync(xn, 0, n * sizeof(D), s));
+  D *bn = E.bb + (n + 1), *xn = bn + (ng + 1);
+  CK(cudaMemcpyAsync(bn, b_host, ng * sizeof(D), cudaMemcpyHostToDevice, s));
+  if (x_host) CK(cudaMemcpyAsync(xn, x_host, ng * sizeof(D), cudaMemcpyHostToDevice, s));
+  else CK(cudaMemsetAsync(xn, 0, ng * sizeof(D), s));
   const int grid = grid_for((n + 255) / 256, 4);
   k_perm<D><<<grid, 256, 0, s>>>(n, E.perm_d, bn, E.bb, 0);
   k_perm<D><<<grid, 256, 0, s>>>(n, E.perm_d, xn, E.xb, 0);
   int rc = E.solve(E.bb, E.xb, rtol, restart, maxit, its, hist, hcap, hlen, frel);
-  k_perm<D><<<grid, 256, 0, s>>>(n, E.perm_d, E.xb, xn, 1);
-  CK(cudaMemcpyAsync(x_host, xn, n * sizeof(D), cudaMemcpyDeviceToHost, s));
+  k_perm<D><<<grid, 256, 0, s>>>(n, E.perm_d, E.xb, xn, 1);   // owned entries; the others keep x0
+  CK(cudaMemcpyAsync(x_host, xn, ng * sizeof(D), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return (gemslr_status)rc;
 }
@@ -1289,6 +1591,7 @@ gemslr_status gemslr_to_natural(gemslr_ctx *c, const void *xl, void *xn) { retur
 gemslr_status gemslr_export_setup(const gemslr_ctx *c, const char *dir) {
   if (!c || !dir) return GEMSLR_ERR_INVALID_ARG;
   if (!c->ready) return fail(c, GEMSLR_ERR_STATE, "export before setup");
+  if (c->comm.nranks > 1) return fail(c, GEMSLR_ERR_STATE, "export_setup is single-rank only");
   return guarded(const_cast<gemslr_ctx *>(c), [&]() -> gemslr_status {
     if (c->dtype == GEMSLR_F64) c->ed->export_bundle(dir); else c->ez->export_bundle(dir);
     return GEMSLR_OK;

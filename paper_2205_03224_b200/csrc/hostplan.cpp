@@ -93,6 +93,49 @@ void make_stage(const std::vector<int64_t> &bl, const std::vector<Factor<T>> &fa
 
 }  // namespace
 
+// Halo plan of this rank from every rank's sorted list of needed remote
+// positions (all ranks compute the same lists, so sends and receives match).
+static HaloPlan make_halo(int rank, int nranks, const std::vector<int32_t> &owner, const std::vector<int64_t> &loc,
+                          const std::vector<std::vector<int64_t>> &needed) {
+  HaloPlan h;
+  std::vector<std::vector<int64_t>> sendto(nranks), recvfrom(nranks);
+  for (int64_t pos : needed[rank]) recvfrom[owner[pos]].push_back(pos);
+  for (int r = 0; r < nranks; ++r) {
+    if (r == rank) continue;
+    for (int64_t pos : needed[r])
+      if (owner[pos] == rank) sendto[r].push_back(pos);
+  }
+  for (int r = 0; r < nranks; ++r) {
+    if (r == rank || (sendto[r].empty() && recvfrom[r].empty())) continue;
+    h.peer.push_back(r);
+    for (int64_t pos : sendto[r]) { h.sidx.push_back((int32_t)loc[pos]); h.sglob.push_back(pos); }
+    for (int64_t pos : recvfrom[r]) h.rglob.push_back(pos);
+    h.soff.push_back((int64_t)h.sidx.size());
+    h.roff.push_back((int64_t)h.rglob.size());
+  }
+  return h;
+}
+
+// needed[r]: sorted unique remote positions referenced by rank r's rows
+// [r0, r1) of M (columns in [c0, c1), excluding `skip_from` and above).
+template <typename T>
+static std::vector<std::vector<int64_t>> needed_sets(const Csr<T> &M, int nranks, const std::vector<int32_t> &owner,
+                                                     int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+  std::vector<std::vector<int64_t>> need(nranks);
+  for (int64_t i = r0; i < r1; ++i) {
+    const int r = owner[i];
+    for (int64_t p = M.ptr[i]; p < M.ptr[i + 1]; ++p) {
+      const int64_t j = M.col[p];
+      if (j >= c0 && j < c1 && owner[j] != r) need[r].push_back(j);
+    }
+  }
+  for (auto &v : need) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }
+  return need;
+}
+
 template <typename T>
 bool build_host_plan(int64_t n, const int64_t *rowptr, const int32_t *colidx, const T *vals,
                      const SetupOptions &opt, HostPlan<T> &plan, Error &err) {
@@ -105,26 +148,159 @@ bool build_host_plan(int64_t n, const int64_t *rowptr, const int32_t *colidx, co
       if (p > rowptr[i] && colidx[p] <= colidx[p - 1]) { err = {-2, "BAD_CSR: unsorted or duplicate columns in row " + std::to_string(i)}; return false; }
     }
   }
+  const int G = opt.nranks, me = opt.rank;
+  if (G < 1 || me < 0 || me >= G || opt.p % G != 0) {
+    err = {-1, "INVALID_ARG: subdomains must be a multiple of the number of ranks (P:L76)"};
+    return false;
+  }
   Graph g = build_graph(n, rowptr, colidx);
   if (!build_structure(g, opt, plan.st, err)) return false;
   const Structure &st = plan.st;
   plan.Ahat = permute(n, rowptr, colidx, vals, st);
+  const Csr<T> &Ah = plan.Ahat;
   const int L = st.L;
-  plan.fac.resize(L);
-  plan.E.resize(L);
-  plan.F.resize(L);
-  plan.stage.resize(L);
+  plan.nranks = G;
+  plan.rank = me;
+  // ---- ownership: level-0 parts in contiguous rank ranges;
+  // a part of a later level (and a C_last row) goes to the rank owning most of
+  // its neighbours in earlier levels (ties -> lower rank)
+  std::vector<int32_t> &owner = plan.owner;
+  owner.assign(n, 0);
+  std::vector<std::vector<int32_t>> blk_owner(L);
+  auto vote = [&](int64_t r0, int64_t r1, int64_t below) {
+    std::vector<int64_t> v(G, 0);
+    for (int64_t i = r0; i < r1; ++i)
+      for (int64_t p = Ah.ptr[i]; p < Ah.ptr[i + 1]; ++p)
+        if (Ah.col[p] < below) v[owner[Ah.col[p]]]++;
+    int best = 0;
+    for (int r = 1; r < G; ++r)
+      if (v[r] > v[best]) best = r;
+    return best;
+  };
+  for (int l = 0; l < L; ++l) {
+    const auto &bl = st.blk[l];
+    const int nb = (int)bl.size() - 1;
+    blk_owner[l].assign(nb, 0);
+    for (int q = 0; q < nb; ++q) {
+      const int r = (l == 0) ? (int)((int64_t)q * G / nb) : (G == 1 ? 0 : vote(bl[q], bl[q + 1], st.o[l]));
+      blk_owner[l][q] = r;
+      for (int64_t i = bl[q]; i < bl[q + 1]; ++i) owner[i] = r;
+    }
+  }
+  if (G > 1)
+    for (int64_t i = st.o[L]; i < n; ++i) owner[i] = vote(i, i + 1, st.o[L]);
+  // ---- local layout
+  std::vector<int64_t> loc(n, -1);
+  plan.gpos.clear();
+  plan.lo.assign(L + 1, 0);
+  for (int l = 0; l <= L; ++l) {
+    plan.lo[l] = (int64_t)plan.gpos.size();
+    const int64_t a = st.o[l], b = (l == L) ? n : st.o[l + 1];
+    for (int64_t i = a; i < b; ++i)
+      if (owner[i] == me) { loc[i] = (int64_t)plan.gpos.size(); plan.gpos.push_back(i); }
+  }
+  plan.nloc = (int64_t)plan.gpos.size();
+  plan.slast = n - st.o[L];
+  const int64_t nloc = plan.nloc;
+  plan.last_idx.clear();
+  for (int64_t j = plan.lo[L]; j < nloc; ++j) plan.last_idx.push_back((int32_t)(plan.gpos[j] - st.o[L]));
+  // ---- halo plans
+  plan.hA = make_halo(me, G, owner, loc, needed_sets(Ah, G, owner, 0, n, 0, n));
+  plan.hE.assign(L, HaloPlan());
+  plan.hF.assign(L, HaloPlan());
+  for (int l = 0; l < L; ++l) {
+    plan.hE[l] = make_halo(me, G, owner, loc, needed_sets(Ah, G, owner, st.o[l + 1], n, st.o[l], st.o[l + 1]));
+    const int64_t fcend = (G > 1) ? st.o[L] : n;       // C_last is replicated when G > 1
+    plan.hF[l] = make_halo(me, G, owner, loc, needed_sets(Ah, G, owner, st.o[l], st.o[l + 1], st.o[l + 1], fcend));
+  }
+  auto halo_index = [](const HaloPlan &h) {
+    std::vector<std::pair<int64_t, int64_t>> m;
+    for (int64_t i = 0; i < (int64_t)h.rglob.size(); ++i) m.push_back({h.rglob[i], i});
+    std::sort(m.begin(), m.end());
+    return m;
+  };
+  auto lookup = [](const std::vector<std::pair<int64_t, int64_t>> &m, int64_t pos) {
+    auto it = std::lower_bound(m.begin(), m.end(), std::make_pair(pos, (int64_t)-1));
+    return it->second;
+  };
+  // ---- local operators with remapped columns
+  auto local_rows = [&](int64_t lr0, int64_t lr1, int64_t c0, int64_t c1, const HaloPlan &h, bool clast_rep) {
+    Csr<T> M;
+    M.n = lr1 - lr0;
+    M.ptr.assign(M.n + 1, 0);
+    const auto idx = halo_index(h);
+    const int64_t nh = h.nrecv();
+    for (int64_t li = lr0; li < lr1; ++li) {
+      const int64_t i = plan.gpos[li];
+      for (int64_t p = Ah.ptr[i]; p < Ah.ptr[i + 1]; ++p) {
+        const int64_t j = Ah.col[p];
+        if (j < c0 || j >= c1) continue;
+        int64_t c;
+        if (clast_rep && j >= st.o[L]) c = nloc + nh + (j - st.o[L]);
+        else if (owner[j] == me) c = loc[j];
+        else c = nloc + lookup(idx, j);
+        M.col.push_back((int32_t)c);
+        M.val.push_back(Ah.val[p]);
+      }
+      M.ptr[li - lr0 + 1] = (int64_t)M.col.size();
+    }
+    return M;
+  };
+  plan.Aloc = local_rows(0, nloc, 0, n, plan.hA, false);
+  plan.E.assign(L, Csr<T>());
+  plan.F.assign(L, Csr<T>());
+  plan.fac.assign(L, {});
+  plan.stage.assign(L, Stage<T>());
   plan.fac_nnz = 0;
   for (int l = 0; l < L; ++l) {
-    if (!factor_blocks(plan.Ahat, st.blk[l], opt, plan.fac[l], "level " + std::to_string(l), err)) return false;
-    plan.E[l] = sub(plan.Ahat, st.o[l + 1], n, st.o[l], st.o[l + 1], false);
-    plan.F[l] = sub(plan.Ahat, st.o[l], st.o[l + 1], st.o[l + 1], n, false);
-    for (auto &f : plan.fac[l]) plan.fac_nnz += f.L.nnz() + f.U.nnz();
-    make_stage(st.blk[l], plan.fac[l], plan.stage[l]);
+    const auto &bl = st.blk[l];
+    const int nb = (int)bl.size() - 1;
+    // factor the owned blocks only (independent per subdomain)
+    std::vector<int64_t> own_bl{bl[0]};
+    std::vector<int> own_q;
+    for (int q = 0; q < nb; ++q)
+      if (blk_owner[l][q] == me) own_q.push_back(q);
+    std::vector<Factor<T>> own_fac;
+    {
+      std::vector<int64_t> b2;
+      std::vector<Factor<T>> f2;
+      for (int q : own_q) { b2.push_back(bl[q]); b2.push_back(bl[q + 1]); }
+      // factor each owned block independently
+      const int no = (int)own_q.size();
+      f2.assign(no, Factor<T>());
+      std::vector<std::string> errs(no);
+      std::vector<char> ok(no, 1);
+#pragma omp parallel for schedule(dynamic, 1)
+      for (int t = 0; t < no; ++t) {
+        const int q = own_q[t];
+        Csr<T> B = sub(Ah, bl[q], bl[q + 1], bl[q], bl[q + 1], true);
+        ok[t] = opt.ilu == 0 ? ilu0(B, f2[t], errs[t]) : ilut(B, opt.tau, opt.lfil, f2[t], errs[t]);
+      }
+      for (int t = 0; t < no; ++t)
+        if (!ok[t]) {
+          err = {-4, "ZERO_PIVOT: level " + std::to_string(l) + ", block " + std::to_string(own_q[t]) + ": " + errs[t]};
+          return false;
+        }
+      plan.fac[l].assign(nb, Factor<T>());
+      for (int t = 0; t < no; ++t) {
+        plan.fac_nnz += f2[t].L.nnz() + f2[t].U.nnz();
+        plan.fac[l][own_q[t]] = f2[t];
+      }
+      own_fac = f2;
+    }
+    // local stage: owned blocks are contiguous in the local layout
+    std::vector<int64_t> lb{plan.lo[l]};
+    for (size_t t = 0; t < own_q.size(); ++t) lb.push_back(lb.back() + (bl[own_q[t] + 1] - bl[own_q[t]]));
+    make_stage(lb, own_fac, plan.stage[l]);
+    plan.E[l] = local_rows(plan.lo[l + 1], nloc, st.o[l], st.o[l + 1], plan.hE[l], false);
+    plan.F[l] = local_rows(plan.lo[l], plan.lo[l + 1], st.o[l + 1], n, plan.hF[l], G > 1);
   }
-  if (!factor_blocks(plan.Ahat, st.last, opt, plan.lastfac, "C_last", err)) return false;
+  // C_last: every rank factors and solves all blocks (replicated)
+  if (!factor_blocks(Ah, st.last, opt, plan.lastfac, "C_last", err)) return false;
   for (auto &f : plan.lastfac) plan.fac_nnz += f.L.nnz() + f.U.nnz();
-  make_stage(st.last, plan.lastfac, plan.last_stage);
+  std::vector<int64_t> rel;
+  for (int64_t v : st.last) rel.push_back(v - st.o[L]);
+  make_stage(rel, plan.lastfac, plan.last_stage);
   return true;
 }
 

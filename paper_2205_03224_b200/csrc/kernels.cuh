@@ -83,11 +83,13 @@ __device__ inline void cluster_sync_all() {
 // ----------------------------------------------------------------- K1 SpMV
 // SELL-32: slice s holds rows 32s..32s+31; entry e of lane r at off[s] + 32e + r;
 // padding has col = -1.  mode 0: y = A x ; mode 1: y = b - A x.
-template <typename T>
+// Columns c >= nloc refer to the halo buffer xh (values received from the
+// owners of exterior columns, Note N P:L59-61); one GPU has no halo.
+template <typename T, bool HALO>
 __global__ void __launch_bounds__(256) k_spmv_sell(int64_t n, int64_t nslices, const int64_t *__restrict__ off,
                                                    const int32_t *__restrict__ col, const T *__restrict__ val,
-                                                   const T *__restrict__ x, T *__restrict__ y, int mode,
-                                                   const T *__restrict__ b, const int *__restrict__ done) {
+                                                   const T *__restrict__ x, const T *__restrict__ xh, T *__restrict__ y,
+                                                   int mode, const T *__restrict__ b, const int *__restrict__ done) {
   if (done && *done) return;
   const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= nslices) return;
@@ -101,10 +103,27 @@ __global__ void __launch_bounds__(256) k_spmv_sell(int64_t n, int64_t nslices, c
   for (int e = 0; e < w; ++e) {
     const int32_t c = __ldg(cp + 32 * e);
     const T v = ld_nc(vp + 32 * e);
-    if (c >= 0) acc += v * ld_nc(x + c);
+    if (c >= 0) acc += v * ((!HALO || c < n) ? ld_nc(x + c) : ld_nc(xh + (c - n)));
   }
   const int64_t row = s * 32 + lane;
   if (row < n) y[row] = mode ? b[row] - acc : acc;
+}
+
+// halo send buffer: buf[i] = src[idx[i]]
+template <typename T>
+__global__ void k_gather_idx(int64_t n, const int *__restrict__ idx, const T *__restrict__ src, T *__restrict__ buf,
+                             const int *__restrict__ done) {
+  if (done && *done) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = src[idx[i]];
+}
+// replicated last separator: dst[idx[i]] = src[i] (scatter) / dst[i] = src[idx[i]] (gather)
+template <typename T>
+__global__ void k_scatter_idx(int64_t n, const int *__restrict__ idx, const T *__restrict__ src, T *__restrict__ dst,
+                              const int *__restrict__ done) {
+  if (done && *done) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[idx[i]] = src[i];
 }
 
 // ----------------------------------------------------------------- K4/K5/K9 trisolve
@@ -156,11 +175,13 @@ __global__ void __launch_bounds__(256) k_trisolve(TriDev<T> Lp, TriDev<T> Up, co
     in = rhs;
     out = x;
   } else {
-    for (int64_t i = r0 + gt; i < r1; i += nt) {              // t = F_l y_J
-      const int64_t li = i - Fbase;
-      T acc = dzero<T>();
-      for (int64_t p = Fptr[li]; p < Fptr[li + 1]; ++p) acc += Fval[p] * x[Fcol[p]];
-      tmp[i] = acc;
+    if (Fptr) {                                                 // t = F_l y_J (else precomputed in tmp)
+      for (int64_t i = r0 + gt; i < r1; i += nt) {
+        const int64_t li = i - Fbase;
+        T acc = dzero<T>();
+        for (int64_t p = Fptr[li]; p < Fptr[li + 1]; ++p) acc += Fval[p] * x[Fcol[p]];
+        tmp[i] = acc;
+      }
     }
     barrier();
     in = tmp;
@@ -457,12 +478,16 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
 }
 
 // Packs the L-sweep right-hand sides of a stage in chunk order:
-// DOWN: dst[lpos[i]] = src[row0 + i];  UP: dst[lpos[i]] = (F_l y_J)_{row0 + i}.
+// DOWN: dst[lpos[i]] = src[row0 + i];  UP: dst[lpos[i]] = (F_l y_J)_{row0 + i},
+// with F_l's columns local (< nloc), in the halo yh (< nloc + nh) or in the
+// replicated last-separator vector yl.
 template <typename T>
 __global__ void __launch_bounds__(256) k_pack_rhs(int64_t nrows, int64_t row0, const int *__restrict__ lpos, T *__restrict__ dst,
                                                   const T *__restrict__ src, const int64_t *__restrict__ Fptr,
                                                   const int32_t *__restrict__ Fcol, const T *__restrict__ Fval,
-                                                  int64_t Fbase, const T *__restrict__ y, const int *__restrict__ done) {
+                                                  int64_t Fbase, const T *__restrict__ y, int64_t nloc,
+                                                  const T *__restrict__ yh, int64_t nh, const T *__restrict__ yl,
+                                                  const int *__restrict__ done) {
   if (done && *done) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
     T v;
@@ -471,9 +496,13 @@ __global__ void __launch_bounds__(256) k_pack_rhs(int64_t nrows, int64_t row0, c
     } else {
       const int64_t li = row0 + i - Fbase;
       v = dzero<T>();
-      for (int64_t p = Fptr[li]; p < Fptr[li + 1]; ++p) v += Fval[p] * y[Fcol[p]];
+      for (int64_t p = Fptr[li]; p < Fptr[li + 1]; ++p) {
+        const int64_t c = Fcol[p];
+        const T yc = c < nloc ? y[c] : (c < nloc + nh ? yh[c - nloc] : yl[c - nloc - nh]);
+        v += Fval[p] * yc;
+      }
     }
-    dst[lpos[i]] = v;
+    dst[lpos ? lpos[i] : row0 + i] = v;
   }
 }
 
@@ -494,20 +523,21 @@ __device__ inline void reduce_partials(const T *partial, int G, int ncol, T *out
 }
 
 // ----------------------------------------------------------------- K6+K7
-// Rows J_l = [rowbase, rowbase + s): dst_i = src_i - Σ_j E_ij z_j (src == nullptr: 0),
-// then per-column partial sums of conj(W_ic) dst_i; the last CTA reduces the
-// partials in CTA order, s = W^H r_J, and writes t = G s.
+// Rows J_l = [rowbase, rowbase + s): dst_i = src_i - Σ_j E_ij z_j (src == nullptr: 0;
+// columns >= nloc in the halo zh), then per-column partial sums of conj(W_ic) dst_i;
+// the last CTA reduces the partials in CTA order into this rank's part of
+// s = W^H r_J (summed over ranks by an all-reduce).
 // CTA = 8 warps; a tile is 256 rows; warp w owns the columns c ≡ w (mod 8).
 constexpr int EW_NACC = 6;   // k <= 48
 template <typename T>
 __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const int64_t *__restrict__ Eptr,
                                             const int32_t *__restrict__ Ecol, const T *__restrict__ Eval,
-                                            const T *__restrict__ z, const T *src, T *dst, const T *__restrict__ W,
+                                            const T *__restrict__ z, const T *__restrict__ zh, int64_t nloc,
+                                            const T *src, T *dst, const T *__restrict__ W,
                                             int64_t ldw, int k, T *__restrict__ partial, unsigned *ticket,
-                                            const T *__restrict__ G, T *__restrict__ tout, const int *__restrict__ done) {
+                                            T *__restrict__ sout, const int *__restrict__ done) {
   if (done && *done) return;
   __shared__ T sv[256];
-  __shared__ T sred[64];
   __shared__ bool amlast;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   T acc[EW_NACC];
@@ -519,7 +549,10 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
     T v = dzero<T>();
     if (i < s) {
       T e = dzero<T>();
-      for (int64_t p = Eptr[i]; p < Eptr[i + 1]; ++p) e += Eval[p] * z[Ecol[p]];
+      for (int64_t p = Eptr[i]; p < Eptr[i + 1]; ++p) {
+        const int64_t c = Ecol[p];
+        e += Eval[p] * (c < nloc ? z[c] : zh[c - nloc]);
+      }
       v = (src ? src[rowbase + i] : dzero<T>()) - e;
       dst[rowbase + i] = v;
     }
@@ -553,23 +586,26 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
   __syncthreads();
   if (!amlast) return;
   __threadfence();
-  reduce_partials(partial, (int)gridDim.x, k, sred);
-  __syncthreads();
-  if (tid < k) {
-    T t = dzero<T>();
-    for (int a = 0; a < k; ++a) t += G[(int64_t)a * k + tid] * sred[a];   // (G s)_c, G column-major
-    tout[tid] = t;
-  }
+  reduce_partials(partial, (int)gridDim.x, k, sout);             // this rank's part of s = W^H r_J
   if (tid == 0) *ticket = 0;
 }
 
 // ----------------------------------------------------------------- K8
+// r_J += W_l (G_l s): the k x k product G_l s is formed redundantly by every
+// CTA in its prologue, G_l column-major.
 template <typename T>
 __global__ void __launch_bounds__(256) k_waxpy(int64_t s, int64_t rowbase, const T *__restrict__ W, int64_t ldw, int k,
-                                               const T *__restrict__ t, T *dst, const int *__restrict__ done) {
+                                               const T *__restrict__ G, const T *__restrict__ sv, T *dst,
+                                               const int *__restrict__ done) {
   if (done && *done) return;
-  __shared__ T st[64];
-  if (threadIdx.x < k) st[threadIdx.x] = t[threadIdx.x];
+  __shared__ T ss[64], st[64];
+  if (threadIdx.x < k) ss[threadIdx.x] = sv[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < k) {
+    T t = dzero<T>();
+    for (int a = 0; a < k; ++a) t += G[(int64_t)a * k + threadIdx.x] * ss[a];
+    st[threadIdx.x] = t;
+  }
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
     T acc = dzero<T>();

@@ -123,21 +123,52 @@ struct Stage {                                  // the blocks of one level (or o
   PipePack<T> pipe;
 };
 
+// Neighbour exchange of one distributed operator: this rank
+// sends sidx[soff[i]..soff[i+1]) (local indices) to peer[i] and receives
+// roff[i+1]-roff[i] values from peer[i] into its halo buffer at roff[i].
+// sglob / rglob are the global permuted positions of those values.
+struct HaloPlan {
+  std::vector<int32_t> peer;
+  std::vector<int64_t> soff{0}, roff{0};
+  std::vector<int32_t> sidx;
+  std::vector<int64_t> sglob, rglob;
+  int64_t nsend() const { return soff.back(); }
+  int64_t nrecv() const { return roff.back(); }
+};
+
+// Everything below is for THIS rank of `nranks` (one rank: the global problem).
+// Local layout: the owned global positions in ascending order, which is
+// level-major ([owned I_0 | owned I_1 | ... | owned C_last rows]); lo[l] is the
+// local start of level l and lo[L] the start of the owned C_last rows.
+// Column conventions of the local operators:
+//   Aloc, E_l: c < nloc local, else halo index c - nloc (hA / hE[l]);
+//   F_l: c < nloc local, c < nloc + hF[l].nrecv() halo, else the C_last
+//        index c - nloc - nrecv of the replicated last-separator vector (nranks > 1).
 template <typename T>
 struct HostPlan {
   Structure st;
-  Csr<T> Ahat;                                  // Pᵀ A P, absolute columns
-  std::vector<std::vector<Factor<T>>> fac;      // per level, per block (block-local)
-  std::vector<Factor<T>> lastfac;               // per C_last block
-  std::vector<Csr<T>> E;                        // E_l: rows J_l (local row i - o_{l+1}), absolute columns in I_l
-  std::vector<Csr<T>> F;                        // F_l: rows I_l (local row i - o_l), absolute columns in J_l
-  std::vector<Stage<T>> stage;                  // per level
-  Stage<T> last_stage;
-  int64_t fac_nnz = 0;                          // nnz(L+U) over every block (L strict + U incl. diag)
+  Csr<T> Ahat;                                  // Pᵀ A P, global, absolute columns
+  int nranks = 1, rank = 0;
+  std::vector<int32_t> owner;                   // per global position
+  std::vector<int64_t> gpos;                    // local -> global position
+  std::vector<int64_t> lo;                      // local level offsets (L + 1 entries)
+  int64_t nloc = 0, slast = 0;
+  Csr<T> Aloc;                                  // owned rows of Â, local columns
+  HaloPlan hA;
+  std::vector<HaloPlan> hE, hF;
+  std::vector<int32_t> last_idx;                // owned C_last rows: index inside C_last
+  std::vector<std::vector<Factor<T>>> fac;      // per level, per global block (owned blocks filled)
+  std::vector<Factor<T>> lastfac;               // per C_last block (replicated)
+  std::vector<Csr<T>> E;                        // E_l: owned rows of J_l (local row - lo[l+1])
+  std::vector<Csr<T>> F;                        // F_l: owned rows of I_l (local row - lo[l])
+  std::vector<Stage<T>> stage;                  // per level: owned blocks, local rows
+  Stage<T> last_stage;                          // all C_last blocks, rows relative to o_L
+  int64_t fac_nnz = 0;                          // nnz(L+U) of the factors held by this rank
 };
 
 struct SetupOptions {
   int levels = 1, p = 1, ilu = 0, lfil = 10, last_blocks = 0;
+  int nranks = 1, rank = 0;
   double tau = 1e-3;
   int coord_dim = 0;
   const double *coords = nullptr;               // n x coord_dim (optional)
