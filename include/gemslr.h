@@ -97,6 +97,20 @@ gemslr_status gemslr_nccl_unique_id(const char *nccl_lib, void *id128);
 gemslr_status gemslr_create_dist(gemslr_ctx **out, int cuda_device, void *cuda_stream, int nranks, int rank,
                                  const void *nccl_id, const char *nccl_lib);
 
+/* Host-staged communication backend: the caller supplies the collectives as
+ * callbacks on HOST buffers (e.g. torch.distributed over gloo); the library
+ * synchronises its stream and stages device data through pinned memory.  It
+ * runs the same distributed algorithm as the NCCL backend and lets several
+ * ranks share one GPU (each rank only waits on the host, never in a kernel).
+ * allreduce: sum `count` doubles in place over all ranks.  sendrecv: for each
+ * of the npeers peers send sendcounts[i] doubles and receive recvcounts[i]
+ * doubles (a grouped, deadlock-free exchange).  Callbacks return 0 on success. */
+typedef int (*gemslr_allreduce_fn)(void *user, double *buf, size_t count);
+typedef int (*gemslr_sendrecv_fn)(void *user, int npeers, const int *peers, const double *const *sendbufs,
+                                  const size_t *sendcounts, double *const *recvbufs, const size_t *recvcounts);
+gemslr_status gemslr_create_hostcomm(gemslr_ctx **out, int cuda_device, void *cuda_stream, int nranks, int rank,
+                                     gemslr_allreduce_fn allreduce, gemslr_sendrecv_fn sendrecv, void *user);
+
 /* Halo plan of this rank (inspection/tests): which = 0 SpMV, 1 E_l, 2 F_l (level
  * `level`).  counts (host, 2*nranks): values sent to / received from each rank;
  * sglob, rglob (host, may be NULL): global permuted positions of the values,

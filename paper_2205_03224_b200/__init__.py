@@ -21,7 +21,7 @@ _lib = None
 GEMSLR_OK, GEMSLR_NOT_CONVERGED = 0, 1
 STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "INVALID_ARG", -2: "BAD_CSR", -3: "PARTITION", -4: "ZERO_PIVOT",
           -5: "LOWRANK", -6: "STATE", -7: "CUDA", -8: "NCCL", -9: "OOM"}
-ABI_FUNCTIONS = ["gemslr_create", "gemslr_nccl_unique_id", "gemslr_create_dist", "gemslr_halo_plan", "gemslr_set_allocator", "gemslr_set_coordinates", "gemslr_setup", "gemslr_layout",
+ABI_FUNCTIONS = ["gemslr_create", "gemslr_nccl_unique_id", "gemslr_create_dist", "gemslr_create_hostcomm", "gemslr_halo_plan", "gemslr_set_allocator", "gemslr_set_coordinates", "gemslr_setup", "gemslr_layout",
                  "gemslr_spmv", "gemslr_apply_precond", "gemslr_solve", "gemslr_solve_host", "gemslr_to_local",
                  "gemslr_to_natural", "gemslr_export_setup", "gemslr_stats", "gemslr_profile", "gemslr_last_error",
                  "gemslr_destroy"]
@@ -53,6 +53,7 @@ def lib():
         L.gemslr_nccl_unique_id.argtypes = [C.c_char_p, vp]
         L.gemslr_create_dist.argtypes = [C.POINTER(vp), C.c_int, vp, C.c_int, C.c_int, vp, C.c_char_p]
         L.gemslr_halo_plan.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp]
+        L.gemslr_create_hostcomm.argtypes = [C.POINTER(vp), C.c_int, vp, C.c_int, C.c_int, _ALLRED, _SENDRECV, vp]
         L.gemslr_set_coordinates.argtypes = [vp, C.c_int, vp]
         L.gemslr_setup.argtypes = [vp, C.c_int, i64, vp, vp, vp, C.POINTER(Params)]
         L.gemslr_layout.argtypes = [vp, C.POINTER(i64), vp]
@@ -76,6 +77,41 @@ def lib():
                 getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
+
+
+_ALLRED = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_size_t)
+_SENDRECV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.POINTER(C.c_double)),
+                        C.POINTER(C.c_size_t), C.POINTER(C.POINTER(C.c_double)), C.POINTER(C.c_size_t))
+
+
+def _torch_host_callbacks():
+    """Host-staged collectives over the default torch.distributed group (gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    def allreduce(_user, buf, count):
+        try:
+            t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(count,)))
+            dist.all_reduce(t)
+            return 0
+        except Exception:
+            return 1
+
+    def sendrecv(_user, npeers, peers, sbufs, scounts, rbufs, rcounts):
+        try:
+            reqs = []
+            for i in range(npeers):
+                if scounts[i]:
+                    reqs.append(dist.isend(torch.from_numpy(np.ctypeslib.as_array(sbufs[i], shape=(scounts[i],))), peers[i]))
+                if rcounts[i]:
+                    reqs.append(dist.irecv(torch.from_numpy(np.ctypeslib.as_array(rbufs[i], shape=(rcounts[i],))), peers[i]))
+            for r in reqs:
+                r.wait()
+            return 0
+        except Exception:
+            return 1
+
+    return _ALLRED(allreduce), _SENDRECV(sendrecv)
 
 
 def nccl_lib_path():
@@ -105,11 +141,12 @@ class Solver:
 
     def __init__(self, rowptr, colidx, values, levels, subdomains, rank, ilu="ilut", ilut_drop=1e-3,
                  ilut_fill=10, last_blocks=0, coords=None, device=0, stream=None, seed=0, arnoldi_tol=1e-2,
-                 arnoldi_max_cycles=10, cluster_ctas=0, nranks=None, my_rank=None):
+                 arnoldi_max_cycles=10, cluster_ctas=0, nranks=None, my_rank=None, comm="nccl"):
         """nranks/my_rank: None = single GPU, or taken from an initialised
         torch.distributed world (one process per GPU; the NCCL id is broadcast
         with torch.distributed).  device = -1 with explicit nranks/my_rank builds
-        the host-only plan of that rank (no GPU, no NCCL)."""
+        the host-only plan of that rank (no GPU, no NCCL).  comm = "host" uses the
+        host-staged backend over torch.distributed (gloo) instead of NCCL."""
         L = lib()
         self.rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
         self.colidx = np.ascontiguousarray(colidx, dtype=np.int32)
@@ -129,6 +166,10 @@ class Solver:
         self.my_rank = my_rank or 0
         if self.nranks == 1:
             self._check(L.gemslr_create(C.byref(self.h), int(device), None, C.c_void_p(stream or 0)), "create")
+        elif comm == "host" and device >= 0:
+            self._cbs = _torch_host_callbacks()
+            self._check(L.gemslr_create_hostcomm(C.byref(self.h), int(device), C.c_void_p(stream or 0), self.nranks,
+                                                 self.my_rank, self._cbs[0], self._cbs[1], None), "create_hostcomm")
         else:
             libp = nccl_lib_path()
             idb = C.create_string_buffer(128)

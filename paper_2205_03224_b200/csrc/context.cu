@@ -218,14 +218,41 @@ struct Comm {
     nranks = n;
     rank = r;
   }
+  // host-staged backend (gemslr_create_hostcomm): the caller's callbacks move
+  // host buffers (e.g. torch.distributed over gloo); device data is staged
+  // through pinned host memory after a stream synchronisation
+  gemslr_allreduce_fn h_allreduce = nullptr;
+  gemslr_sendrecv_fn h_sendrecv = nullptr;
+  void *h_user = nullptr;
+  double *hbuf = nullptr;
+  size_t hcap = 0;
+  double *host(size_t ndouble) {
+    if (ndouble > hcap) {
+      if (hbuf) cudaFreeHost(hbuf);
+      hcap = std::max<size_t>(ndouble, 1 << 16);
+      if (cudaMallocHost(&hbuf, hcap * sizeof(double)) != cudaSuccess) throw Error{GEMSLR_ERR_OOM, "pinned staging"};
+    }
+    return hbuf;
+  }
+  bool hostmode() const { return h_allreduce != nullptr; }
   // sum over ranks in place; count in doubles (complex = 2 doubles each)
   void allreduce(void *buf, size_t ndouble, cudaStream_t s) {
     if (nranks == 1 || ndouble == 0) return;
-    check(allreduce_(buf, buf, ndouble, 8 /*ncclFloat64*/, 0 /*ncclSum*/, comm, s), "AllReduce");
+    if (hostmode()) {
+      double *h = host(ndouble);
+      if (cudaMemcpyAsync(h, buf, ndouble * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+        throw Error{GEMSLR_ERR_CUDA, "host-staged all-reduce copy"};
+      if (h_allreduce(h_user, h, ndouble) != 0) throw Error{GEMSLR_ERR_NCCL, "host all-reduce callback failed"};
+      if (cudaMemcpyAsync(buf, h, ndouble * 8, cudaMemcpyHostToDevice, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+        throw Error{GEMSLR_ERR_CUDA, "host-staged all-reduce copy"};
+    } else {
+      check(allreduce_(buf, buf, ndouble, 8 /*ncclFloat64*/, 0 /*ncclSum*/, comm, s), "AllReduce");
+    }
     allreduces++;
   }
   ~Comm() {
     if (owned && comm && destroy_) destroy_(comm);
+    if (hbuf) cudaFreeHost(hbuf);
   }
 };
 
@@ -506,13 +533,34 @@ void Engine<T>::exchange(HaloDev<D> &h, const D *src, const int *doneflag) {
     k_gather_idx<D><<<grid, 256, 0, ctx->stream>>>(h.nsend, h.sidx, src, h.sbuf, doneflag);
     CK(cudaGetLastError());
   }
-  C.check(C.gstart_(), "GroupStart");
-  for (size_t i = 0; i < h.peer.size(); ++i) {
-    const int64_t ns = h.soff[i + 1] - h.soff[i], nr = h.roff[i + 1] - h.roff[i];
-    if (ns > 0) C.check(C.send_(h.sbuf + h.soff[i], (size_t)ns * w, 8, h.peer[i], C.comm, ctx->stream), "Send");
-    if (nr > 0) C.check(C.recv_(h.rbuf + h.roff[i], (size_t)nr * w, 8, h.peer[i], C.comm, ctx->stream), "Recv");
+  if (C.hostmode()) {
+    const size_t ns = (size_t)h.nsend * w, nr = (size_t)h.nrecv * w;
+    double *hs = C.host(ns + nr);
+    double *hr = hs + ns;
+    CK(cudaMemcpyAsync(hs, h.sbuf, ns * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::vector<const double *> sp;
+    std::vector<double *> rp;
+    std::vector<size_t> sc, rc;
+    for (size_t i = 0; i < h.peer.size(); ++i) {
+      sp.push_back(hs + h.soff[i] * w);
+      sc.push_back((size_t)(h.soff[i + 1] - h.soff[i]) * w);
+      rp.push_back(hr + h.roff[i] * w);
+      rc.push_back((size_t)(h.roff[i + 1] - h.roff[i]) * w);
+    }
+    if (C.h_sendrecv(C.h_user, (int)h.peer.size(), h.peer.data(), sp.data(), sc.data(), rp.data(), rc.data()) != 0)
+      throw Error{GEMSLR_ERR_NCCL, "host send/recv callback failed"};
+    CK(cudaMemcpyAsync(h.rbuf, hr, nr * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  } else {
+    C.check(C.gstart_(), "GroupStart");
+    for (size_t i = 0; i < h.peer.size(); ++i) {
+      const int64_t ns = h.soff[i + 1] - h.soff[i], nr = h.roff[i + 1] - h.roff[i];
+      if (ns > 0) C.check(C.send_(h.sbuf + h.soff[i], (size_t)ns * w, 8, h.peer[i], C.comm, ctx->stream), "Send");
+      if (nr > 0) C.check(C.recv_(h.rbuf + h.roff[i], (size_t)nr * w, 8, h.peer[i], C.comm, ctx->stream), "Recv");
+    }
+    C.check(C.gend_(), "GroupEnd");
   }
-  C.check(C.gend_(), "GroupEnd");
   C.exchanges++;
 }
 
@@ -1360,6 +1408,21 @@ gemslr_status gemslr_create_dist(gemslr_ctx **out, int cuda_device, void *cuda_s
       return (gemslr_status)e.code;
     }
   }
+  *out = c;
+  return GEMSLR_OK;
+}
+
+gemslr_status gemslr_create_hostcomm(gemslr_ctx **out, int cuda_device, void *cuda_stream, int nranks, int rank,
+                                     gemslr_allreduce_fn allreduce, gemslr_sendrecv_fn sendrecv, void *user) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !allreduce || !sendrecv) return GEMSLR_ERR_INVALID_ARG;
+  gemslr_ctx *c = nullptr;
+  gemslr_status st = create_common(out, cuda_device, cuda_stream, &c);
+  if (st) return st;
+  c->comm.nranks = nranks;
+  c->comm.rank = rank;
+  c->comm.h_allreduce = allreduce;
+  c->comm.h_sendrecv = sendrecv;
+  c->comm.h_user = user;
   *out = c;
   return GEMSLR_OK;
 }
