@@ -21,7 +21,7 @@
 
 namespace gemslr {
 
-constexpr int PIPE_SB_DEV = 16 * 1024;    // = PIPE_SB
+constexpr int PIPE_SB_DEV = 44 * 1024;    // = PIPE_SB
 constexpr int PIPE_NW_DEV = 8;            // = PIPE_NW
 
 // ----------------------------------------------------------------- scalars
@@ -298,7 +298,7 @@ __device__ inline void cp_async_arrive_noinc(unsigned long long *b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
-template <typename T> __host__ __device__ constexpr int pipe_stages() { return sizeof(T) == 8 ? 8 : 7; }
+template <typename T> __host__ __device__ constexpr int pipe_stages() { return 3; }
 template <typename T> __host__ __device__ constexpr size_t pipe_smem_bytes(int ring) {
   return (size_t)ring * sizeof(T) + (size_t)pipe_stages<T>() * (PIPE_SB_DEV + 32 * PIPE_NW_DEV * sizeof(T)) +
          (size_t)(2 * pipe_stages<T>() + 2) * 8;
@@ -422,6 +422,10 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
       fetch(k, cur);
     }
     if (dbg && b == 0 && tid == 0 && k < 4096) dbg[4 * k + 1] = clock64();
+    if (dbg && b == 0 && tid == 0 && k < 4096 && cur.row >= 0) {   // after the first column load
+      const int c0 = cur.cp[0];
+      dbg[5 * 4096 + k] = clock64() + (c0 == -7 ? 1 : 0);
+    }
     const bool upper = cur.flags & 1;
     if (cur.row >= 0) {
       T acc = cur.rhs;
@@ -439,17 +443,26 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
         // branch-free: padding has value 0 and column -1 (ring slot R-1, finite
         // because the ring is zero-initialised); two partial sums shorten the
         // dependent DFMA chain
-        T acc1 = dzero<T>();
+        // four partial sums: the dependent DFMA chain of a ~10-entry row is 3 deep
+        T a1 = dzero<T>(), a2 = dzero<T>(), a3 = dzero<T>();
         int e = 0;
-#pragma unroll 4
-        for (; e + 2 <= w; e += 2) {
-          const int ca = cp[32 * e], cb = cp[32 * (e + 1)];
-          const T va = vp[32 * e], vb = vp[32 * (e + 1)];
-          acc -= va * ring[ca & (R - 1)];
-          acc1 -= vb * ring[cb & (R - 1)];
+#pragma unroll 2
+        for (; e + 4 <= w; e += 4) {
+          const int c0 = cp[32 * e], c1 = cp[32 * (e + 1)], c2 = cp[32 * (e + 2)], c3 = cp[32 * (e + 3)];
+          const T v0 = vp[32 * e], v1 = vp[32 * (e + 1)], v2 = vp[32 * (e + 2)], v3 = vp[32 * (e + 3)];
+          acc -= v0 * ring[c0 & (R - 1)];
+          a1 -= v1 * ring[c1 & (R - 1)];
+          a2 -= v2 * ring[c2 & (R - 1)];
+          a3 -= v3 * ring[c3 & (R - 1)];
         }
-        if (e < w) acc -= vp[32 * e] * ring[cp[32 * e] & (R - 1)];
-        acc += acc1;
+        if (e < w) a1 -= vp[32 * e] * ring[cp[32 * e] & (R - 1)];
+        if (e + 1 < w) a2 -= vp[32 * (e + 1)] * ring[cp[32 * (e + 1)] & (R - 1)];
+        if (e + 2 < w) a3 -= vp[32 * (e + 2)] * ring[cp[32 * (e + 2)] & (R - 1)];
+        acc = (acc + a1) + (a2 + a3);
+      }
+      if (dbg && b == 0 && tid == 0 && k < 4096) {
+        const double probe = dabs2(acc);
+        dbg[4 * 4096 + k] = clock64() + (probe != probe ? 1 : 0);
       }
       if (upper) acc = acc * cur.dg;                              // diag holds 1 / u_ii
       else P.rhsU[cur.auxv] = acc;                                 // right-hand side of the U sweep

@@ -53,12 +53,8 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
       std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
       for (int64_t i = 0; i < n; ++i) rows[pos[lev[i]]++] = i;
     }
-    // inside a level (independent rows) sort by entry count, longest first, so
-    // the 32 rows of a SELL slice have similar widths (less padding)
     auto len = [&](int64_t i) { return M.ptr[i + 1] - M.ptr[i]; };
-    for (int32_t v = 0; v < nlev; ++v)
-      std::stable_sort(rows.begin() + cnt[v], rows.begin() + cnt[v + 1],
-                       [&](int64_t a, int64_t b) { return len(a) > len(b); });
+    (void)len;
     for (int32_t v = 0; v < nlev; ++v) {
       for (int64_t s0 = cnt[v]; s0 < cnt[v + 1]; s0 += 32) {
         const int64_t s1 = std::min<int64_t>(s0 + 32, cnt[v + 1]);
