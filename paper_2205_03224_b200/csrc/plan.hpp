@@ -100,8 +100,8 @@ struct ChunkDesc {                          // 16 bytes, one vector load in the 
   int32_t nsflags;                          // ns << 1 | (1 if U sweep)
 };
 constexpr int PIPE_NW = 8;                  // consumer warps per CTA = max slices per chunk
-constexpr int PIPE_SB = 44 * 1024;          // blob bytes per pipeline stage
-constexpr int PIPE_RING_BYTES = 64 * 1024;  // solution window
+constexpr int PIPE_SB = 30 * 1024;          // blob bytes per pipeline stage
+constexpr int PIPE_RING_ENTRIES = 16384;     // solution window (double; 8192 for complex)
 
 template <typename T>
 struct PipePack {

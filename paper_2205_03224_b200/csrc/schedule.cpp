@@ -96,7 +96,7 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
 template <typename T>
 void pack_pipe(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPack<T> &Up, PipePack<T> &P) {
   P = PipePack<T>();
-  P.ring = PIPE_RING_BYTES / (int)sizeof(T);
+  P.ring = sizeof(T) == 8 ? PIPE_RING_ENTRIES : PIPE_RING_ENTRIES / 2;
   const int R = P.ring;
   const size_t nb = blk.size() - 1;
   const int64_t R0 = blk.front(), NR = blk.back() - blk.front();
