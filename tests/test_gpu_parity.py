@@ -170,3 +170,80 @@ def test_cluster_sizes_agree(tmp_path, cps):
     s, B, st, Pc = make_pair(prob, prm, tmp_path, cluster_ctas=cps)
     r = P.rhs_vector(prob.n, False, 2)
     assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
+
+
+# ---------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("kind", ["tiny1d", "p1", "fullrank", "early_stop", "random_bfs", "complex_bfs"])
+def test_edge_cases(tmp_path, kind):
+    import scipy.sparse as sp
+    if kind == "tiny1d":               # 1D chain: ILU(0) is exact LU, separators are points
+        n = 40
+        A = sp.diags([-1.0 * np.ones(n - 1), 2.5 * np.ones(n), -1.2 * np.ones(n - 1)], [-1, 0, 1], format="csr")
+        prob = P.Problem("1d", (n,), A.indptr.astype(np.int64), A.indices.astype(np.int32), A.data,
+                         np.stack([np.arange(n), np.zeros(n), np.zeros(n)], 1).astype(float))
+        prm = dict(levels=2, subdomains=2, rank=2, ilu="ilu0")
+    elif kind == "p1":                 # one subdomain per level
+        prob = P.laplacian((9, 8, 7))
+        prm = dict(levels=2, subdomains=1, rank=3, ilu="ilut")
+    elif kind == "fullrank":           # rank >= separator size
+        prob = P.convdiff_upwind((10, 10))
+        prm = dict(levels=1, subdomains=4, rank=40, ilu="ilu0")
+    elif kind == "early_stop":         # more levels requested than the separators allow
+        prob = P.laplacian((12, 12))
+        prm = dict(levels=6, subdomains=4, rank=4, ilu="ilut")
+    elif kind == "random_bfs":         # unstructured nonsymmetric pattern, BFS partitioner
+        r = np.random.default_rng(3)
+        n = 600
+        M = sp.random(n, n, density=6.0 / n, random_state=4, format="csr")
+        M = M + M.T.multiply(r.uniform(0.5, 1.5, (n, n)) > 1.2) + sp.identity(n) * 8.0
+        M = sp.csr_matrix(M)
+        M.sort_indices()
+        prob = P.Problem("rnd", (n,), M.indptr.astype(np.int64), M.indices.astype(np.int32), M.data,
+                         np.zeros((n, 3)))
+        prm = dict(levels=2, subdomains=4, rank=4, ilu="ilut")
+    else:                              # complex without coordinates
+        prob = P.helmholtz_shifted((8, 7, 6))
+        prm = dict(levels=2, subdomains=4, rank=5, ilu="ilut")
+    prm.update(ilut_drop=1e-3, ilut_fill=10)
+    coords = kind not in ("random_bfs", "complex_bfs")
+    s, B, st, Pc = make_pair(prob, prm, tmp_path, coords=coords)
+    n = prob.n
+    x = P.rhs_vector(n, prob.is_complex, 2)
+    assert rel(s.apply_precond(to_dev(s, x)).cpu().numpy(), Pc.apply(x)) <= TOL
+    y = s.spmv(to_dev(s, x[st["perm"]])).cpu().numpy()
+    yn = np.empty_like(y)
+    yn[st["perm"]] = y
+    assert rel(yn, oracle.spmv(prob, x)) <= TOL
+    b = P.rhs_vector(n, prob.is_complex, 9)
+    out = s.solve(to_dev(s, b[st["perm"]]), rtol=1e-8, restart=20, maxit=400)
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=1e-8, restart=20, maxit=400)
+    assert abs(out["its"] - ref["its"]) <= 1 and out["status"] == ref["status"] == 0
+
+
+def test_zero_rhs_and_maxit(tmp_path):
+    prob, b, xt, prm = P.make_config("C2", dims=(10, 10, 10), subdomains=4, rank=3)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    out = s.solve(to_dev(s, np.zeros(prob.n)), rtol=1e-8, restart=10)
+    assert out["its"] == 0 and out["status"] == 0 and torch.count_nonzero(out["x"]) == 0
+    out = s.solve(to_dev(s, b[st["perm"]]), rtol=1e-14, restart=5, maxit=7)
+    assert out["its"] == 7 and out["status"] == 1            # NOT_CONVERGED
+    assert len(out["hist"]) == 8
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C2", "C5"])
+def test_full_size_parity(tmp_path, name):
+    """BASELINE sizes (64^3 / 128^3), the configuration bench.py times: full-vector
+    SpMV and apply parity, and the first FGMRES iterations' residual estimates."""
+    prob, b, xt, prm = P.make_config(name)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    perm = st["perm"]
+    x = P.rhs_vector(prob.n, False, 13)
+    y = s.spmv(to_dev(s, x[perm])).cpu().numpy()
+    yo = oracle.spmv(prob, x)[perm]
+    assert rel(y, yo) <= TOL
+    yg = s.apply_precond(to_dev(s, x)).cpu().numpy()
+    assert rel(yg, Pc.apply(x)) <= TOL
+    out = s.solve(to_dev(s, b[perm]), rtol=1e-300, restart=prm["restart"], maxit=8)
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=8)
+    assert np.allclose(out["hist"], ref["hist"], rtol=1e-7, atol=0)
