@@ -67,6 +67,8 @@ typedef struct {
   int arnoldi_max_cycles;   /* thick-restart cycles (cycle length m = 2k); 0 = 10                   */
   unsigned long long seed;  /* Arnoldi start vector seed                                                    */
   int cluster_ctas;         /* CTAs per thread-block cluster in the triangular solves; 0 = automatic        */
+  int tri_kernel;           /* triangular-solve kernel: 0 = automatic (register-prefetched k_tri_reg where
+                               the setup proves it applies), 1 = TMA-staged k_tri_pipe, 2 = level kernel     */
 } gemslr_params;
 
 typedef struct gemslr_ctx gemslr_ctx;

@@ -31,6 +31,7 @@ namespace gemslr {
 
 static constexpr int kNumSM = 148;
 long long *g_tri_dbg = nullptr;   // debug: per-chunk clock64 trace of block 0 (gemslr_debug_trace)
+int g_tri_dbg_level = 0;          // level whose down launch is traced
 static_assert(PIPE_SB == PIPE_SB_DEV && PIPE_NW == PIPE_NW_DEV, "pipeline constants");
 
 #define CK(x)                                                                          \
@@ -95,11 +96,12 @@ static const char *kKernelName[KC_COUNT] = {"spmv", "trisolve_down", "trisolve_u
 
 struct Profiler {
   bool on = false;
-  struct Rec { int kc; cudaEvent_t a, b; };
+  struct Rec { int kc, sub; cudaEvent_t a, b; };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> freelist;
   double ms[KC_COUNT] = {0};
   long long count[KC_COUNT] = {0};
+  double sub_ms[KC_COUNT][4] = {{0}};         // per level (trisolve classes)
   cudaEvent_t ev() {
     if (!freelist.empty()) { cudaEvent_t e = freelist.back(); freelist.pop_back(); return e; }
     cudaEvent_t e;
@@ -113,6 +115,7 @@ struct Profiler {
       cudaEventElapsedTime(&t, r.a, r.b);
       ms[r.kc] += t;
       count[r.kc] += 1;
+      sub_ms[r.kc][std::min(r.sub, 3)] += t;
       freelist.push_back(r.a);
       freelist.push_back(r.b);
     }
@@ -120,7 +123,11 @@ struct Profiler {
   }
   void reset() {
     flush();
-    for (int i = 0; i < KC_COUNT; ++i) { ms[i] = 0; count[i] = 0; }
+    for (int i = 0; i < KC_COUNT; ++i) {
+      ms[i] = 0;
+      count[i] = 0;
+      for (int q = 0; q < 4; ++q) sub_ms[i][q] = 0;
+    }
   }
   ~Profiler() {
     for (auto &r : pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -131,16 +138,16 @@ struct Profiler {
 struct Timed {                                  // RAII event pair around one launch
   Profiler &P;
   cudaStream_t s;
-  int kc;
+  int kc, sub;
   cudaEvent_t a = nullptr;
-  Timed(Profiler &p, cudaStream_t st, int k) : P(p), s(st), kc(k) {
+  Timed(Profiler &p, cudaStream_t st, int k, int sb = 0) : P(p), s(st), kc(k), sub(sb) {
     if (P.on) { a = P.ev(); cudaEventRecord(a, s); }
   }
   ~Timed() {
     if (P.on) {
       cudaEvent_t b = P.ev();
       cudaEventRecord(b, s);
-      P.pending.push_back({kc, a, b});
+      P.pending.push_back({kc, sub, a, b});
       if (P.pending.size() > 4096) P.flush();
     }
   }
@@ -266,6 +273,10 @@ struct StageDev {
   int depthL = 0, depthU = 0;
   bool pipe = false;       // TMA-pipelined kernel (k_tri_pipe) instead of the level kernel
   PipeDev<D> P{};
+  bool reg = false;        // register-prefetched kernel (k_tri_reg), preferred when available
+  int reg_w = 0;           // record width W (4, 8, 10, 12 or 16)
+  RegDev<D> Rg{};
+  int64_t reg_bytes = 0;   // record bytes of both sweeps
   int64_t nchunks = 0, far = 0, nearc = 0;
   int64_t nnz = 0;         // real stored nonzeros (L + U incl. diagonal)
   int64_t padded = 0;      // stored entries incl. padding
@@ -373,7 +384,7 @@ struct Ctx {
 
 // ----------------------------------------------------------------- upload
 template <typename D, typename T>
-static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int cps_override) {
+static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int cps_override, int tri_kernel) {
   StageDev<D> d;
   d.nblk = (int)S.blk.size() - 1;
   d.rows = S.blk.empty() ? 0 : S.blk.back() - S.blk.front();
@@ -394,7 +405,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
   d.U = up(S.Up);
   d.depthL = S.Lp.max_depth;
   d.depthU = S.Up.max_depth;
-  if (S.pipe.ok && cps_override <= 0 && d.nblk > 0 && pipe_smem_bytes<D>(S.pipe.ring) <= 232448) {
+  if (S.pipe.ok && cps_override <= 0 && tri_kernel != 2 && d.nblk > 0 && pipe_smem_bytes<D>(S.pipe.ring) <= 232448) {
     static_assert(sizeof(ChunkDesc) == sizeof(ChunkDev), "chunk descriptor layout");
     d.pipe = true;
     d.P.blob = P.upload<unsigned char>(S.pipe.blob, s);
@@ -409,6 +420,23 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     d.nchunks = (int64_t)S.pipe.chunks.size();
     d.far = S.pipe.far;
     d.nearc = S.pipe.near;
+  }
+  if (S.reg.ok && cps_override <= 0 && tri_kernel == 0 && d.nblk > 0 &&
+      reg_smem_bytes<D>(S.reg.ring, S.reg.max_block_slices) <= 232448) {
+    static_assert(REG_BINFO == REG_BINFO_INTS, "binfo layout");
+    d.reg = true;
+    d.reg_w = S.reg.W;
+    d.Rg.data = P.upload<unsigned char>(S.reg.data, s);
+    d.Rg.slev = P.upload<unsigned short>(S.reg.slev, s);
+    d.Rg.max_slices = S.reg.max_block_slices;
+    d.Rg.rec_bytes = (long long)S.reg.rec_bytes;
+    d.Rg.binfo = P.upload<int>(S.reg.binfo, s);
+    d.Rg.lev_off = P.upload<int>(S.reg.lev_off, s);
+    d.Rg.rhsL = P.get<D>(std::max<int64_t>(S.reg.lslices * 32, 1));
+    d.Rg.mid = P.get<D>(std::max<int64_t>(S.reg.uslices * 32, 1));
+    d.Rg.ring = S.reg.ring;
+    d.reg_bytes = (int64_t)S.reg.data.size();
+    if (!d.pipe) d.P.lpos = P.upload<int>(S.reg.lpos, s);
   }
   d.nnz = S.Lp.nnz_real + S.Up.nnz_real + (int64_t)d.rows;
   d.padded = (int64_t)S.Lp.val.size() + (int64_t)S.Up.val.size() + (int64_t)S.Up.diag.size();
@@ -496,14 +524,14 @@ void Engine<T>::upload(cudaStream_t s) {
     d.o0 = plan.lo[l];
     d.o1 = plan.lo[l + 1];
     d.s = n - d.o1;
-    d.st = upload_stage<D>(P, s, plan.stage[l], ctx->params.cluster_ctas);
+    d.st = upload_stage<D>(P, s, plan.stage[l], ctx->params.cluster_ctas, ctx->params.tri_kernel);
     d.E = upload_csr<D>(P, s, plan.E[l]);
     d.F = upload_csr<D>(P, s, plan.F[l]);
     hE[l] = upload_halo<D>(P, s, plan.hE[l]);
     hF[l] = upload_halo<D>(P, s, plan.hF[l]);
   }
   hA = upload_halo<D>(P, s, plan.hA);
-  last = upload_stage<D>(P, s, plan.last_stage, ctx->params.cluster_ctas);
+  last = upload_stage<D>(P, s, plan.last_stage, ctx->params.cluster_ctas, ctx->params.tri_kernel);
   if (plan.nranks > 1) {
     rl_full = P.get<D>(plan.slast + 1);
     yl_full = P.get<D>(plan.slast + 1);
@@ -586,7 +614,7 @@ struct FArgs {
 
 template <typename D>
 static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *rhs, D *x, D *tmp,
-                            const FArgs<D> &fa, const int *doneflag, int kc) {
+                            const FArgs<D> &fa, const int *doneflag, int kc, int lvl = 0) {
   if (S.nblk <= 0 || S.rows == 0) return;
   const CsrDev<D> *F = fa.F;
   const int64_t Fbase = fa.Fbase;
@@ -594,6 +622,41 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
   const int32_t *Fc = F ? F->col : nullptr;
   const D *Fv = F ? F->val : nullptr;
   const int pgrid = grid_for((S.rows + 255) / 256, 4);
+  if (S.reg) {
+    constexpr int NW = sizeof(D) == 8 ? 15 : 7;   // (NW + 1) warps a multiple of 4: full register budget
+    const size_t smem = reg_smem_bytes<D>(S.Rg.ring, S.Rg.max_slices);
+    {
+      Timed tp(ctx->prof, ctx->stream, KC_PACK);
+      k_pack_rhs<D><<<pgrid, 256, 0, ctx->stream>>>(S.rows, S.row0, S.P.lpos, const_cast<D *>(S.Rg.rhsL),
+                                                    mode == TRI_DOWN ? rhs : nullptr, Fp, Fc, Fv, Fbase, x, fa.nloc,
+                                                    fa.yh, fa.nh, fa.yl, doneflag);
+    }
+    Timed t(ctx->prof, ctx->stream, kc, lvl);
+    static bool attr = false;
+    if (!attr) {
+      const int smax = 232448;
+      CK(cudaFuncSetAttribute(k_tri_reg<D, 4, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+      CK(cudaFuncSetAttribute(k_tri_reg<D, 8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+      CK(cudaFuncSetAttribute(k_tri_reg<D, 10, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+      CK(cudaFuncSetAttribute(k_tri_reg<D, 12, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+      CK(cudaFuncSetAttribute(k_tri_reg<D, 16, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+      attr = true;
+    }
+    RegDev<D> Rg = S.Rg;
+    Rg.dbg = (kc == KC_TRI_DOWN && lvl == g_tri_dbg_level) ? g_tri_dbg : nullptr;
+    static const int reg_flags = getenv("GEMSLR_REG_FLAGS") ? atoi(getenv("GEMSLR_REG_FLAGS")) : 0;
+    Rg.flags = reg_flags;
+    auto go = [&](auto kern) { kern<<<S.nblk, 32 * (NW + 1), smem, ctx->stream>>>(Rg, mode, x, tmp, doneflag); };
+    switch (S.reg_w) {
+      case 4: go(k_tri_reg<D, 4, NW>); break;
+      case 8: go(k_tri_reg<D, 8, NW>); break;
+      case 10: go(k_tri_reg<D, 10, NW>); break;
+      case 12: go(k_tri_reg<D, 12, NW>); break;
+      default: go(k_tri_reg<D, 16, NW>); break;
+    }
+    CK(cudaGetLastError());
+    return;
+  }
   if (S.pipe) {
     const size_t smem = pipe_smem_bytes<D>(S.P.ring);
     static bool attr_set = false;
@@ -607,7 +670,7 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
       k_pack_rhs<D><<<pgrid, 256, 0, ctx->stream>>>(S.rows, S.row0, S.P.lpos, S.P.rhsL, mode == TRI_DOWN ? rhs : nullptr,
                                                     Fp, Fc, Fv, Fbase, x, fa.nloc, fa.yh, fa.nh, fa.yl, doneflag);
     }
-    Timed t(ctx->prof, ctx->stream, kc);
+    Timed t(ctx->prof, ctx->stream, kc, lvl);
     long long *dbg = kc == KC_TRI_DOWN ? g_tri_dbg : nullptr;
     if (S.far > 0)
       k_tri_pipe<D, true><<<S.nblk, 32 * (PIPE_NW_DEV + 1), smem, ctx->stream>>>(S.P, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag, dbg);
@@ -623,7 +686,7 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
                                                   fa.yh, fa.nh, fa.yl, doneflag);
     Fp = nullptr;
   }
-  Timed t(ctx->prof, ctx->stream, kc);
+  Timed t(ctx->prof, ctx->stream, kc, lvl);
   if (S.cps <= 1) {
     k_trisolve<D, false><<<S.nblk, 256, 0, ctx->stream>>>(S.L, S.U, S.blk, mode, rhs, x, tmp, Fp, Fc, Fv, Fbase, doneflag);
   } else {
@@ -669,7 +732,7 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     LevelDev<D> &d = lev[l];
     const D *src = (l == l0) ? in : r;
     // z1 = U_l^-1 L_l^-1 b1  -> out[I_l]
-    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN);
+    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, l);
     if (d.s > 0 || dist) {
       exchange(hE[l], out, doneflag);                              // z1 entries of E_l's exterior columns
       // z2 = b2 - E_l z1 ; this rank's part of s = W^H z2
@@ -717,7 +780,7 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     fa.yh = hF[l].rbuf;
     fa.nh = hF[l].nrecv;
     fa.yl = yl_full;
-    launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP);
+    launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP, l);
   }
 }
 
@@ -1275,7 +1338,9 @@ std::string Engine<T>::stats_json() const {
            std::to_string(S.cps) + ", \"depth_L\": " + std::to_string(S.depthL) + ", \"depth_U\": " +
            std::to_string(S.depthU) + ", \"nnz\": " + std::to_string(S.nnz) + ", \"padded\": " + std::to_string(S.padded) +
            ", \"pipe\": " + (S.pipe ? "true" : "false") + ", \"chunks\": " + std::to_string(S.nchunks) +
-           ", \"far\": " + std::to_string(S.far) + ", \"near\": " + std::to_string(S.nearc) + "}";
+           ", \"far\": " + std::to_string(S.far) + ", \"near\": " + std::to_string(S.nearc) +
+           ", \"kernel\": \"" + (S.reg ? "reg" : S.pipe ? "pipe" : "level") + "\", \"reg_w\": " + std::to_string(S.reg_w) +
+           ", \"reg_bytes\": " + std::to_string(S.reg_bytes) + "}";
   };
   j += ", \"stages\": [";
   for (size_t l = 0; l < lev.size(); ++l) {
@@ -1303,7 +1368,9 @@ std::string Engine<T>::stats_json() const {
     if (!first) j += ", ";
     first = false;
     j += "\"" + std::string(kKernelName[k]) + "\": {\"ms\": " + std::to_string(ctx->prof.ms[k]) + ", \"count\": " +
-         std::to_string(ctx->prof.count[k]) + "}";
+         std::to_string(ctx->prof.count[k]) + ", \"by_level\": [" + std::to_string(ctx->prof.sub_ms[k][0]) + ", " +
+         std::to_string(ctx->prof.sub_ms[k][1]) + ", " + std::to_string(ctx->prof.sub_ms[k][2]) + ", " +
+         std::to_string(ctx->prof.sub_ms[k][3]) + "]}";
   }
   j += "}}";
   return j;
@@ -1674,6 +1741,7 @@ gemslr_status gemslr_stats(const gemslr_ctx *c, char *json, size_t cap) {
 // Debug hook (not in gemslr.h): record a clock64 trace of block 0 of the down-sweep
 // trisolve launches into a device buffer of 4 * 4096 int64.
 extern "C" void gemslr_debug_trace(void *dev_buf) { g_tri_dbg = static_cast<long long *>(dev_buf); }
+extern "C" void gemslr_debug_trace_level(int level) { g_tri_dbg_level = level; }
 
 gemslr_status gemslr_profile(gemslr_ctx *c, int enable, int reset) {
   if (!c) return GEMSLR_ERR_INVALID_ARG;

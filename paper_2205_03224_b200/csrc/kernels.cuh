@@ -503,6 +503,195 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
     for (int64_t i = r0 + tid; i < r1; i += NCONS) x[i] = x[i] - tmp[i];   // y1 = z1 - U^-1 L^-1 F y2
 }
 
+// ----------------------------------------------------------------- K4/K5/K9 register-prefetched
+// One CTA per block, NW consumer warps + one L2-prefetch warp.  The slices of a
+// sweep (level order) go round-robin to the consumer warps: slice s -> warp
+// s mod NW, so a warp's next slice is NW slices on and its record (values,
+// 16-bit ring slots, output position, 1/u_ii) is loaded straight into registers
+// two slices ahead — no shared-memory staging of the factor stream, whose
+// 128 B/clk port was the floor of k_tri_pipe.  Levels are separated by one
+// named barrier among the consumer warps; a dependency is a shared-memory load
+// from the ring of the last `ring` solution values (the setup proves every
+// dependency is still in the window, RegPack::far == 0).  The helper warp keeps
+// the records of the next REG_L2_AHEAD levels in L2 (cp.async.bulk.prefetch.L2),
+// paced by the level counter the consumers publish.
+// DOWN: x[rows] = U^-1 L^-1 rhs (rhsL = rhs packed in L order by k_pack_rhs)
+// UP:   x[rows] -= U^-1 L^-1 (F_l y_J) (rhsL = F_l y_J packed by k_pack_rhs)
+// The L results go to `mid` at their packed U position: the U sweep's right-hand
+// sides, read after the sweep-transition barrier.
+template <typename T>
+struct RegDev {
+  const unsigned char *data;   // fixed-size records (RegPack)
+  const unsigned short *slev;  // level of every record in its sweep
+  long long rec_bytes;
+  const int *binfo;
+  const int *lev_off;
+  const T *rhsL;
+  T *mid;
+  int ring;
+  long long *dbg;          // debug trace (block 0): 8 words per slice, 2048 slices per sweep
+  int flags;               // bit 0: no L2 prefetch helper (experiments)
+  int max_slices;          // L + U records of the largest block (shared-memory level table)
+};
+constexpr int REG_L2_AHEAD = 12;
+template <typename T> __host__ __device__ inline size_t reg_smem_bytes(int ring, int max_slices) {
+  return (size_t)ring * sizeof(T) + 16 + (((size_t)max_slices * 2 + 15) & ~(size_t)15);
+}
+constexpr int REG_BINFO = 12;            // ints per block in RegDev::binfo (= REG_BINFO_INTS)
+
+__device__ inline void prefetch_l2_bulk(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// Level v of a sweep ends at named barrier 1 + v % 15 (15 ids in rotation).
+// A warp that computes in level v + 1 SYNCS there (arrive + wait); every other
+// warp only ARRIVES (bar.arrive, no wait) — right after its last slice of level
+// v, so its prefetch loads and global stores overlap the following levels.  A warp can
+// run at most NW - 1 levels ahead of the slowest (its next slice is NW slices
+// on), so with NW <= 15 no barrier id is reused before its instance completes.
+template <int NW> __device__ inline void reg_arrive(int v) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(1 + v % 15), "n"(32 * NW) : "memory");
+}
+template <int NW> __device__ inline void reg_sync(int v) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + v % 15), "n"(32 * NW) : "memory");
+}
+template <int NW> __device__ inline void reg_sync_all() { asm volatile("bar.sync 0, %0;" ::"n"(32 * NW) : "memory"); }
+
+template <typename T, int W>
+struct RegBuf {
+  static constexpr int W4 = (W + 3) / 4;
+  T v[W];
+  unsigned long long c[W4];
+  T rhs, dg;
+  int out;
+};
+
+template <typename T, int W, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
+                                                            const int *__restrict__ done) {
+  if (done && *done) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  T *ring = reinterpret_cast<T *>(smem);
+  volatile int *prog = reinterpret_cast<volatile int *>(smem + (size_t)P.ring * sizeof(T));
+  unsigned short *lvt = reinterpret_cast<unsigned short *>(smem + (size_t)P.ring * sizeof(T) + 16);
+  const int R = P.ring;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int *bi = P.binfo + REG_BINFO * blockIdx.x;
+  {                                                                // level table of the block's records (L then U)
+    const int f = bi[0], nl = bi[1] + bi[4];                       // U records follow the L records of the block
+    for (int i = tid; i < nl; i += blockDim.x) lvt[i] = P.slev[f + i];
+  }
+  for (int i = tid; i < R; i += blockDim.x) ring[i] = dzero<T>();
+  if (tid == 0) *prog = 0;
+  __syncthreads();
+  const size_t RB = (size_t)P.rec_bytes;
+  if (warp == NW) {                                                // ---- L2 prefetch helper (one lane)
+    if (lane != 0 || (P.flags & 1)) return;
+    int passed = 0;                                                // levels issued over both sweeps
+    for (int sw = 0; sw < 2; ++sw) {
+      const int nlev = bi[3 * sw + 2];
+      const int *lo = P.lev_off + bi[6 + sw];
+      for (int v = 0; v < nlev; ++v, ++passed) {
+        while (passed > *prog + REG_L2_AHEAD) __nanosleep(200);
+        const long long a = (long long)lo[v] * (long long)RB, e = (long long)lo[v + 1] * (long long)RB;
+        for (long long q = a; q < e; q += 65536) prefetch_l2_bulk(P.data + q, (unsigned)min(65536LL, e - q));
+      }
+    }
+    return;
+  }
+  static_assert(NW <= 15, "barrier ids rotate over 15 named barriers");
+  using Buf = RegBuf<T, W>;
+  constexpr int W4 = Buf::W4;
+  int base_lev = 0;                                                // levels of earlier sweeps (for prog)
+#pragma unroll 1
+  for (int sw = 0; sw < 2; ++sw) {
+    const bool upper = sw == 1;
+    const int r0 = bi[3 * sw], ns = bi[3 * sw + 1], nlev = bi[3 * sw + 2], gbase = bi[10 + sw];
+    const int lvbase = upper ? bi[1] : 0;
+    // Issues the loads of slice s; every address is arithmetic on s, so the
+    // warp never waits here and reaches the next barrier right after its slice.
+    auto load = [&](Buf &B, int s) {
+      if (s >= ns) return;
+      const unsigned char *rec = P.data + (size_t)(r0 + s) * RB;
+      const T *vp = reinterpret_cast<const T *>(rec) + lane;
+      const unsigned long long *cp = reinterpret_cast<const unsigned long long *>(rec + (size_t)W * 32 * sizeof(T)) + lane;
+      const int *op = reinterpret_cast<const int *>(cp + (W4 - 1) * 32 + (32 - lane));   // record's out[]
+#pragma unroll
+      for (int e = 0; e < W; ++e) B.v[e] = ld_nc(vp + 32 * e);
+#pragma unroll
+      for (int j = 0; j < W4; ++j) B.c[j] = __ldg(cp + 32 * j);
+      B.out = __ldg(op + lane);
+      const size_t ri = (size_t)(gbase + s) * 32 + lane;
+      if (upper) {
+        B.dg = ld_nc(reinterpret_cast<const T *>(op + 32) + lane);
+        B.rhs = ld_cg(P.mid + ri);                                 // written by this CTA's L sweep
+      } else {
+        B.rhs = ld_nc(P.rhsL + ri);
+      }
+    };
+    int cur = 0;
+    auto compute = [&](const Buf &B, int s) {
+      const bool tr = P.dbg && blockIdx.x == 0 && lane == 0 && s < 2048;
+      long long *tp = tr ? P.dbg + 8 * (sw * 2048 + s) : nullptr;
+      if (tr) { tp[0] = clock64(); tp[7] = warp; }
+      const int lv = lvt[lvbase + s];
+      for (; cur < lv - 1; ++cur) reg_arrive<NW>(cur);             // levels with no slice of this warp
+      if (cur < lv) {                                               // wait for level lv - 1 to complete
+        reg_sync<NW>(cur);
+        ++cur;
+        if (warp == 0 && lane == 0) *prog = base_lev + cur;
+      }
+      if (tr) { const int pv = *prog; tp[2] = clock64() + (pv == -7 ? 1 : 0); tp[6] = lv; }
+      T acc = B.rhs, a1 = dzero<T>(), a2 = dzero<T>(), a3 = dzero<T>();
+#pragma unroll
+      for (int j = 0; j < W4; ++j) {
+        const unsigned long long c = B.c[j];
+        const int e = 4 * j;
+        acc -= B.v[e] * ring[(unsigned)(c & 0xffff)];
+        if (e + 1 < W) a1 -= B.v[e + 1 < W ? e + 1 : 0] * ring[(unsigned)((c >> 16) & 0xffff)];
+        if (e + 2 < W) a2 -= B.v[e + 2 < W ? e + 2 : 0] * ring[(unsigned)((c >> 32) & 0xffff)];
+        if (e + 3 < W) a3 -= B.v[e + 3 < W ? e + 3 : 0] * ring[(unsigned)(c >> 48)];
+      }
+      acc = (acc + a1) + (a2 + a3);
+      if (tr) { const double pr = dabs2(acc); tp[1] = clock64() + (pr != pr ? 1 : 0); }
+      if (upper) acc = acc * B.dg;
+      if (B.out >= 0) {
+        ring[(s * 32 + lane) & (R - 1)] = acc;
+        if (!upper) P.mid[B.out] = acc;
+        else if (mode == TRI_UP) tmp[B.out] = acc;                 // x -= tmp after the sweep
+        else x[B.out] = acc;
+      }
+      // done with level lv: signal without waiting, unless this warp's next
+      // slice is in level lv + 1 (then its next compute syncs at barrier lv)
+      if (s + NW >= ns || lvt[lvbase + s + NW] > lv + 1) {
+        reg_arrive<NW>(lv);
+        cur = lv + 1;
+      }
+      if (tr) tp[3] = clock64();
+    };
+    // slices s (buffer A) and s + NW (B) in registers
+    int s = warp;
+    Buf A, B;
+    load(A, s);
+    load(B, s + NW);
+    while (s < ns) {
+      compute(A, s);
+      load(A, s + 2 * NW);
+      s += NW;
+      if (s >= ns) break;
+      compute(B, s);
+      load(B, s + 2 * NW);
+      s += NW;
+    }
+    for (; cur < nlev; ++cur) reg_arrive<NW>(cur);
+    base_lev += nlev;
+    __threadfence_block();
+    reg_sync_all<NW>();                                            // sweep transition: mid / tmp visible, ring free
+    if (warp == 0 && lane == 0) *prog = base_lev;
+  }
+  if (mode == TRI_UP)                                              // y1 = z1 - U^-1 L^-1 F y2 (Alg. 2 l.9)
+    for (int i = bi[8] + tid; i < bi[9]; i += 32 * NW) x[i] = x[i] - ld_cg(tmp + i);
+}
+
 // Packs the L-sweep right-hand sides of a stage in chunk order:
 // DOWN: dst[lpos[i]] = src[row0 + i];  UP: dst[lpos[i]] = (F_l y_J)_{row0 + i},
 // with F_l's columns local (< nloc), in the halo yh (< nloc + nh) or in the

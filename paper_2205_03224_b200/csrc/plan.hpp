@@ -116,11 +116,58 @@ struct PipePack {
   int64_t near = 0, far = 0;
 };
 
+// Register-prefetched form of a stage's two sweeps (k_tri_reg).  Per block and
+// sweep the slices are numbered in level order; slice s goes to consumer warp
+// s mod NW, which loads its record straight into registers two slices ahead.
+// Records have ONE size per stage (W = reg_width(widest slice) entries), so a
+// record's address is plain arithmetic on the slice index — no loaded header
+// feeds an address (a loaded address would make the warp wait on the load
+// before it reaches the next level barrier).  Record of a slice, 128-byte
+// aligned, for lane r:
+//   T val[W][32] (0 on padding); uint64 col[ceil(W/4)][32]: four 16-bit ring
+//   slots (padding -> slot ring-1); int32 out[32]; T rdiag[32] = 1/u_ii (U
+//   sweep; 1 in the L sweep).  The level of every record (uint16 `slev`, in the
+//   sweep) is copied to shared memory at kernel start: the barrier count of a
+//   warp never waits on a global load.
+// out: L sweep -> stage-global packed U position (where the U sweep reads its
+// right-hand side), U sweep -> the row; -1 = padding lane.
+// binfo per block (REG_BINFO ints): L first record, L slices, L levels, U first
+// record, U slices, U levels, first lev_off entry of L, of U, first row, end
+// row, stage-global packed L slice of the block's first L slice (right-hand
+// sides rhsL[(base + s) * 32 + lane]), same for U (mid).
+// lev_off: per block and sweep, the first record of every level and the end.
+constexpr int REG_RING_BYTES = 128 * 1024;     // solution window: 16384 doubles / 8192 complex
+constexpr int REG_BINFO_INTS = 12;
+inline int reg_width(int w) { return w <= 4 ? 4 : w <= 8 ? 8 : w <= 10 ? 10 : w <= 12 ? 12 : w <= 16 ? 16 : 0; }
+template <typename T>
+inline size_t reg_record_bytes(int W) {
+  const size_t b = (size_t)W * 32 * sizeof(T) + (size_t)((W + 3) / 4) * 32 * 8 + 32 * 4 + 32 * sizeof(T);
+  return (b + 127) / 128 * 128;
+}
+template <typename T>
+struct RegPack {
+  bool ok = false;
+  int ring = 0;
+  int wmax = 0;                                 // widest slice of the stage
+  int W = 0;                                    // record width (reg_width(wmax))
+  size_t rec_bytes = 0;
+  std::vector<uint8_t> data;
+  std::vector<uint16_t> slev;                   // per record: level in its sweep
+  int max_block_slices = 0;                     // L + U records of the largest block
+  std::vector<int32_t> binfo;                   // REG_BINFO_INTS per block
+  std::vector<int32_t> lev_off;
+  std::vector<int32_t> lpos;                    // per stage row: packed L index
+  int64_t lslices = 0, uslices = 0, nrec = 0;
+  int64_t near = 0, far = 0;
+  int max_levels = 0;
+};
+
 template <typename T>
 struct Stage {                                  // the blocks of one level (or of C_last)
   std::vector<int64_t> blk;                     // absolute boundaries (empty blocks removed)
   TriPack<T> Lp, Up;
   PipePack<T> pipe;
+  RegPack<T> reg;
 };
 
 // Neighbour exchange of one distributed operator: this rank

@@ -206,6 +206,100 @@ void pack_pipe(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriP
   P.ok = true;
 }
 
+// Register-prefetched records of the two sweeps (RegPack, k_tri_reg).
+template <typename T>
+void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPack<T> &Up, RegPack<T> &P) {
+  P = RegPack<T>();
+  P.ring = REG_RING_BYTES / (int)sizeof(T);
+  const int R = P.ring;
+  const size_t nb = blk.size() - 1;
+  const int64_t R0 = blk.front(), NR = blk.back() - blk.front();
+  P.lslices = (int64_t)Lp.slice_row.size() / 32;
+  P.uslices = (int64_t)Up.slice_row.size() / 32;
+  for (const TriPack<T> *S : {&Lp, &Up})
+    for (size_t s = 0; s + 1 < S->slice_off.size(); ++s)
+      P.wmax = std::max(P.wmax, (int)((S->slice_off[s + 1] - S->slice_off[s]) / 32));
+  P.W = reg_width(std::max(P.wmax, 1));
+  if (P.W == 0) return;
+  const int W = P.W, W4 = (W + 3) / 4;
+  P.rec_bytes = reg_record_bytes<T>(W);
+  P.nrec = P.lslices + P.uslices;
+  P.data.assign((size_t)P.nrec * P.rec_bytes, 0);
+  std::vector<int32_t> upos(NR, -1);
+  P.lpos.assign(NR, -1);
+  for (int64_t s = 0; s < P.lslices; ++s)
+    for (int lane = 0; lane < 32; ++lane) {
+      const int32_t row = Lp.slice_row[s * 32 + lane];
+      if (row >= 0) P.lpos[row - R0] = (int32_t)(s * 32 + lane);
+    }
+  for (int64_t s = 0; s < P.uslices; ++s)
+    for (int lane = 0; lane < 32; ++lane) {
+      const int32_t row = Up.slice_row[s * 32 + lane];
+      if (row >= 0) upos[row - R0] = (int32_t)(s * 32 + lane);
+    }
+  int64_t rec = 0;
+  for (size_t b = 0; b < nb; ++b) {
+    int32_t info[REG_BINFO_INTS];
+    info[8] = (int32_t)blk[b];
+    info[9] = (int32_t)blk[b + 1];
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      const TriPack<T> &S = sweep ? Up : Lp;
+      const bool upper = sweep == 1;
+      const int32_t lv0 = S.blk_lev[b], lv1 = S.blk_lev[b + 1];
+      const int32_t sb0 = S.lev_slice[lv0];
+      info[3 * sweep + 0] = (int32_t)rec;
+      info[3 * sweep + 1] = S.lev_slice[lv1] - sb0;
+      info[3 * sweep + 2] = lv1 - lv0;
+      info[6 + sweep] = (int32_t)P.lev_off.size();
+      info[10 + sweep] = sb0;
+      P.max_levels = std::max(P.max_levels, lv1 - lv0);
+      for (int32_t v = lv0; v < lv1; ++v) {
+        P.lev_off.push_back((int32_t)rec);
+        const int32_t send = S.lev_slice[v + 1] - sb0;     // level end (block-relative slice)
+        for (int32_t s = S.lev_slice[v]; s < S.lev_slice[v + 1]; ++s, ++rec) {
+          const int w = (int)((S.slice_off[s + 1] - S.slice_off[s]) / 32);
+          uint8_t *base = P.data.data() + (size_t)rec * P.rec_bytes;
+          T *val = reinterpret_cast<T *>(base);
+          uint64_t *col = reinterpret_cast<uint64_t *>(base + (size_t)W * 32 * sizeof(T));
+          int32_t *out = reinterpret_cast<int32_t *>(col + (size_t)W4 * 32);
+          T *rdiag = reinterpret_cast<T *>(out + 32);
+          if (v - lv0 > 65535) return;
+          P.slev.push_back((uint16_t)(v - lv0));
+          for (int lane = 0; lane < 32; ++lane) {
+            const int32_t row = S.slice_row[(int64_t)s * 32 + lane];
+            out[lane] = row < 0 ? -1 : (upper ? row : upos[row - R0]);
+            rdiag[lane] = upper ? T(1) / S.diag[(int64_t)s * 32 + lane] : T(1);
+            for (int j = 0; j < W4; ++j) {
+              uint64_t word = 0;
+              for (int t = 0; t < 4; ++t) {
+                const int e = 4 * j + t;
+                uint64_t slot = (uint64_t)(R - 1);
+                if (e < w) {
+                  const int64_t g = S.slice_off[s] + 32 * e + lane;
+                  val[e * 32 + lane] = S.val[g];
+                  const int32_t dep = S.col[g];
+                  if (dep >= 0) {
+                    const int32_t pd = upper ? upos[dep - R0] : P.lpos[dep - R0];
+                    const int32_t q = pd - sb0 * 32;            // block-relative position
+                    if ((int64_t)send * 32 - 1 - q < R) { slot = (uint64_t)(q & (R - 1)); P.near++; }
+                    else { P.far++; }
+                  }
+                }
+                word |= slot << (16 * t);
+              }
+              col[j * 32 + lane] = word;
+            }
+          }
+        }
+      }
+      P.lev_off.push_back((int32_t)rec);
+    }
+    P.binfo.insert(P.binfo.end(), info, info + REG_BINFO_INTS);
+    P.max_block_slices = std::max(P.max_block_slices, info[1] + info[4]);
+  }
+  P.ok = P.far == 0 && R <= 65536 && P.nrec < INT32_MAX;
+}
+
 }  // namespace
 
 template <typename T>
@@ -214,6 +308,7 @@ void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
   pack_sweep(blk, fac, false, S.Lp);
   pack_sweep(blk, fac, true, S.Up);
   pack_pipe(blk, S.Lp, S.Up, S.pipe);
+  pack_reg(blk, S.Lp, S.Up, S.reg);
 }
 
 template void pack_stage<double>(const std::vector<int64_t> &, const std::vector<Factor<double>> &, Stage<double> &);
