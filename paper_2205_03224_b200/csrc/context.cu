@@ -422,7 +422,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     d.nearc = S.pipe.near;
   }
   if (S.reg.ok && cps_override <= 0 && tri_kernel == 0 && d.nblk > 0 &&
-      reg_smem_bytes<D>(S.reg.ring, S.reg.max_block_slices) <= 232448) {
+      reg_smem_bytes<D>(S.reg.ring, S.reg.max_block_slices) <= 232448 - 1024) {
     static_assert(REG_BINFO == REG_BINFO_INTS, "binfo layout");
     d.reg = true;
     d.reg_w = S.reg.W;
@@ -634,7 +634,7 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
     Timed t(ctx->prof, ctx->stream, kc, lvl);
     static bool attr = false;
     if (!attr) {
-      const int smax = 232448;
+      const int smax = 232448 - 1024;   // room for the static shared block info
       CK(cudaFuncSetAttribute(k_tri_reg<D, 4, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       CK(cudaFuncSetAttribute(k_tri_reg<D, 8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       CK(cudaFuncSetAttribute(k_tri_reg<D, 10, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));

@@ -556,13 +556,39 @@ template <int NW> __device__ inline void reg_sync(int v) {
 }
 template <int NW> __device__ inline void reg_sync_all() { asm volatile("bar.sync 0, %0;" ::"n"(32 * NW) : "memory"); }
 
+// 16 bytes of values per lane and load: VE entries (2 doubles / 1 complex)
+template <typename T> struct Vec16;
+template <> struct Vec16<double> { using type = double2; static constexpr int VE = 2; };
+template <> struct Vec16<cd> { using type = double2; static constexpr int VE = 1; };
+template <typename T> __device__ inline T vec_get(const double2 &u, int k);
+template <> __device__ inline double vec_get<double>(const double2 &u, int k) { return k ? u.y : u.x; }
+template <> __device__ inline cd vec_get<cd>(const double2 &u, int) { return cd{u.x, u.y}; }
+
 template <typename T, int W>
 struct RegBuf {
-  static constexpr int W4 = (W + 3) / 4;
-  T v[W];
-  unsigned long long c[W4];
+  static constexpr int VE = Vec16<T>::VE;
+  static constexpr int NV = (W + VE - 1) / VE;   // 16-byte value loads
+  static constexpr int W8 = (W + 7) / 8;         // 16-byte slot loads (8 x uint16)
+  double2 v[NV];
+  uint4 c[W8];
   T rhs, dg;
   int out;
+  __device__ T val(int e) const { return vec_get<T>(v[e / VE], e % VE); }
+  // Wait here for this buffer's loads.  ptxas puts all prefetch loads on one
+  // scoreboard slot, and a read of a loaded register waits for EVERY load on
+  // that slot; settling the next buffer before the other one is refilled
+  // keeps the two-slice prefetch depth (the wait then covers only this
+  // buffer's loads, issued a slice earlier, after this warp's barrier arrival).
+  __device__ void settle() const {
+    unsigned long long t;
+    asm volatile("mov.b64 %0, %1;" : "=l"(t) : "l"(__double_as_longlong(v[0].x)));
+  }
+  __device__ unsigned slot(int e) const {
+    const uint4 &q = c[e / 8];
+    const int k = (e % 8) / 2;
+    const unsigned w = k == 0 ? q.x : k == 1 ? q.y : k == 2 ? q.z : q.w;
+    return (e & 1) ? (w >> 16) : (w & 0xffffu);
+  }
 };
 
 template <typename T, int W, int NW>
@@ -575,7 +601,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
   unsigned short *lvt = reinterpret_cast<unsigned short *>(smem + (size_t)P.ring * sizeof(T) + 16);
   const int R = P.ring;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int *bi = P.binfo + REG_BINFO * blockIdx.x;
+  // The block's info goes through shared memory: a register loaded from global
+  // memory shares a scoreboard slot with the prefetch loads issued later, and
+  // every later read of it would wait for those (shared loads use another slot).
+  __shared__ int bis[REG_BINFO];
+  if (tid < REG_BINFO) bis[tid] = P.binfo[REG_BINFO * blockIdx.x + tid];
+  __syncthreads();
+  const int *bi = bis;
   {                                                                // level table of the block's records (L then U)
     const int f = bi[0], nl = bi[1] + bi[4];                       // U records follow the L records of the block
     for (int i = tid; i < nl; i += blockDim.x) lvt[i] = P.slev[f + i];
@@ -600,7 +632,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
   }
   static_assert(NW <= 15, "barrier ids rotate over 15 named barriers");
   using Buf = RegBuf<T, W>;
-  constexpr int W4 = Buf::W4;
+  constexpr int NV = Buf::NV, W8 = Buf::W8;
   int base_lev = 0;                                                // levels of earlier sweeps (for prog)
 #pragma unroll 1
   for (int sw = 0; sw < 2; ++sw) {
@@ -612,13 +644,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
     auto load = [&](Buf &B, int s) {
       if (s >= ns) return;
       const unsigned char *rec = P.data + (size_t)(r0 + s) * RB;
-      const T *vp = reinterpret_cast<const T *>(rec) + lane;
-      const unsigned long long *cp = reinterpret_cast<const unsigned long long *>(rec + (size_t)W * 32 * sizeof(T)) + lane;
-      const int *op = reinterpret_cast<const int *>(cp + (W4 - 1) * 32 + (32 - lane));   // record's out[]
+      const double2 *vp = reinterpret_cast<const double2 *>(rec) + lane;
+      const uint4 *cp = reinterpret_cast<const uint4 *>(rec + (size_t)W * 32 * sizeof(T)) + lane;
+      const int *op = reinterpret_cast<const int *>(rec + (size_t)W * 32 * sizeof(T) + (size_t)W8 * 512);   // out[]
 #pragma unroll
-      for (int e = 0; e < W; ++e) B.v[e] = ld_nc(vp + 32 * e);
+      for (int k = 0; k < NV; ++k) B.v[k] = __ldg(vp + 32 * k);
 #pragma unroll
-      for (int j = 0; j < W4; ++j) B.c[j] = __ldg(cp + 32 * j);
+      for (int j = 0; j < W8; ++j) B.c[j] = __ldg(cp + 32 * j);
       B.out = __ldg(op + lane);
       const size_t ri = (size_t)(gbase + s) * 32 + lane;
       if (upper) {
@@ -641,30 +673,35 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
         if (warp == 0 && lane == 0) *prog = base_lev + cur;
       }
       if (tr) { const int pv = *prog; tp[2] = clock64() + (pv == -7 ? 1 : 0); tp[6] = lv; }
+      if (tr) {
+        const double pr = dabs2(B.val(0)) + dabs2(B.val(W - 1)) + (double)B.slot(0) + (double)B.slot(W - 1) + dabs2(B.rhs);
+        tp[4] = clock64() + (pr != pr ? 1 : 0);
+        const double q = dabs2(ring[B.slot(0)]) + dabs2(ring[B.slot(W - 1)]);
+        tp[5] = clock64() + (q != q ? 1 : 0);
+      }
       T acc = B.rhs, a1 = dzero<T>(), a2 = dzero<T>(), a3 = dzero<T>();
 #pragma unroll
-      for (int j = 0; j < W4; ++j) {
-        const unsigned long long c = B.c[j];
-        const int e = 4 * j;
-        acc -= B.v[e] * ring[(unsigned)(c & 0xffff)];
-        if (e + 1 < W) a1 -= B.v[e + 1 < W ? e + 1 : 0] * ring[(unsigned)((c >> 16) & 0xffff)];
-        if (e + 2 < W) a2 -= B.v[e + 2 < W ? e + 2 : 0] * ring[(unsigned)((c >> 32) & 0xffff)];
-        if (e + 3 < W) a3 -= B.v[e + 3 < W ? e + 3 : 0] * ring[(unsigned)(c >> 48)];
+      for (int e = 0; e < W; e += 4) {
+        acc -= B.val(e) * ring[B.slot(e)];
+        if (e + 1 < W) a1 -= B.val(e + 1) * ring[B.slot(e + 1)];
+        if (e + 2 < W) a2 -= B.val(e + 2) * ring[B.slot(e + 2)];
+        if (e + 3 < W) a3 -= B.val(e + 3) * ring[B.slot(e + 3)];
       }
       acc = (acc + a1) + (a2 + a3);
       if (tr) { const double pr = dabs2(acc); tp[1] = clock64() + (pr != pr ? 1 : 0); }
       if (upper) acc = acc * B.dg;
-      if (B.out >= 0) {
-        ring[(s * 32 + lane) & (R - 1)] = acc;
-        if (!upper) P.mid[B.out] = acc;
-        else if (mode == TRI_UP) tmp[B.out] = acc;                 // x -= tmp after the sweep
-        else x[B.out] = acc;
-      }
+      if (B.out >= 0) ring[(s * 32 + lane) & (R - 1)] = acc;
       // done with level lv: signal without waiting, unless this warp's next
-      // slice is in level lv + 1 (then its next compute syncs at barrier lv)
+      // slice is in level lv + 1 (then its next compute syncs at barrier lv);
+      // the global stores below are read only after the sweep-transition barrier
       if (s + NW >= ns || lvt[lvbase + s + NW] > lv + 1) {
         reg_arrive<NW>(lv);
         cur = lv + 1;
+      }
+      if (B.out >= 0) {
+        if (!upper) P.mid[B.out] = acc;
+        else if (mode == TRI_UP) tmp[B.out] = acc;                 // x -= tmp after the sweep
+        else x[B.out] = acc;
       }
       if (tr) tp[3] = clock64();
     };
@@ -675,10 +712,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
     load(B, s + NW);
     while (s < ns) {
       compute(A, s);
+      if (s + NW < ns) B.settle();
       load(A, s + 2 * NW);
       s += NW;
       if (s >= ns) break;
       compute(B, s);
+      if (s + NW < ns) A.settle();
       load(B, s + 2 * NW);
       s += NW;
     }

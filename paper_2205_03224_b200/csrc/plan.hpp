@@ -124,9 +124,10 @@ struct PipePack {
 // feeds an address (a loaded address would make the warp wait on the load
 // before it reaches the next level barrier).  Record of a slice, 128-byte
 // aligned, for lane r:
-//   T val[W][32] (0 on padding); uint64 col[ceil(W/4)][32]: four 16-bit ring
-//   slots (padding -> slot ring-1); int32 out[32]; T rdiag[32] = 1/u_ii (U
-//   sweep; 1 in the L sweep).  The level of every record (uint16 `slev`, in the
+//   values and ring slots in 16-byte units per lane, so a warp's load is one
+//   512-byte LDG.128: T val[W/VE][32][VE] (VE = 16 / sizeof(T) entries per unit,
+//   0 on padding); uint16 col[ceil(W/8)][32][8] ring slots (padding -> slot
+//   ring-1); int32 out[32]; T rdiag[32] = 1/u_ii (U sweep; 1 in the L sweep).  The level of every record (uint16 `slev`, in the
 //   sweep) is copied to shared memory at kernel start: the barrier count of a
 //   warp never waits on a global load.
 // out: L sweep -> stage-global packed U position (where the U sweep reads its
@@ -141,7 +142,7 @@ constexpr int REG_BINFO_INTS = 12;
 inline int reg_width(int w) { return w <= 4 ? 4 : w <= 8 ? 8 : w <= 10 ? 10 : w <= 12 ? 12 : w <= 16 ? 16 : 0; }
 template <typename T>
 inline size_t reg_record_bytes(int W) {
-  const size_t b = (size_t)W * 32 * sizeof(T) + (size_t)((W + 3) / 4) * 32 * 8 + 32 * 4 + 32 * sizeof(T);
+  const size_t b = (size_t)W * 32 * sizeof(T) + (size_t)((W + 7) / 8) * 32 * 16 + 32 * 4 + 32 * sizeof(T);
   return (b + 127) / 128 * 128;
 }
 template <typename T>

@@ -221,7 +221,7 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
       P.wmax = std::max(P.wmax, (int)((S->slice_off[s + 1] - S->slice_off[s]) / 32));
   P.W = reg_width(std::max(P.wmax, 1));
   if (P.W == 0) return;
-  const int W = P.W, W4 = (W + 3) / 4;
+  const int W = P.W, W8 = (W + 7) / 8, VE = 16 / (int)sizeof(T);
   P.rec_bytes = reg_record_bytes<T>(W);
   P.nrec = P.lslices + P.uslices;
   P.data.assign((size_t)P.nrec * P.rec_bytes, 0);
@@ -260,34 +260,59 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
           const int w = (int)((S.slice_off[s + 1] - S.slice_off[s]) / 32);
           uint8_t *base = P.data.data() + (size_t)rec * P.rec_bytes;
           T *val = reinterpret_cast<T *>(base);
-          uint64_t *col = reinterpret_cast<uint64_t *>(base + (size_t)W * 32 * sizeof(T));
-          int32_t *out = reinterpret_cast<int32_t *>(col + (size_t)W4 * 32);
+          uint16_t *col = reinterpret_cast<uint16_t *>(base + (size_t)W * 32 * sizeof(T));
+          int32_t *out = reinterpret_cast<int32_t *>(col + (size_t)W8 * 32 * 8);
           T *rdiag = reinterpret_cast<T *>(out + 32);
           if (v - lv0 > 65535) return;
           P.slev.push_back((uint16_t)(v - lv0));
+          // entries of every lane with their ring slots
+          struct Ent { T v; uint16_t slot; };
+          std::vector<Ent> ent[32];
           for (int lane = 0; lane < 32; ++lane) {
             const int32_t row = S.slice_row[(int64_t)s * 32 + lane];
             out[lane] = row < 0 ? -1 : (upper ? row : upos[row - R0]);
             rdiag[lane] = upper ? T(1) / S.diag[(int64_t)s * 32 + lane] : T(1);
-            for (int j = 0; j < W4; ++j) {
-              uint64_t word = 0;
-              for (int t = 0; t < 4; ++t) {
-                const int e = 4 * j + t;
-                uint64_t slot = (uint64_t)(R - 1);
-                if (e < w) {
-                  const int64_t g = S.slice_off[s] + 32 * e + lane;
-                  val[e * 32 + lane] = S.val[g];
-                  const int32_t dep = S.col[g];
-                  if (dep >= 0) {
-                    const int32_t pd = upper ? upos[dep - R0] : P.lpos[dep - R0];
-                    const int32_t q = pd - sb0 * 32;            // block-relative position
-                    if ((int64_t)send * 32 - 1 - q < R) { slot = (uint64_t)(q & (R - 1)); P.near++; }
-                    else { P.far++; }
-                  }
+            for (int e = 0; e < w; ++e) {
+              const int64_t g = S.slice_off[s] + 32 * e + lane;
+              const int32_t dep = S.col[g];
+              if (dep < 0) continue;
+              const int32_t pd = upper ? upos[dep - R0] : P.lpos[dep - R0];
+              const int32_t q = pd - sb0 * 32;                  // block-relative position
+              if ((int64_t)send * 32 - 1 - q < R) { ent[lane].push_back(Ent{S.val[g], (uint16_t)(q & (R - 1))}); P.near++; }
+              else { P.far++; }
+            }
+          }
+          // Column e of the slice is one shared-memory gather of 32 lanes (8 or 16
+          // bytes each); order each lane's entries (any order gives the same sum up
+          // to rounding) so that every column spreads its distinct slots over the
+          // bank groups: greedily give each lane the entry whose group is least
+          // used in the column so far.
+          const int G = (int)(128 / sizeof(T));                 // bank groups of one 128-byte wavefront
+          for (int e = 0; e < W; ++e) {
+            std::vector<int> cnt(G, 0);
+            std::vector<uint16_t> seen;
+            for (int lane = 0; lane < 32; ++lane) {
+              uint16_t slot = (uint16_t)(R - 1);
+              T v = T(0);
+              auto &L = ent[lane];
+              if (!L.empty()) {
+                size_t best = 0;
+                int bc = 1 << 30;
+                for (size_t k = 0; k < L.size(); ++k) {
+                  const bool dup = std::find(seen.begin(), seen.end(), L[k].slot) != seen.end();
+                  const int c = dup ? -1 : cnt[L[k].slot % G];          // a repeated slot is a broadcast
+                  if (c < bc) { bc = c; best = k; }
                 }
-                word |= slot << (16 * t);
+                slot = L[best].slot;
+                v = L[best].v;
+                L.erase(L.begin() + (long)best);
               }
-              col[j * 32 + lane] = word;
+              if (std::find(seen.begin(), seen.end(), slot) == seen.end()) {
+                seen.push_back(slot);
+                cnt[slot % G]++;
+              }
+              val[((e / VE) * 32 + lane) * VE + e % VE] = v;
+              col[((e / 8) * 32 + lane) * 8 + e % 8] = slot;
             }
           }
         }

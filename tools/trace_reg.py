@@ -25,7 +25,18 @@ for sw in range(2):
     lv, wp = r[:, 6], r[:, 7]
     nl = int(lv.max()) + 1
     print(f"sweep {'LU'[sw]}: slices {len(r)} levels {nl}; per level {(acc.max() - acc.min()) / nl:.0f} cyc")
-    print(f"   rel->data {np.median(rot - rel):.0f} data->acc {np.median(acc - rot):.0f}  acc->end(stores) {np.median(end - acc):.0f} end->loads issued {np.median(ldi - end):.0f}")
+    print(f"   rel->acc {np.median(acc - rel):.0f} (p90 {np.percentile(acc - rel, 90):.0f})  acc->end(stores) {np.median(end - acc):.0f}")
+    print(f"   rel->data ready {np.median(rot - rel):.0f}  data->2 ring LDS done {np.median(ldi - rot):.0f}  -> acc {np.median(acc - ldi):.0f}")
+    # critical chain per level: the slice whose acc is last in level v-1 -> release of v
+    crit = []
+    for v in range(1, nl):
+        m0, m1 = lv == v - 1, lv == v
+        if m0.any() and m1.any():
+            crit.append((rel[m1].min() - acc[m0].max(), (acc - rel)[m1].max()))
+    crit = np.array(crit)
+    print(f"   per level: last acc(v-1) -> first release(v) median {np.median(crit[:, 0]):.0f}; slowest compute in level median {np.median(crit[:, 1]):.0f}")
+    ns_per = np.bincount(lv.astype(int))
+    print(f"   slices per level: mean {ns_per.mean():.1f} max {ns_per.max()}; frac of slices whose warp's next slice is next level: {np.mean([lv[i + 15] == lv[i] + 1 for i in range(len(lv) - 15)]):.2f}")
     gaps = []
     for v in range(1, nl):
         m0, m1 = lv == v - 1, lv == v
