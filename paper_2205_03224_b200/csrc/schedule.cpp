@@ -210,8 +210,6 @@ void pack_pipe(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriP
 template <typename T>
 void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPack<T> &Up, RegPack<T> &P) {
   P = RegPack<T>();
-  P.ring = REG_RING_BYTES / (int)sizeof(T);
-  const int R = P.ring;
   const size_t nb = blk.size() - 1;
   const int64_t R0 = blk.front(), NR = blk.back() - blk.front();
   P.lslices = (int64_t)Lp.slice_row.size() / 32;
@@ -237,6 +235,28 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
       const int32_t row = Up.slice_row[s * 32 + lane];
       if (row >= 0) upos[row - R0] = (int32_t)(s * 32 + lane);
     }
+  // solution window: the smallest power of two covering every dependency
+  // distance (level end - dependency position), so the ring leaves shared
+  // memory to the record stages of k_tri_seq
+  int64_t need = 1;
+  for (size_t b = 0; b < nb; ++b)
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      const TriPack<T> &S = sweep ? Up : Lp;
+      const int32_t lv0 = S.blk_lev[b], lv1 = S.blk_lev[b + 1];
+      const int32_t sb0 = S.lev_slice[lv0];
+      for (int32_t v = lv0; v < lv1; ++v) {
+        const int64_t send = S.lev_slice[v + 1] - sb0;
+        for (int64_t g = S.slice_off[S.lev_slice[v]]; g < S.slice_off[S.lev_slice[v + 1]]; ++g) {
+          const int32_t dep = S.col[g];
+          if (dep < 0) continue;
+          const int32_t q = (sweep ? upos[dep - R0] : P.lpos[dep - R0]) - sb0 * 32;
+          need = std::max(need, send * 32 - q);
+        }
+      }
+    }
+  P.ring = 1024;
+  while (P.ring < need && P.ring < REG_RING_BYTES / (int)sizeof(T)) P.ring *= 2;
+  const int R = P.ring;
   int64_t rec = 0;
   for (size_t b = 0; b < nb; ++b) {
     int32_t info[REG_BINFO_INTS];
