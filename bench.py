@@ -223,8 +223,14 @@ def run_ours(args):
         per_kernel[kname] = rec
     dom = max((k for k in per_kernel if k in gb), key=lambda k: per_kernel[k]["ms_total"])
     dd = per_kernel[dom]
+    traffic = None                                   # DRAM bytes per launch from the committed ncu launch list
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        traffic = None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": dd["GBps"], "peak": peak, "unit": "GB/s",
-                "frac": dd["frac"], "traffic": None, "peak_source": peak_src,
+                "frac": dd["frac"], "traffic": round(traffic) if traffic else None, "peak_source": peak_src,
                 "bytes_per_launch": round(gb[dom] / dd["launches"]), "us_per_launch": dd["us_per_launch"]}
     launches = int(sum(d["count"] for d in kern.values()))
     # end-to-end: host vectors in natural order through gemslr_solve_host

@@ -172,6 +172,21 @@ def test_cluster_sizes_agree(tmp_path, cps):
     assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
 
 
+@pytest.mark.parametrize("name,dims,over", [("C5", (32, 32, 24), dict(subdomains=4, rank=4)),
+                                             ("C4", (16, 16, 14), dict(subdomains=8, rank=6)),
+                                             ("C3", (20, 18, 16), dict(subdomains=8, rank=0, ilu="ilu0"))])
+@pytest.mark.parametrize("tri_kernel,expect", [(0, "reg"), (1, "pipe"), (2, "level")])
+def test_trisolve_kernels(tmp_path, name, dims, over, tri_kernel, expect):
+    """Each triangular-solve kernel (register-prefetched k_tri_reg, TMA-staged
+    k_tri_pipe, level kernel) against the oracle, fp64 and complex128."""
+    prob, b, xt, prm = P.make_config(name, dims=dims, **over)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path, tri_kernel=tri_kernel)
+    assert all(L["stage"]["kernel"] == expect for L in s.stats()["stages"])
+    for seed in (2, 3):
+        r = P.rhs_vector(prob.n, prob.is_complex, seed)
+        assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
+
+
 # ---------------------------------------------------------------- edge cases
 @pytest.mark.parametrize("kind", ["tiny1d", "p1", "fullrank", "early_stop", "random_bfs", "complex_bfs"])
 def test_edge_cases(tmp_path, kind):

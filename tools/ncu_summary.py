@@ -12,23 +12,56 @@ def short(n):
 
 
 def launches(path, out):
+    """Per-kernel share of the NVTX-filtered solve launches, with DRAM bytes per
+    launch when captured.  k_tri_reg launches come 7 per preconditioner apply
+    (down l0, l1, l2, last, up l2, l1, l0); their classes are written to
+    <out>.traffic.json for bench.py's roofline `traffic`."""
+    import json
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if 'Kernel Name' in r][0]
     h, data = rows[hi], rows[hi + 1:]
-    ik, iv = h.index('Kernel Name'), h.index('Metric Value')
-    tot, cnt = collections.defaultdict(float), collections.Counter()
+    ik, iv, iid = h.index('Kernel Name'), h.index('Metric Value'), h.index('ID')
+    imn = h.index('Metric Name') if 'Metric Name' in h else None
+    per = collections.OrderedDict()          # launch id -> (kernel, {metric: value})
     for r in data:
         if len(r) <= iv:
             continue
+        lid = int(r[iid])
         k = short(r[ik])
-        tot[k] += float(r[iv].replace(',', ''))
+        m = r[imn] if imn is not None else 'gpu__time_duration.sum'
+        per.setdefault(lid, (k, {}))[1][m] = float(r[iv].replace(',', ''))
+    tot, cnt, dram = collections.defaultdict(float), collections.Counter(), collections.defaultdict(float)
+    tri = []
+    for lid, (k, m) in per.items():
+        t = m.get('gpu__time_duration.sum', 0.0)
+        unit_ns = 1.0
+        tot[k] += t * unit_ns
         cnt[k] += 1
+        b = m.get('dram__bytes_read.sum', 0.0) + m.get('dram__bytes_write.sum', 0.0)
+        dram[k] += b
+        if k.startswith('k_tri_reg') or k.startswith('k_tri_pipe'):
+            tri.append((t, b))
     T = sum(tot.values())
-    lines = ["| kernel | launches | total µs | µs/launch | share |", "|---|---|---|---|---|"]
+    lines = ["| kernel | launches | total µs | µs/launch | share | DRAM MB/launch |", "|---|---|---|---|---|---|"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
-        lines.append(f"| {k} | {cnt[k]} | {v / 1e3:.1f} | {v / 1e3 / cnt[k]:.2f} | {100 * v / T:.1f}% |")
+        lines.append(f"| {k} | {cnt[k]} | {v / 1e3:.1f} | {v / 1e3 / cnt[k]:.2f} | {100 * v / T:.1f}% | {dram[k] / cnt[k] / 1e6:.2f} |")
     lines.append(f"\nTotal {T / 1e3:.1f} µs over {sum(cnt.values())} launches (ncu, `--clock-control none`, "
                  "serialised cold-cache launches: compare shares, not absolute times).")
+    cls = {}
+    if tri and len(tri) % 7 == 0:
+        names = ['down_l0', 'down_l1', 'down_l2', 'last', 'up_l2', 'up_l1', 'up_l0']
+        for i, nm in enumerate(names):
+            sel = tri[i::7]
+            cls[nm] = (sum(t for t, _ in sel) / len(sel), sum(b for _, b in sel) / len(sel))
+        lines.append("\nTriangular-solve launches by position in the apply (mean per launch):\n")
+        lines.append("| launch | µs | DRAM MB |\n|---|---|---|")
+        for nm, (t, b) in cls.items():
+            lines.append(f"| {nm} | {t / 1e3:.1f} | {b / 1e6:.1f} |")
+        def group(ks):
+            return sum(cls[x][1] for x in ks) / len(ks)
+        json.dump({"trisolve_down": group(['down_l0', 'down_l1', 'down_l2']),
+                   "trisolve_up": group(['up_l0', 'up_l1', 'up_l2']), "trisolve_last": cls['last'][1],
+                   "source": path}, open(out + '.traffic.json', 'w'), indent=1)
     open(out, 'w').write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
