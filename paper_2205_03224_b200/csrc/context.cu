@@ -346,6 +346,11 @@ struct Engine {
   int *ints = nullptr, *done = nullptr;
   int hist_cap = 0;
   D *xb = nullptr, *bb = nullptr;   // host-path staging
+  int *hflags = nullptr;             // pinned: done flag of every iteration of a cycle (async D2H)
+  int hflags_cap = 0;
+  ~Engine() {
+    if (hflags) cudaFreeHost(hflags);
+  }
   double setup_host_s = 0, setup_dev_s = 0, arnoldi_s = 0;
 
   void upload(cudaStream_t s);
@@ -1188,6 +1193,12 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
     }
     D *res1 = res, *res2 = res + (GS_MAXC + 2), *res3 = res + 2 * (GS_MAXC + 2);
     std::vector<cudaEvent_t> evs;
+    if (hflags_cap < m) {
+      if (hflags) cudaFreeHost(hflags);
+      hflags = nullptr;
+      if (cudaMallocHost(&hflags, (size_t)m * sizeof(int)) != cudaSuccess) throw Error{GEMSLR_ERR_OOM, "pinned flags"};
+      hflags_cap = m;
+    }
     int j = 0;
     for (j = 0; j < m; ++j) {
       D *vj = V + (size_t)j * ldv;
@@ -1206,16 +1217,17 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
         Timed t(ctx->prof, s, KC_UTIL);
         k_scale<D><<<grid_for((n + 255) / 256, 4), 256, 0, s>>>(n, w, V + (size_t)(j + 1) * ldv, dbl + 2, done);
       }
-      // keep at most 2 iterations in flight so the host notices convergence
+      // the done flag of iteration j reaches pinned host memory asynchronously;
+      // the host reads it two iterations later, so the GPU always has the next
+      // iterations queued (a synchronous copy would drain the stream)
+      CK(cudaMemcpyAsync(hflags + j, done, sizeof(int), cudaMemcpyDeviceToHost, s));
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       CK(cudaEventRecord(e, s));
       evs.push_back(e);
       if (j >= 2) {
         CK(cudaEventSynchronize(evs[j - 2]));
-        int dflag = 0;
-        CK(cudaMemcpy(&dflag, done, sizeof(int), cudaMemcpyDeviceToHost));
-        if (dflag) break;
+        if (((volatile int *)hflags)[j - 2]) break;
       }
     }
     CK(cudaStreamSynchronize(s));
