@@ -825,7 +825,25 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
     const int grid = grid_for((nn + 32 * tr - 1) / (32 * tr), 3);
     kern<<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv, doneflag);
   };
-  if (ncols <= 8) go(k_gs<D, 8, 1>, 8);
+  static const bool old_gs = getenv("GEMSLR_OLD_GS") != nullptr;
+  auto go2 = [&](auto kern) {
+    const int grid = grid_for((nn + 255) / 256, ncols <= 32 && sizeof(D) == 8 ? 2 : 1);
+    kern<<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv, doneflag);
+  };
+  bool done2 = false;
+  if (!old_gs && ncols <= 32) {
+    go2(k_gs2<D, 32>);
+    done2 = true;
+  } else if constexpr (sizeof(D) == 8) {
+    if (!old_gs && ncols <= 64) {
+      const int grid = grid_for((nn + 127) / 128, 2);
+      k_gs2h<D><<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv,
+                                               doneflag);
+      done2 = true;
+    }
+  }
+  if (done2) {
+  } else if (ncols <= 8) go(k_gs<D, 8, 1>, 8);
   else if (ncols <= 24) go(k_gs<D, 4, 3>, 4);
   else if (ncols <= 48) go(k_gs<D, 2, 6>, 2);
   else go(k_gs<D, 1, 13>, 1);

@@ -975,6 +975,195 @@ __global__ void __launch_bounds__(256) k_gs(int64_t n, const T *__restrict__ V, 
   if (tid == 0) *ticket = 0;
 }
 
+// Warp-tile form of the CGS2 passes: a warp owns 32-row tiles and ALL columns
+// (NC >= ncols, the tile's V values stay in registers between the update and
+// the dot), so there is no block barrier per tile.  The dots of a tile are
+// reduced over the lanes by a transpose-butterfly (31 shuffles per 32 columns;
+// afterwards lane i holds column i), accumulated in registers, and reduced over
+// the warps and CTAs once at the end (deterministic, fixed order).
+template <typename T>
+__device__ inline T shfl_x(T v, int m) { return shfl_xor(v, m); }
+template <typename T>
+__device__ inline void tbfly32(T (&x)[32], int lane) {              // lane i <- sum over lanes of x[i]
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const T send = up ? x[k] : x[k + o];
+      const T keep = up ? x[k + o] : x[k];
+      x[k] = keep + shfl_x(send, o);
+    }
+  }
+}
+template <typename T, int NC>
+__global__ void __launch_bounds__(256, NC * sizeof(T) > 256 ? 1 : 2) k_gs2(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
+                                              int dot, const T *__restrict__ h_in, T *__restrict__ partial,
+                                              unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
+  if (done && *done) return;
+  constexpr int NCH = NC / 32;
+  __shared__ T sh[NC];
+  __shared__ T red[8][NC + 1];
+  __shared__ bool amlast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c = tid; c < NC; c += blockDim.x) sh[c] = (upd && c < ncols) ? h_in[c] : dzero<T>();
+  __syncthreads();
+  T acc[NCH];
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) acc[q] = dzero<T>();
+  double nrm = 0.0;
+  const int64_t ntiles = (n + 31) / 32;
+  for (int64_t tile = (int64_t)blockIdx.x * 8 + warp; tile < ntiles; tile += (int64_t)gridDim.x * 8) {
+    const int64_t r = tile * 32 + lane;
+    const bool ok = r < n;
+    T v[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c] = (c < ncols && ok) ? ld_nc(V + c * ldv + r) : dzero<T>();
+    T wi = ok ? w[r] : dzero<T>();
+    if (upd) {
+      T u0 = dzero<T>(), u1 = dzero<T>();
+#pragma unroll
+      for (int c = 0; c < NC; c += 2) {
+        u0 += v[c] * sh[c];
+        u1 += v[c + 1] * sh[c + 1];
+      }
+      wi = wi - (u0 + u1);
+      if (ok) w[r] = wi;
+    }
+    nrm += dabs2(wi);
+    if (dot) {
+#pragma unroll
+      for (int q = 0; q < NCH; ++q) {
+        T x[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) x[k] = dconj(v[32 * q + k]) * wi;
+        tbfly32(x, lane);
+        acc[q] += x[0];
+      }
+    }
+  }
+  // lane i of warp w holds column 32 q + i of this warp; warp 0 the norm too
+  const int nres = dot ? ncols + 1 : 1;
+  nrm = warp_sum(nrm);
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) red[warp][32 * q + lane] = acc[q];
+  if (lane == 0) {
+    T t = dzero<T>();
+    if constexpr (sizeof(T) == sizeof(double)) t = nrm; else t = T{nrm, 0.0};
+    red[warp][NC] = t;
+  }
+  __syncthreads();
+  for (int c = tid; c < nres; c += blockDim.x) {
+    const int src = (c == nres - 1) ? NC : c;
+    T t = dzero<T>();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += red[q][src];
+    partial[(int64_t)c * gridDim.x + blockIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) amlast = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!amlast) return;
+  __threadfence();
+  reduce_partials(partial, (int)gridDim.x, nres, res);
+  if (tid == 0) *ticket = 0;
+}
+
+// The same with 33..64 columns: a warp covers 16 rows, lanes 0-15 hold columns
+// 0..31 and lanes 16-31 columns 32..63 of the same rows (32 values per lane as
+// in k_gs2<T, 32>); the two halves of the update are combined with one
+// shuffle and the dots reduced over the 16 lanes of a half (15 shuffles per 16
+// columns; afterwards lane sub of half h holds columns 32h + sub and 32h + 16 + sub).
+template <typename T>
+__device__ inline void tbfly16(T (&x)[16], int sub) {
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) {
+    const bool up = (sub & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const T send = up ? x[k] : x[k + o];
+      const T keep = up ? x[k + o] : x[k];
+      x[k] = keep + shfl_x(send, o);
+    }
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(256, 2) k_gs2h(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
+                                               int dot, const T *__restrict__ h_in, T *__restrict__ partial,
+                                               unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
+  if (done && *done) return;
+  __shared__ T sh[64];
+  __shared__ T red[8][65];
+  __shared__ bool amlast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int half = lane >> 4, sub = lane & 15;
+  for (int c = tid; c < 64; c += blockDim.x) sh[c] = (upd && c < ncols) ? h_in[c] : dzero<T>();
+  __syncthreads();
+  T acc0 = dzero<T>(), acc1 = dzero<T>();
+  double nrm = 0.0;
+  const int64_t ntiles = (n + 15) / 16;
+  const T *Vh = V + (int64_t)(32 * half) * ldv;
+  const int nc = ncols - 32 * half;                                 // columns of this half
+  for (int64_t tile = (int64_t)blockIdx.x * 8 + warp; tile < ntiles; tile += (int64_t)gridDim.x * 8) {
+    const int64_t r = tile * 16 + sub;
+    const bool ok = r < n;
+    T v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = (k < nc && ok) ? ld_nc(Vh + k * ldv + r) : dzero<T>();
+    T wi = ok ? w[r] : dzero<T>();
+    if (upd) {
+      T u0 = dzero<T>(), u1 = dzero<T>();
+#pragma unroll
+      for (int k = 0; k < 32; k += 2) {
+        u0 += v[k] * sh[32 * half + k];
+        u1 += v[k + 1] * sh[32 * half + k + 1];
+      }
+      T u = u0 + u1;
+      u = u + shfl_x(u, 16);
+      wi = wi - u;
+      if (ok && half == 0) w[r] = wi;
+    }
+    if (half == 0) nrm += dabs2(wi);
+    if (dot) {
+      T x[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = dconj(v[k]) * wi;
+      tbfly16(x, sub);
+      acc0 += x[0];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = dconj(v[16 + k]) * wi;
+      tbfly16(x, sub);
+      acc1 += x[0];
+    }
+  }
+  const int nres = dot ? ncols + 1 : 1;
+  nrm = warp_sum(nrm);
+  red[warp][32 * half + sub] = acc0;
+  red[warp][32 * half + 16 + sub] = acc1;
+  if (lane == 0) {
+    T t = dzero<T>();
+    if constexpr (sizeof(T) == sizeof(double)) t = nrm; else t = T{nrm, 0.0};
+    red[warp][64] = t;
+  }
+  __syncthreads();
+  for (int c = tid; c < nres; c += blockDim.x) {
+    const int src = (c == nres - 1) ? 64 : c;
+    T t = dzero<T>();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += red[q][src];
+    partial[(int64_t)c * gridDim.x + blockIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) amlast = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!amlast) return;
+  __threadfence();
+  reduce_partials(partial, (int)gridDim.x, nres, res);
+  if (tid == 0) *ticket = 0;
+}
+
 // ----------------------------------------------------------------- FGMRES column (1 thread)
 template <typename T>
 struct FgmDev {
