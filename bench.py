@@ -234,8 +234,10 @@ def run_ours(args):
                 "bytes_per_launch": round(gb[dom] / dd["launches"]), "us_per_launch": dd["us_per_launch"]}
     launches = int(sum(d["count"] for d in kern.values()))
     # end-to-end: host vectors in natural order through gemslr_solve_host
-    bh = np.ascontiguousarray(b)
-    xh = np.zeros_like(bh)
+    # inputs and outputs in pinned host memory (the copies run at link speed)
+    bh_t = torch.from_numpy(np.ascontiguousarray(b)).pin_memory()
+    xh_t = torch.zeros_like(bh_t).pin_memory()
+    bh, xh = bh_t.numpy(), xh_t.numpy()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()

@@ -610,7 +610,17 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
   const int *bi = bis;
   {                                                                // level table of the block's records (L then U)
     const int f = bi[0], nl = bi[1] + bi[4];                       // U records follow the L records of the block
-    for (int i = tid; i < nl; i += blockDim.x) lvt[i] = P.slev[f + i];
+    constexpr int U = 8;                                           // independent loads in flight per thread
+    const int nt = blockDim.x;
+    int i = tid;
+    for (; i + (U - 1) * nt < nl; i += U * nt) {
+      unsigned short v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = P.slev[f + i + u * nt];
+#pragma unroll
+      for (int u = 0; u < U; ++u) lvt[i + u * nt] = v[u];
+    }
+    for (; i < nl; i += nt) lvt[i] = P.slev[f + i];
   }
   for (int i = tid; i < R; i += blockDim.x) ring[i] = dzero<T>();
   if (tid == 0) *prog = 0;
@@ -727,8 +737,22 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
     reg_sync_all<NW>();                                            // sweep transition: mid / tmp visible, ring free
     if (warp == 0 && lane == 0) *prog = base_lev;
   }
-  if (mode == TRI_UP)                                              // y1 = z1 - U^-1 L^-1 F y2 (Alg. 2 l.9)
-    for (int i = bi[8] + tid; i < bi[9]; i += 32 * NW) x[i] = x[i] - ld_cg(tmp + i);
+  if (mode == TRI_UP) {                                            // y1 = z1 - U^-1 L^-1 F y2 (Alg. 2 l.9)
+    constexpr int U = 8;                                           // 8 independent rows in flight per thread
+    const int i0 = bi[8], i1 = bi[9];
+    int i = i0 + tid;
+    for (; i + (U - 1) * 32 * NW < i1; i += U * 32 * NW) {
+      T a[U], t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a[u] = x[i + u * 32 * NW];
+        t[u] = ld_cg(tmp + i + u * 32 * NW);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[i + u * 32 * NW] = a[u] - t[u];
+    }
+    for (; i < i1; i += 32 * NW) x[i] = x[i] - ld_cg(tmp + i);
+  }
 }
 
 // Packs the L-sweep right-hand sides of a stage in chunk order:
