@@ -277,6 +277,11 @@ struct StageDev {
   int reg_w = 0;           // record width W (4, 8, 10, 12 or 16)
   RegDev<D> Rg{};
   int64_t reg_bytes = 0;   // record bytes of both sweeps
+  const int *lrow = nullptr;       // per packed L position: the row (-1 padding), DOWN gather
+  D *rhs_up = nullptr;             // UP right-hand sides (zero except the F_l rows)
+  const int *fpos = nullptr, *frow = nullptr;
+  int64_t nf = -1;                 // rows with F_l entries (-1: not set up, use k_pack_rhs)
+  int64_t lslices = 0;
   int64_t nchunks = 0, far = 0, nearc = 0;
   int64_t nnz = 0;         // real stored nonzeros (L + U incl. diagonal)
   int64_t padded = 0;      // stored entries incl. padding
@@ -438,6 +443,10 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     d.Rg.binfo = P.upload<int>(S.reg.binfo, s);
     d.Rg.lev_off = P.upload<int>(S.reg.lev_off, s);
     d.Rg.rhsL = P.get<D>(std::max<int64_t>(S.reg.lslices * 32, 1));
+    d.lrow = P.upload<int>(S.Lp.slice_row, s);
+    d.lslices = S.reg.lslices;
+    d.rhs_up = P.get<D>(std::max<int64_t>(S.reg.lslices * 32, 1));
+    CK(cudaMemsetAsync(d.rhs_up, 0, std::max<int64_t>(S.reg.lslices * 32, 1) * sizeof(D), s));
     d.Rg.mid = P.get<D>(std::max<int64_t>(S.reg.uslices * 32, 1));
     d.Rg.ring = S.reg.ring;
     d.reg_bytes = (int64_t)S.reg.data.size();
@@ -532,6 +541,27 @@ void Engine<T>::upload(cudaStream_t s) {
     d.st = upload_stage<D>(P, s, plan.stage[l], ctx->params.cluster_ctas, ctx->params.tri_kernel);
     d.E = upload_csr<D>(P, s, plan.E[l]);
     d.F = upload_csr<D>(P, s, plan.F[l]);
+    if (d.st.reg) {                                                // sparse UP pack: the rows with F_l entries
+      const auto &Fh = plan.F[l];
+      const Stage<T> &S = plan.stage[l];
+      const int64_t R0 = S.blk.empty() ? 0 : S.blk.front();
+      std::vector<int32_t> fpos, frow;
+      bool ok = true;
+      for (int64_t i = 0; i < Fh.n && ok; ++i) {
+        if (Fh.ptr[i + 1] == Fh.ptr[i]) continue;
+        const int64_t row = d.o0 + i - R0;
+        if (row < 0 || row >= (int64_t)S.reg.lpos.size() || S.reg.lpos[row] < 0) ok = false;
+        else {
+          fpos.push_back(S.reg.lpos[row]);
+          frow.push_back((int32_t)i);
+        }
+      }
+      if (ok) {
+        d.st.fpos = P.upload<int>(fpos, s);
+        d.st.frow = P.upload<int>(frow, s);
+        d.st.nf = (int64_t)fpos.size();
+      }
+    }
     hE[l] = upload_halo<D>(P, s, plan.hE[l]);
     hF[l] = upload_halo<D>(P, s, plan.hF[l]);
   }
@@ -630,11 +660,22 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
   if (S.reg) {
     constexpr int NW = sizeof(D) == 8 ? 15 : 7;   // (NW + 1) warps a multiple of 4: full register budget
     const size_t smem = reg_smem_bytes<D>(S.Rg.ring, S.Rg.max_slices);
+    RegDev<D> Rg = S.Rg;
     {
       Timed tp(ctx->prof, ctx->stream, KC_PACK);
-      k_pack_rhs<D><<<pgrid, 256, 0, ctx->stream>>>(S.rows, S.row0, S.P.lpos, const_cast<D *>(S.Rg.rhsL),
-                                                    mode == TRI_DOWN ? rhs : nullptr, Fp, Fc, Fv, Fbase, x, fa.nloc,
-                                                    fa.yh, fa.nh, fa.yl, doneflag);
+      if (mode == TRI_DOWN) {
+        const int64_t np = S.lslices * 32;
+        k_pack_gather<D><<<grid_for((np + 255) / 256, 4), 256, 0, ctx->stream>>>(np, S.lrow, rhs, const_cast<D *>(S.Rg.rhsL),
+                                                                                doneflag);
+      } else if (S.nf >= 0) {
+        Rg.rhsL = S.rhs_up;
+        if (S.nf > 0)
+          k_pack_f<D><<<grid_for((S.nf + 255) / 256, 4), 256, 0, ctx->stream>>>(S.nf, S.fpos, S.frow, Fp, Fc, Fv, x, fa.nloc,
+                                                                                fa.yh, fa.nh, fa.yl, S.rhs_up, doneflag);
+      } else {
+        k_pack_rhs<D><<<pgrid, 256, 0, ctx->stream>>>(S.rows, S.row0, S.P.lpos, const_cast<D *>(S.Rg.rhsL), nullptr, Fp, Fc,
+                                                      Fv, Fbase, x, fa.nloc, fa.yh, fa.nh, fa.yl, doneflag);
+      }
     }
     Timed t(ctx->prof, ctx->stream, kc, lvl);
     static bool attr = false;
@@ -647,7 +688,6 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
       CK(cudaFuncSetAttribute(k_tri_reg<D, 16, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       attr = true;
     }
-    RegDev<D> Rg = S.Rg;
     Rg.dbg = (kc == KC_TRI_DOWN && lvl == g_tri_dbg_level) ? g_tri_dbg : nullptr;
     static const int reg_flags = getenv("GEMSLR_REG_FLAGS") ? atoi(getenv("GEMSLR_REG_FLAGS")) : 0;
     Rg.flags = reg_flags;

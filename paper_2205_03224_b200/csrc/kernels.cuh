@@ -755,6 +755,39 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
   }
 }
 
+// Right-hand sides of k_tri_reg's L sweep in packed order (index = slice·32 + lane).
+// DOWN: gather form dst[p] = src[lrow[p]] — coalesced writes, the reads hit L2
+// (the input vector was just written).  UP: only the rows with F_l entries,
+// dst[fpos[i]] = (F_l y_J)_{frow[i]} (~10 % of the rows at level 0); the other
+// positions of the UP buffer are zero from setup on.
+template <typename T>
+__global__ void __launch_bounds__(256) k_pack_gather(int64_t np, const int *__restrict__ lrow, const T *__restrict__ src,
+                                                     T *__restrict__ dst, const int *__restrict__ done) {
+  if (done && *done) return;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x) {
+    const int r = lrow[p];
+    dst[p] = r >= 0 ? src[r] : dzero<T>();
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_pack_f(int64_t nf, const int *__restrict__ fpos, const int *__restrict__ frow,
+                                                const int64_t *__restrict__ Fptr, const int32_t *__restrict__ Fcol,
+                                                const T *__restrict__ Fval, const T *__restrict__ y, int64_t nloc,
+                                                const T *__restrict__ yh, int64_t nh, const T *__restrict__ yl,
+                                                T *__restrict__ dst, const int *__restrict__ done) {
+  if (done && *done) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += (int64_t)gridDim.x * blockDim.x) {
+    const int li = frow[i];
+    T v = dzero<T>();
+    for (int64_t p = Fptr[li]; p < Fptr[li + 1]; ++p) {
+      const int64_t c = Fcol[p];
+      const T yc = c < nloc ? y[c] : (c < nloc + nh ? yh[c - nloc] : yl[c - nloc - nh]);
+      v += Fval[p] * yc;
+    }
+    dst[fpos[i]] = v;
+  }
+}
+
 // Packs the L-sweep right-hand sides of a stage in chunk order:
 // DOWN: dst[lpos[i]] = src[row0 + i];  UP: dst[lpos[i]] = (F_l y_J)_{row0 + i},
 // with F_l's columns local (< nloc), in the halo yh (< nloc + nh) or in the
