@@ -341,6 +341,8 @@ struct Engine {
   // workspace
   D *r = nullptr, *tmp = nullptr, *tvec = nullptr, *partial = nullptr, *res = nullptr;
   unsigned *tickets = nullptr;
+  int *ewflag = nullptr;             // release flag of k_ewx (epoch counter)
+  int ew_epoch = 0;
   size_t partial_cap = 0;
   // Krylov workspace (lazy)
   int kry_m = -1;
@@ -579,6 +581,8 @@ void Engine<T>::upload(cudaStream_t s) {
   partial = P.get<D>(partial_cap);
   res = P.get<D>(4 * (GS_MAXC + 2));
   tickets = P.get<unsigned>(16);
+  ewflag = P.get<int>(1);
+  CK(cudaMemsetAsync(ewflag, 0, sizeof(int), s));
   CK(cudaMemsetAsync(tickets, 0, 16 * sizeof(unsigned), s));
   CK(cudaMemsetAsync(r, 0, (n + 1) * sizeof(D), s));
   CK(cudaMemsetAsync(tmp, 0, (n + 1) * sizeof(D), s));
@@ -780,6 +784,29 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, l);
     if (d.s > 0 || dist) {
       exchange(hE[l], out, doneflag);                              // z1 entries of E_l's exterior columns
+      if (!dist && d.k > 0 && d.k <= 64) {                         // one cooperative launch: K6 + K7 + K8
+        Timed t(ctx->prof, s, KC_EW);
+        static int max_ctas = 0;
+        if (max_ctas == 0) {
+          int per = 0;
+          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ewx<D>, 256, 0));
+          max_ctas = std::max(1, per) * kNumSM;
+        }
+        const int grid = (int)std::min<int64_t>((std::max<int64_t>(d.s, 1) + 255) / 256, max_ctas);
+        ++ew_epoch;
+        int64_t a0 = d.s, a1 = d.o1, a5 = n, a11 = d.ldw;
+        const int64_t *a2 = d.E.ptr;
+        const int32_t *a3 = d.E.col;
+        const D *a4 = d.E.val, *zz = out, *zh = hE[l].rbuf, *sr = src, *Wp = d.W, *Gp = d.G;
+        D *ds = r, *pt = partial, *so = tvec;
+        int kk = d.k, ep = ew_epoch;
+        unsigned *tk = tickets + 0;
+        int *fl = ewflag;
+        const int *dn = doneflag;
+        void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &ep, &dn};
+        CK(cudaLaunchCooperativeKernel((const void *)k_ewx<D>, dim3(grid), dim3(256), args, 0, s));
+        continue;
+      }
       // z2 = b2 - E_l z1 ; this rank's part of s = W^H z2
       {
         Timed t(ctx->prof, s, KC_EW);

@@ -901,6 +901,101 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
   if (tid == 0) *ticket = 0;
 }
 
+// ----------------------------------------------------------------- K6+K7+K8 fused (one GPU)
+// r_J = src_J - E_l z1 ; s = W_l^H r_J ; t = G_l s ; r_J += W_l t in ONE
+// cooperative launch: the last CTA to finish the W^H partials reduces them in
+// CTA order, forms t = G_l s and publishes it with a release flag
+// (epoch); every CTA waits for it (all CTAs are co-resident) and adds W_l t to
+// its rows.  Saves the second launch and its tail on the latency-bound levels.
+template <typename T>
+__global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const int64_t *__restrict__ Eptr,
+                                             const int32_t *__restrict__ Ecol, const T *__restrict__ Eval,
+                                             const T *__restrict__ z, const T *__restrict__ zh, int64_t nloc,
+                                             const T *src, T *dst, const T *__restrict__ W, int64_t ldw, int k,
+                                             const T *__restrict__ G, T *__restrict__ partial, unsigned *ticket,
+                                             T *sout, int *flag, int epoch, const int *__restrict__ done) {
+  if (done && *done) return;
+  __shared__ T sv[256];
+  __shared__ T st[64];
+  __shared__ bool amlast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T acc[EW_NACC];
+#pragma unroll
+  for (int a = 0; a < EW_NACC; ++a) acc[a] = dzero<T>();
+  const int64_t ntiles = (s + 255) / 256;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * 256 + tid;
+    T v = dzero<T>();
+    if (i < s) {
+      T e = dzero<T>();
+      for (int64_t p = Eptr[i]; p < Eptr[i + 1]; ++p) {
+        const int64_t c = Ecol[p];
+        e += Eval[p] * (c < nloc ? z[c] : zh[c - nloc]);
+      }
+      v = (src ? src[rowbase + i] : dzero<T>()) - e;
+      dst[rowbase + i] = v;
+    }
+    sv[tid] = v;
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < EW_NACC; ++a) {
+      const int c = warp + 8 * a;
+      if (c < k) {
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          const int64_t ii = tile * 256 + rr * 32 + lane;
+          if (ii < s) acc[a] += dconj(W[c * ldw + ii]) * sv[rr * 32 + lane];
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < EW_NACC; ++a) {
+    const int c = warp + 8 * a;
+    T r = warp_sum(acc[a]);
+    if (lane == 0 && c < k) partial[(int64_t)c * gridDim.x + blockIdx.x] = r;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) amlast = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (amlast) {
+    __threadfence();
+    reduce_partials(partial, (int)gridDim.x, k, sout);             // s = W^H r_J
+    __syncthreads();
+    if (tid < k) {                                                 // t = G s
+      T t = dzero<T>();
+      for (int a = 0; a < k; ++a) t += G[(int64_t)a * k + tid] * ld_cg(sout + a);
+      sout[64 + tid] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      *ticket = 0;
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+    }
+  }
+  if (tid == 0) {
+    int f;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(flag) : "memory");
+      if (f != epoch) __nanosleep(64);
+    } while (f != epoch);
+  }
+  __syncthreads();
+  if (tid < k) st[tid] = ld_cg(sout + 64 + tid);
+  __syncthreads();
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {  // r_J += W t
+    const int64_t i = tile * 256 + tid;
+    if (i < s) {
+      T a = dzero<T>();
+      for (int c = 0; c < k; ++c) a += ld_nc(W + c * ldw + i) * st[c];
+      dst[rowbase + i] = ld_cg(dst + rowbase + i) + a;
+    }
+  }
+}
+
 // ----------------------------------------------------------------- K8
 // r_J += W_l (G_l s): the k x k product G_l s is formed redundantly by every
 // CTA in its prologue, G_l column-major.
