@@ -326,7 +326,7 @@ struct Engine {
   HostPlan<T> plan;
   int64_t n = 0, nnzA = 0;
   // SpMV (SELL-32 of Â)
-  int64_t nslices = 0, sell_padded = 0;
+  int64_t nslices = 0, sell_padded = 0, sell_wmax = 0;
   const int64_t *sell_off = nullptr;
   const int32_t *sell_col = nullptr;
   const D *sell_val = nullptr;
@@ -516,6 +516,7 @@ void Engine<T>::upload(cudaStream_t s) {
     off[sl + 1] = off[sl] + 32 * w;
   }
   sell_padded = off[nslices];
+  for (int64_t sl = 0; sl < nslices; ++sl) sell_wmax = std::max<int64_t>(sell_wmax, (off[sl + 1] - off[sl]) / 32);
   std::vector<int32_t> col(sell_padded, -1);
   std::vector<T> val(sell_padded, T(0));
   for (int64_t row = 0; row < n; ++row) {
@@ -760,6 +761,18 @@ template <typename T>
 void Engine<T>::spmv(const D *x, D *y, int mode, const D *b, const int *doneflag) {
   exchange(hA, x, doneflag);                                     // exterior columns (Note N P:L59-61)
   Timed t(ctx->prof, ctx->stream, KC_SPMV);
+  if (sell_wmax <= 8) {                                           // 7-point / 5-point stencils and similar
+    constexpr int SPW = 2;
+    const int g2 = (int)std::max<int64_t>((nslices + 8 * SPW - 1) / (8 * SPW), 1);
+    if (hA.nrecv > 0)
+      k_spmv_sell2<D, true, SPW, 8><<<g2, 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, hA.rbuf, y,
+                                                                 mode, b, doneflag);
+    else
+      k_spmv_sell2<D, false, SPW, 8><<<g2, 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, hA.rbuf, y,
+                                                                  mode, b, doneflag);
+    CK(cudaGetLastError());
+    return;
+  }
   const int grid = (int)((nslices + 7) / 8);
   if (hA.nrecv > 0)
     k_spmv_sell<D, true><<<std::max(grid, 1), 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, hA.rbuf,

@@ -109,6 +109,50 @@ __global__ void __launch_bounds__(256) k_spmv_sell(int64_t n, int64_t nslices, c
   if (row < n) y[row] = mode ? b[row] - acc : acc;
 }
 
+// SELL-32 SpMV with more loads in flight: a warp takes SPW consecutive slices
+// of width <= WM, issues all their column and value loads, then all x gathers
+// (the gathers depend on the columns, so batching both levels is what hides
+// the latency; one slice per warp left the kernel at 57 % of HBM).
+template <typename T, bool HALO, int SPW, int WM>
+__global__ void __launch_bounds__(256) k_spmv_sell2(int64_t n, int64_t nslices, const int64_t *__restrict__ off,
+                                                    const int32_t *__restrict__ col, const T *__restrict__ val,
+                                                    const T *__restrict__ x, const T *__restrict__ xh, T *__restrict__ y,
+                                                    int mode, const T *__restrict__ b, const int *__restrict__ done) {
+  if (done && *done) return;
+  const int64_t s0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * SPW;
+  if (s0 >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  int c[SPW][WM];
+  T v[SPW][WM];
+#pragma unroll
+  for (int q = 0; q < SPW; ++q) {
+    const int64_t s = s0 + q;
+    const int64_t o = s < nslices ? off[s] : 0;
+    const int w = s < nslices ? (int)((off[s + 1] - o) >> 5) : 0;
+#pragma unroll
+    for (int e = 0; e < WM; ++e) {
+      c[q][e] = e < w ? __ldg(col + o + 32 * e + lane) : -1;
+      v[q][e] = e < w ? ld_nc(val + o + 32 * e + lane) : dzero<T>();
+    }
+  }
+  T xv[SPW][WM];
+#pragma unroll
+  for (int q = 0; q < SPW; ++q)
+#pragma unroll
+    for (int e = 0; e < WM; ++e) {
+      const int cc = c[q][e];
+      xv[q][e] = cc < 0 ? dzero<T>() : ((!HALO || cc < n) ? ld_nc(x + cc) : ld_nc(xh + (cc - n)));
+    }
+#pragma unroll
+  for (int q = 0; q < SPW; ++q) {
+    T acc = dzero<T>();
+#pragma unroll
+    for (int e = 0; e < WM; ++e) acc += v[q][e] * xv[q][e];
+    const int64_t row = (s0 + q) * 32 + lane;
+    if (row < n) y[row] = mode ? b[row] - acc : acc;
+  }
+}
+
 // halo send buffer: buf[i] = src[idx[i]]
 template <typename T>
 __global__ void k_gather_idx(int64_t n, const int *__restrict__ idx, const T *__restrict__ src, T *__restrict__ buf,
