@@ -907,19 +907,29 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
   };
   static const bool old_gs = getenv("GEMSLR_OLD_GS") != nullptr;
   auto go2 = [&](auto kern) {
-    const int grid = grid_for((nn + 255) / 256, ncols <= 32 && sizeof(D) == 8 ? 2 : 1);
+    const int grid = grid_for((nn + 255) / 256, ncols * (int)sizeof(D) <= 256 ? 2 : 1);
     kern<<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv, doneflag);
   };
   bool done2 = false;
-  if (!old_gs && ncols <= 32) {
-    go2(k_gs2<D, 32>);
+  if (!old_gs) {
+    // measured on C5 (ncu, per pass): the warp-tile kernel sized to the column
+    // count up to 32 columns (≈ 90 % of HBM), the column-split k_gs from 33 to
+    // 48, the half-warp k_gs2h above (k_gs <1,13> is 2x slower there)
     done2 = true;
-  } else if constexpr (sizeof(D) == 8) {
-    if (!old_gs && ncols <= 64) {
-      const int grid = grid_for((nn + 127) / 128, 2);
-      k_gs2h<D><<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv,
-                                               doneflag);
-      done2 = true;
+    if (ncols <= 8) go2(k_gs2<D, 8>);
+    else if (ncols <= 16) go2(k_gs2<D, 16>);
+    else if (ncols <= 24) go2(k_gs2<D, 24>);
+    else if (ncols <= 32) go2(k_gs2<D, 32>);
+    else if constexpr (sizeof(D) == 8) {
+      if (ncols > 48 && ncols <= 64) {
+        const int grid = grid_for((nn + 127) / 128, 2);
+        k_gs2h<D><<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv,
+                                                 doneflag);
+      } else {
+        done2 = false;
+      }
+    } else {
+      done2 = false;
     }
   }
   if (done2) {

@@ -1197,7 +1197,7 @@ __global__ void __launch_bounds__(256, NC * sizeof(T) > 256 ? 1 : 2) k_gs2(int64
                                               int dot, const T *__restrict__ h_in, T *__restrict__ partial,
                                               unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
   if (done && *done) return;
-  constexpr int NCH = NC / 32;
+  constexpr int NCH = (NC + 31) / 32;                              // 32-column butterfly chunks
   __shared__ T sh[NC];
   __shared__ T red[8][NC + 1];
   __shared__ bool amlast;
@@ -1221,7 +1221,7 @@ __global__ void __launch_bounds__(256, NC * sizeof(T) > 256 ? 1 : 2) k_gs2(int64
 #pragma unroll
       for (int c = 0; c < NC; c += 2) {
         u0 += v[c] * sh[c];
-        u1 += v[c + 1] * sh[c + 1];
+        if (c + 1 < NC) u1 += v[c + 1 < NC ? c + 1 : 0] * sh[c + 1 < NC ? c + 1 : 0];
       }
       wi = wi - (u0 + u1);
       if (ok) w[r] = wi;
@@ -1232,7 +1232,7 @@ __global__ void __launch_bounds__(256, NC * sizeof(T) > 256 ? 1 : 2) k_gs2(int64
       for (int q = 0; q < NCH; ++q) {
         T x[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) x[k] = dconj(v[32 * q + k]) * wi;
+        for (int k = 0; k < 32; ++k) x[k] = (32 * q + k < NC) ? dconj(v[32 * q + k < NC ? 32 * q + k : 0]) * wi : dzero<T>();
         tbfly32(x, lane);
         acc[q] += x[0];
       }
@@ -1242,7 +1242,8 @@ __global__ void __launch_bounds__(256, NC * sizeof(T) > 256 ? 1 : 2) k_gs2(int64
   const int nres = dot ? ncols + 1 : 1;
   nrm = warp_sum(nrm);
 #pragma unroll
-  for (int q = 0; q < NCH; ++q) red[warp][32 * q + lane] = acc[q];
+  for (int q = 0; q < NCH; ++q)
+    if (32 * q + lane < NC) red[warp][32 * q + lane] = acc[q];
   if (lane == 0) {
     T t = dzero<T>();
     if constexpr (sizeof(T) == sizeof(double)) t = nrm; else t = T{nrm, 0.0};
