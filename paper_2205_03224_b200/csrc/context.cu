@@ -1317,13 +1317,10 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
       gs_pass(V, ldv, n, j + 1, w, 1, 1, res1, res2, 8, done);    // w -= V h ; h2 = V^H w
       gs_pass(V, ldv, n, j + 1, w, 1, 0, res2, res3, 9, done);    // w -= V h2 ; ||w||^2
       {
-        Timed t(ctx->prof, s, KC_FGM);
-        k_fgmres_col<D><<<1, 32, 0, s>>>(f, m, j, res1, res2, res3);
+        Timed t(ctx->prof, s, KC_FGM);                           // Givens column + v_{j+1} = w / h_{j+1}
+        k_fgmres_scale<D><<<grid_for((n + 255) / 256, 4), 256, 0, s>>>(f, m, j, res1, res2, res3, n, w,
+                                                                       V + (size_t)(j + 1) * ldv);
         CK(cudaGetLastError());
-      }
-      {
-        Timed t(ctx->prof, s, KC_UTIL);
-        k_scale<D><<<grid_for((n + 255) / 256, 4), 256, 0, s>>>(n, w, V + (size_t)(j + 1) * ldv, dbl + 2, done);
       }
       // the done flag of iteration j reaches pinned host memory asynchronously;
       // the host reads it two iterations later, so the GPU always has the next

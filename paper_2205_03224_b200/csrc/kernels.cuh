@@ -1375,10 +1375,8 @@ struct FgmDev {
 };
 
 template <typename T>
-__global__ void k_fgmres_col(FgmDev<T> f, int m, int j, const T *__restrict__ res1, const T *__restrict__ res2,
-                             const T *__restrict__ res3) {
-  if (*f.done) return;
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ inline void fgmres_col_body(FgmDev<T> f, int m, int j, const T *__restrict__ res1, const T *__restrict__ res2,
+                                       const T *__restrict__ res3) {
   T *Hj = f.H + (int64_t)j * (m + 1);
   double eta2, hn2;
   if constexpr (sizeof(T) == sizeof(double)) { eta2 = res1[j + 1]; hn2 = res3[0]; }
@@ -1422,6 +1420,30 @@ __global__ void k_fgmres_col(FgmDev<T> f, int m, int j, const T *__restrict__ re
   f.hist[its] = est / f.dbl[0];
   f.dbl[2] = hnext > 0 ? 1.0 / hnext : 0.0;
   if (est <= f.dbl[1] * f.dbl[0] || hnext <= 1e-14 * eta || its >= f.ints[2] || j + 1 >= m) *f.done = 1;
+}
+
+template <typename T>
+__global__ void k_fgmres_col(FgmDev<T> f, int m, int j, const T *__restrict__ res1, const T *__restrict__ res2,
+                             const T *__restrict__ res3) {
+  if (*f.done) return;
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  fgmres_col_body(f, m, j, res1, res2, res3);
+}
+
+// The Givens column (thread 0 of CTA 0) and v_{j+1} = w / h_{j+1} (every CTA;
+// h_{j+1} = ||w|| is res3[0], known to all) in one launch.
+template <typename T>
+__global__ void __launch_bounds__(256) k_fgmres_scale(FgmDev<T> f, int m, int j, const T *__restrict__ res1,
+                                                      const T *__restrict__ res2, const T *__restrict__ res3, int64_t n,
+                                                      const T *__restrict__ w, T *__restrict__ vnext) {
+  if (*f.done) return;
+  double hn2;
+  if constexpr (sizeof(T) == sizeof(double)) hn2 = res3[0]; else hn2 = res3[0].x;
+  const double hnext = sqrt(hn2 > 0 ? hn2 : 0.0);
+  const double sc = hnext > 0 ? 1.0 / hnext : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) fgmres_col_body(f, m, j, res1, res2, res3);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    vnext[i] = dscale(w[i], sc);
 }
 
 // ----------------------------------------------------------------- utilities
