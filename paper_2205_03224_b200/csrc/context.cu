@@ -341,8 +341,7 @@ struct Engine {
   // workspace
   D *r = nullptr, *tmp = nullptr, *tvec = nullptr, *partial = nullptr, *res = nullptr;
   unsigned *tickets = nullptr;
-  int *ewflag = nullptr;             // release flag of k_ewx (epoch counter)
-  int ew_epoch = 0;
+  int *ewflag = nullptr;             // k_ewx generation counter (device-side)
   size_t partial_cap = 0;
   // Krylov workspace (lazy)
   int kry_m = -1;
@@ -355,8 +354,14 @@ struct Engine {
   D *xb = nullptr, *bb = nullptr;   // host-path staging
   int *hflags = nullptr;             // pinned: done flag of every iteration of a cycle (async D2H)
   int hflags_cap = 0;
+  std::vector<cudaGraphExec_t> graphs;   // FGMRES iteration j captured once (one GPU)
+  int graph_m = -1;
+  const D *graph_V = nullptr;
+  cudaStream_t cap_stream = nullptr;
   ~Engine() {
     if (hflags) cudaFreeHost(hflags);
+    for (auto &ge : graphs) if (ge) cudaGraphExecDestroy(ge);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
   }
   double setup_host_s = 0, setup_dev_s = 0, arnoldi_s = 0;
 
@@ -806,17 +811,16 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
           max_ctas = std::max(1, per) * kNumSM;
         }
         const int grid = (int)std::min<int64_t>((std::max<int64_t>(d.s, 1) + 255) / 256, max_ctas);
-        ++ew_epoch;
         int64_t a0 = d.s, a1 = d.o1, a5 = n, a11 = d.ldw;
         const int64_t *a2 = d.E.ptr;
         const int32_t *a3 = d.E.col;
         const D *a4 = d.E.val, *zz = out, *zh = hE[l].rbuf, *sr = src, *Wp = d.W, *Gp = d.G;
         D *ds = r, *pt = partial, *so = tvec;
-        int kk = d.k, ep = ew_epoch;
+        int kk = d.k;
         unsigned *tk = tickets + 0;
         int *fl = ewflag;
         const int *dn = doneflag;
-        void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &ep, &dn};
+        void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &dn};
         CK(cudaLaunchCooperativeKernel((const void *)k_ewx<D>, dim3(grid), dim3(256), args, 0, s));
         continue;
       }
@@ -1308,19 +1312,78 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
       hflags_cap = m;
     }
     int j = 0;
-    for (j = 0; j < m; ++j) {
-      D *vj = V + (size_t)j * ldv;
-      D *zj = Z + (size_t)j * ldv;
+    // one FGMRES iteration: every launch is on ctx->stream with fixed buffers,
+    // so iteration j can be captured once as a CUDA graph and replayed
+    auto iteration = [&](int jj) {
+      cudaStream_t st = ctx->stream;
+      D *vj = V + (size_t)jj * ldv;
+      D *zj = Z + (size_t)jj * ldv;
       apply_from(0, vj, zj, done);                                // Z_j = M^{-1} V_j
       spmv(zj, w, 0, nullptr, done);                              // w = A Z_j
-      gs_pass(V, ldv, n, j + 1, w, 0, 1, nullptr, res1, 7, done); // h = V^H w, ||w||^2
-      gs_pass(V, ldv, n, j + 1, w, 1, 1, res1, res2, 8, done);    // w -= V h ; h2 = V^H w
-      gs_pass(V, ldv, n, j + 1, w, 1, 0, res2, res3, 9, done);    // w -= V h2 ; ||w||^2
+      gs_pass(V, ldv, n, jj + 1, w, 0, 1, nullptr, res1, 7, done);  // h = V^H w, ||w||^2
+      gs_pass(V, ldv, n, jj + 1, w, 1, 1, res1, res2, 8, done);     // w -= V h ; h2 = V^H w
+      gs_pass(V, ldv, n, jj + 1, w, 1, 0, res2, res3, 9, done);     // w -= V h2 ; ||w||^2
       {
-        Timed t(ctx->prof, s, KC_FGM);                           // Givens column + v_{j+1} = w / h_{j+1}
-        k_fgmres_scale<D><<<grid_for((n + 255) / 256, 4), 256, 0, s>>>(f, m, j, res1, res2, res3, n, w,
-                                                                       V + (size_t)(j + 1) * ldv);
+        Timed t(ctx->prof, st, KC_FGM);                          // Givens column + v_{j+1} = w / h_{j+1}
+        k_fgmres_scale<D><<<grid_for((n + 255) / 256, 4), 256, 0, st>>>(f, m, jj, res1, res2, res3, n, w,
+                                                                        V + (size_t)(jj + 1) * ldv);
         CK(cudaGetLastError());
+      }
+    };
+    static const bool no_graph = getenv("GEMSLR_NO_GRAPH") != nullptr;
+    const bool use_graph = !no_graph && plan.nranks == 1 && !ctx->prof.on;
+    if (use_graph && (graph_m != m || graph_V != V)) {
+      for (auto &ge : graphs) if (ge) cudaGraphExecDestroy(ge);
+      graphs.assign(m, nullptr);
+      graph_m = m;
+      graph_V = V;
+    }
+    auto capture = [&](int jj) {                                 // capture on a private stream, replay on ours
+      if (!cap_stream) CK(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+      cudaStream_t user = ctx->stream;
+      ctx->stream = cap_stream;
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeRelaxed));
+      try {
+        iteration(jj);
+      } catch (...) {
+        cudaStreamEndCapture(cap_stream, &g);
+        if (g) cudaGraphDestroy(g);
+        ctx->stream = user;
+        throw;
+      }
+      CK(cudaStreamEndCapture(cap_stream, &g));
+      ctx->stream = user;
+      CK(cudaGraphInstantiate(&graphs[jj], g, 0));
+      cudaGraphDestroy(g);
+    };
+    if (use_graph)                                                // all m iterations captured before the first runs
+      for (int jj = 0; jj < m; ++jj)
+        if (!graphs[jj]) capture(jj);
+    for (j = 0; j < m; ++j) {
+      if (use_graph) {
+        if (!graphs[j]) {                                         // (not reached: captured above)
+          if (!cap_stream) CK(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+          cudaStream_t user = ctx->stream;
+          ctx->stream = cap_stream;
+          cudaGraph_t g = nullptr;
+          CK(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeRelaxed));
+          try {
+            iteration(j);
+          } catch (...) {
+            cudaStreamEndCapture(cap_stream, &g);
+            if (g) cudaGraphDestroy(g);
+            ctx->stream = user;
+            throw;
+          }
+          CK(cudaStreamEndCapture(cap_stream, &g));
+          ctx->stream = user;
+          CK(cudaGraphInstantiate(&graphs[j], g, 0));
+          cudaGraphDestroy(g);
+        }
+        CK(cudaGraphLaunch(graphs[j], s));
+      } else {
+        iteration(j);
       }
       // the done flag of iteration j reaches pinned host memory asynchronously;
       // the host reads it two iterations later, so the GPU always has the next

@@ -951,17 +951,21 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
 // CTA order, forms t = G_l s and publishes it with a release flag
 // (epoch); every CTA waits for it (all CTAs are co-resident) and adds W_l t to
 // its rows.  Saves the second launch and its tail on the latency-bound levels.
+// The flag is a generation counter in device memory: every CTA reads it before
+// taking its ticket, the last CTA (which takes the final ticket, so after every
+// read) advances it — no host-side epoch, so the launch can live in a CUDA graph.
 template <typename T>
 __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const int64_t *__restrict__ Eptr,
                                              const int32_t *__restrict__ Ecol, const T *__restrict__ Eval,
                                              const T *__restrict__ z, const T *__restrict__ zh, int64_t nloc,
                                              const T *src, T *dst, const T *__restrict__ W, int64_t ldw, int k,
                                              const T *__restrict__ G, T *__restrict__ partial, unsigned *ticket,
-                                             T *sout, int *flag, int epoch, const int *__restrict__ done) {
+                                             T *sout, int *flag, const int *__restrict__ done) {
   if (done && *done) return;
   __shared__ T sv[256];
   __shared__ T st[64];
   __shared__ bool amlast;
+  __shared__ int gen0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   T acc[EW_NACC];
 #pragma unroll
@@ -1002,8 +1006,14 @@ __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const i
   }
   __threadfence();
   __syncthreads();
-  if (tid == 0) amlast = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  if (tid == 0) {
+    int g;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(g) : "l"(flag) : "memory");
+    gen0 = g;
+    amlast = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
   __syncthreads();
+  const int epoch = gen0 + 1;
   if (amlast) {
     __threadfence();
     reduce_partials(partial, (int)gridDim.x, k, sout);             // s = W^H r_J
