@@ -50,10 +50,12 @@ def launches(path, out):
     cls = {}
     if tri and len(tri) % 7 == 0:
         names = ['down_l0', 'down_l1', 'down_l2', 'last', 'up_l2', 'up_l1', 'up_l0']
+        import statistics
         for i, nm in enumerate(names):
-            sel = tri[i::7]
-            cls[nm] = (sum(t for t, _ in sel) / len(sel), sum(b for _, b in sel) / len(sel))
-        lines.append("\nTriangular-solve launches by position in the apply (mean per launch):\n")
+            sel = tri[i::7]                              # median: the last iterations of a solve exit early (done flag)
+            cls[nm] = (statistics.median(t for t, _ in sel), statistics.median(b for _, b in sel))
+        lines.append("\nTriangular-solve launches by position in the apply (median per launch; kernels of the "
+                     "iterations queued after the done flag exit at once):\n")
         lines.append("| launch | µs | DRAM MB |\n|---|---|---|")
         for nm, (t, b) in cls.items():
             lines.append(f"| {nm} | {t / 1e3:.1f} | {b / 1e6:.1f} |")
