@@ -69,6 +69,9 @@ typedef struct {
   int cluster_ctas;         /* CTAs per thread-block cluster in the triangular solves; 0 = automatic        */
   int tri_kernel;           /* triangular-solve kernel: 0 = automatic (register-prefetched k_tri_reg where
                                the setup proves it applies), 1 = TMA-staged k_tri_pipe, 2 = level kernel     */
+  double ilu_shift;         /* complex diagonal shift of the block ILUs: sigma = i*ilu_shift*sum|a_ii|/n added
+                               to every B_l and C_last block before factoring (the paper uses
+                               0.05); 0 = off; GEMSLR_C128 only (INVALID_ARG for GEMSLR_F64)               */
 } gemslr_params;
 
 typedef struct gemslr_ctx gemslr_ctx;

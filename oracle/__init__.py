@@ -45,7 +45,7 @@ def lib():
         L.or_ilu_solve.argtypes = [vp, vp, vp]
         L.or_ilu_destroy.argtypes = [vp]
         L.or_precond_create.argtypes = [C.c_int, i64, vp, vp, vp, vp, C.c_int, vp, vp, vp, C.c_int, vp,
-                                        C.c_int, C.c_double, C.c_int, C.c_char_p, C.c_int]
+                                        C.c_int, C.c_double, C.c_int, C.c_double, C.c_char_p, C.c_int]
         L.or_precond_create.restype = vp
         L.or_precond_destroy.argtypes = [vp]
         L.or_precond_set_lowrank.argtypes = [vp, C.c_int, C.c_int, vp, vp]
@@ -145,9 +145,11 @@ class Precond:
       blocks      list of L int64 arrays of absolute block boundaries per level
       last_off    int64 array of absolute C_last block boundaries
     ilu: (kind, tau, lfil).  Factors are computed by the oracle itself.
+    shift: complex diagonal shift factor of the block ILUs, sigma = i*shift*sum|a_ii|/n
+    (reading Q33; complex problems only).
     """
 
-    def __init__(self, A, structure, ilu=(ILU0, 0.0, 0)):
+    def __init__(self, A, structure, ilu=(ILU0, 0.0, 0), shift=0.0):
         rp, ci, v, cplx = _csr_args(*as_csr(A))
         self.n = len(rp) - 1
         self.dtype = v.dtype
@@ -165,7 +167,7 @@ class Precond:
         kind, tau, lfil = ilu
         self.h = lib().or_precond_create(cplx, self.n, _p(rp), _p(ci), _p(v), _p(self.perm), self.L, _p(self.o),
                                          _p(nblk), _p(blk_off), len(last) - 1, _p(last), int(kind), float(tau),
-                                         int(min(lfil, 2**31 - 1)), err, 1024)
+                                         int(min(lfil, 2**31 - 1)), float(shift), err, 1024)
         if not self.h:
             raise RuntimeError(err.value.decode())
         self._keep = (rp, ci, v)

@@ -548,12 +548,34 @@ Csr<T> permute(const Csr<T> &A, const int64_t *perm) {
   return B;
 }
 
+// Complex diagonal shift of the ILU factorizations: "a complex
+// shift equal to 0.05 i Σ_i |A_ii| / n_A during the ILU factorization of the
+// on-diagonal blocks" — sigma = i * factor * Σ|a_ii| / n, added to the diagonal
+// of every block before it is factored (reading Q33: B_l blocks and the C_last
+// blocks; complex problems only).
+template <typename T> T shift_sigma(const Csr<T> &, double) { return T(0); }
+template <> zc shift_sigma<zc>(const Csr<zc> &A, double factor) {
+  if (factor == 0.0) return zc(0);
+  double s = 0;
+  for (int64_t i = 0; i < A.n; ++i)
+    for (int64_t p = A.ptr[i]; p < A.ptr[i + 1]; ++p)
+      if (A.col[p] == i) s += std::abs(A.val[p]);
+  return zc(0.0, factor * s / (double)A.n);
+}
+template <typename T>
+void add_diag(Csr<T> &B, T sigma) {
+  for (int64_t i = 0; i < B.n; ++i)
+    for (int64_t p = B.ptr[i]; p < B.ptr[i + 1]; ++p)
+      if (B.col[p] == i) B.val[p] += sigma;
+}
+
 template <typename T>
 Precond<T> *build_precond(int64_t n, const int64_t *rowptr, const int32_t *col, const void *val,
                           const int64_t *perm, int L, const int64_t *level_off,
                           const int32_t *nblk, const int64_t *blk_off, int nlast, const int64_t *last_off,
-                          int ilu_type, double tau, int lfil, std::string &err) {
+                          int ilu_type, double tau, int lfil, double shift, std::string &err) {
   Csr<T> A = make_csr<T>(n, rowptr, col, val);
+  const T sigma = shift_sigma<T>(A, shift);
   auto *P = new Precond<T>();
   P->N = n;
   P->L = L;
@@ -570,6 +592,7 @@ Precond<T> *build_precond(int64_t n, const int64_t *rowptr, const int32_t *col, 
     std::vector<Ilu<T>> f;
     for (int q = 0; q < nblk[l]; ++q) {
       Csr<T> B = submatrix(P->Ahat, b[q], b[q + 1], b[q], b[q + 1]);
+      add_diag(B, sigma);
       f.push_back(factor(B, ilu_type, tau, lfil, err));
       if (!err.empty()) { err += " (level " + std::to_string(l) + ", block " + std::to_string(q) + ")"; delete P; return nullptr; }
     }
@@ -580,6 +603,7 @@ Precond<T> *build_precond(int64_t n, const int64_t *rowptr, const int32_t *col, 
   P->last.assign(last_off, last_off + nlast + 1);
   for (int q = 0; q < nlast; ++q) {
     Csr<T> C = submatrix(P->Ahat, P->last[q], P->last[q + 1], P->last[q], P->last[q + 1]);
+    add_diag(C, sigma);
     P->lastfac.push_back(factor(C, ilu_type, tau, lfil, err));
     if (!err.empty()) { err += " (C_last block " + std::to_string(q) + ")"; delete P; return nullptr; }
   }
@@ -676,13 +700,13 @@ void or_ilu_destroy(void *hv) {
 void *or_precond_create(int cplx, int64_t n, const int64_t *rowptr, const int32_t *col, const void *val,
                         const int64_t *perm, int L, const int64_t *level_off,
                         const int32_t *nblk, const int64_t *blk_off, int nlast, const int64_t *last_off,
-                        int ilu_type, double tau, int lfil, char *err, int errcap) {
+                        int ilu_type, double tau, int lfil, double shift, char *err, int errcap) {
   std::string e;
   auto *h = new Handle();
   h->is_cplx = cplx;
   h->perm.assign(perm, perm + n);
-  if (cplx) h->p = build_precond<zc>(n, rowptr, col, val, perm, L, level_off, nblk, blk_off, nlast, last_off, ilu_type, tau, lfil, e);
-  else h->p = build_precond<double>(n, rowptr, col, val, perm, L, level_off, nblk, blk_off, nlast, last_off, ilu_type, tau, lfil, e);
+  if (cplx) h->p = build_precond<zc>(n, rowptr, col, val, perm, L, level_off, nblk, blk_off, nlast, last_off, ilu_type, tau, lfil, shift, e);
+  else h->p = build_precond<double>(n, rowptr, col, val, perm, L, level_off, nblk, blk_off, nlast, last_off, ilu_type, tau, lfil, shift, e);
   if (!h->p) { set_err(err, errcap, e); delete h; return nullptr; }
   return h;
 }

@@ -1707,6 +1707,7 @@ static gemslr_status do_setup(gemslr_ctx *c, std::unique_ptr<Engine<T>> &E, int6
   opt.tau = prm->ilut_drop;
   opt.lfil = prm->ilut_fill > 0 ? prm->ilut_fill : 10;
   opt.last_blocks = prm->last_blocks;
+  opt.shift = prm->ilu_shift;
   opt.nranks = c->comm.nranks;
   opt.rank = c->comm.rank;
   if (c->coord_dim > 0 && c->coords_src) {
@@ -1746,6 +1747,8 @@ gemslr_status gemslr_setup(gemslr_ctx *c, gemslr_dtype dtype, int64_t n, const i
       (prm->ilu != GEMSLR_ILU0 && prm->ilu != GEMSLR_ILUT) || prm->ilut_drop < 0)
     return fail(c, GEMSLR_ERR_INVALID_ARG, "levels < 1, subdomains < 1, rank < 0 or bad dtype/ilu");
   if (2 * prm->rank + 2 > GS_MAXC) return fail(c, GEMSLR_ERR_INVALID_ARG, "rank > 50 not supported (cycle 2k <= 102)");
+  if (prm->ilu_shift != 0.0 && (dtype != GEMSLR_C128 || !(prm->ilu_shift == prm->ilu_shift)))
+    return fail(c, GEMSLR_ERR_INVALID_ARG, "ilu_shift needs complex arithmetic (GEMSLR_C128)");
   c->params = *prm;
   gemslr_status st = guarded(c, [&]() -> gemslr_status {
     if (dtype == GEMSLR_F64) return do_setup<double>(c, c->ed, n, rowptr, colidx, values, prm);

@@ -56,8 +56,29 @@ Csr<T> sub(const Csr<T> &A, int64_t r0, int64_t r1, int64_t c0, int64_t c1, bool
   return S;
 }
 
+// Complex diagonal shift during the block ILUs ("a complex shift
+// equal to 0.05 i Σ_i |A_ii| / n_A during the ILU factorization of the
+// on-diagonal blocks"): sigma = i * opt.shift * Σ|a_ii| / n, added to the
+// diagonal of every B_l block and every C_last block before factoring (Q33).
+template <typename T> T ilu_sigma(const Csr<T> &, double) { return T(0); }
+template <> zc ilu_sigma<zc>(const Csr<zc> &A, double factor) {
+  if (factor == 0.0) return zc(0);
+  double s = 0;
+  for (int64_t i = 0; i < A.n; ++i)
+    for (int64_t p = A.ptr[i]; p < A.ptr[i + 1]; ++p)
+      if (A.col[p] == i) s += std::abs(A.val[p]);
+  return zc(0.0, factor * s / (double)A.n);
+}
 template <typename T>
-bool factor_blocks(const Csr<T> &Ahat, const std::vector<int64_t> &bl, const SetupOptions &opt,
+void shift_diag(Csr<T> &B, T sigma) {
+  if (sigma == T(0)) return;
+  for (int64_t i = 0; i < B.n; ++i)
+    for (int64_t p = B.ptr[i]; p < B.ptr[i + 1]; ++p)
+      if (B.col[p] == i) B.val[p] += sigma;
+}
+
+template <typename T>
+bool factor_blocks(const Csr<T> &Ahat, const std::vector<int64_t> &bl, const SetupOptions &opt, T sigma,
                    std::vector<Factor<T>> &out, const std::string &where, Error &err) {
   const int nb = (int)bl.size() - 1;
   out.assign(nb, Factor<T>());
@@ -66,6 +87,7 @@ bool factor_blocks(const Csr<T> &Ahat, const std::vector<int64_t> &bl, const Set
 #pragma omp parallel for schedule(dynamic, 1)
   for (int q = 0; q < nb; ++q) {
     Csr<T> B = sub(Ahat, bl[q], bl[q + 1], bl[q], bl[q + 1], true);
+    shift_diag(B, sigma);
     ok[q] = opt.ilu == 0 ? ilu0(B, out[q], errs[q]) : ilut(B, opt.tau, opt.lfil, out[q], errs[q]);
   }
   for (int q = 0; q < nb; ++q)
@@ -158,6 +180,7 @@ bool build_host_plan(int64_t n, const int64_t *rowptr, const int32_t *colidx, co
   const Structure &st = plan.st;
   plan.Ahat = permute(n, rowptr, colidx, vals, st);
   const Csr<T> &Ah = plan.Ahat;
+  const T sigma = ilu_sigma<T>(Ah, opt.shift);                     // Σ|a_ii| is invariant under the permutation
   const int L = st.L;
   plan.nranks = G;
   plan.rank = me;
@@ -274,6 +297,7 @@ bool build_host_plan(int64_t n, const int64_t *rowptr, const int32_t *colidx, co
       for (int t = 0; t < no; ++t) {
         const int q = own_q[t];
         Csr<T> B = sub(Ah, bl[q], bl[q + 1], bl[q], bl[q + 1], true);
+        shift_diag(B, sigma);
         ok[t] = opt.ilu == 0 ? ilu0(B, f2[t], errs[t]) : ilut(B, opt.tau, opt.lfil, f2[t], errs[t]);
       }
       for (int t = 0; t < no; ++t)
@@ -296,7 +320,7 @@ bool build_host_plan(int64_t n, const int64_t *rowptr, const int32_t *colidx, co
     plan.F[l] = local_rows(plan.lo[l], plan.lo[l + 1], st.o[l + 1], n, plan.hF[l], G > 1);
   }
   // C_last: every rank factors and solves all blocks (replicated)
-  if (!factor_blocks(Ah, st.last, opt, plan.lastfac, "C_last", err)) return false;
+  if (!factor_blocks(Ah, st.last, opt, sigma, plan.lastfac, "C_last", err)) return false;
   for (auto &f : plan.lastfac) plan.fac_nnz += f.L.nnz() + f.U.nnz();
   std::vector<int64_t> rel;
   for (int64_t v : st.last) rel.push_back(v - st.o[L]);

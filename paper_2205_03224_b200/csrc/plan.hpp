@@ -218,6 +218,7 @@ struct SetupOptions {
   int levels = 1, p = 1, ilu = 0, lfil = 10, last_blocks = 0;
   int nranks = 1, rank = 0;
   double tau = 1e-3;
+  double shift = 0.0;                           // complex ILU shift factor, complex only
   int coord_dim = 0;
   const double *coords = nullptr;               // n x coord_dim (optional)
 };

@@ -124,10 +124,11 @@ def convdiff_upwind(dims, beta=(20.0, 20.0, 20.0), name=None):
                     name=name or f"convdiff{nd}d_{'x'.join(map(str, dims))}")
 
 
-def helmholtz_shifted(dims, omega2h2=0.1, name=None):
-    """-Δu - (ω² + 0.5iω²)u, h^2-scaled: diag 2d - ω²h²(1+0.5i) (reading Q19), c128."""
+def helmholtz_shifted(dims, omega2h2=0.1, damping=0.5, name=None):
+    """-Δu - (ω² + damping·iω²)u, h^2-scaled: diag 2d - ω²h²(1 + damping·i) (reading Q19;
+    C4 is ω²h² = 0.1, damping 0.5), c128."""
     nd = len(dims)
-    diag = complex(2.0 * nd - omega2h2, -0.5 * omega2h2)
+    diag = complex(2.0 * nd - omega2h2, -damping * omega2h2)
     return _stencil(dims, diag, [-1.0 + 0j] * nd, [-1.0 + 0j] * nd, dtype=np.complex128,
                     name=name or f"helmholtz{nd}d_{'x'.join(map(str, dims))}")
 
@@ -176,13 +177,13 @@ def c5_dims(gpus: int):
             8: (256, 256, 256)}[gpus]
 
 
-def make_matrix(kind, dims):
+def make_matrix(kind, dims, **kw):
     if kind == "laplacian":
         return laplacian(dims)
     if kind == "convdiff":
         return convdiff_upwind(dims)
     if kind == "helmholtz":
-        return helmholtz_shifted(dims)
+        return helmholtz_shifted(dims, **kw)
     raise ValueError(kind)
 
 
@@ -197,7 +198,7 @@ def make_config(name, dims=None, seed=0, gpus=1, **overrides):
         dims = c5_dims(gpus) if name == "C5" else cfg["dims"]
         if name == "C5":
             cfg["subdomains"] = 32 * gpus
-    prob = make_matrix(cfg["kind"], dims)
+    prob = make_matrix(cfg["kind"], dims, **{k: cfg[k] for k in ("omega2h2", "damping") if k in cfg})
     prob.name = f"{name}:{prob.name}"
     if cfg["rhs"] == "manufactured":
         b, x_true = manufactured_rhs(prob, seed)

@@ -187,6 +187,32 @@ def test_trisolve_kernels(tmp_path, name, dims, over, tri_kernel, expect):
         assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
 
 
+def test_complex_shifted_ilu_NEXT3(tmp_path):
+    """C4 recipe with the paper's complex ILU shift 0.05 i sum|a_ii|/n:
+    apply parity against the oracle's own shifted factors, FGMRES iterations within ±1."""
+    prob, b, xt, prm = P.make_config("C4", dims=(16, 16, 14), subdomains=8, rank=6)
+    s = gm.Solver(prob.rowptr, prob.colidx, prob.values, prm["levels"], prm["subdomains"], prm["rank"],
+                  ilu=prm["ilu"], coords=prob.coords, device=0, ilu_shift=0.05)
+    d = s.export(str(tmp_path / "bundle"))
+    B = Bundle(d)
+    st = B.structure()
+    Pc = oracle.Precond(prob.scipy(), st, ilu=(oracle.ILUT, 1e-3, 10), shift=0.05)
+    for l in range(B.L):
+        lr = B.lowrank(l)
+        if lr is not None:
+            Pc.set_lowrank(l, lr[0], lr[2])
+    for seed in (2, 3):
+        r = P.rhs_vector(prob.n, True, seed)
+        assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
+    out = s.solve(to_dev(s, b[st["perm"]]), rtol=prm["rtol"], restart=prm["restart"])
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"])
+    assert out["status"] == 0 and abs(out["its"] - ref["its"]) <= 1, (out["its"], ref["its"])
+    with pytest.raises(gm.GemslrError):                    # real problems have no complex shift
+        p5, _, _, q5 = P.make_config("C5", dims=(8, 8, 8), subdomains=4, rank=2)
+        gm.Solver(p5.rowptr, p5.colidx, p5.values, q5["levels"], q5["subdomains"], q5["rank"], ilu=q5["ilu"],
+                  coords=p5.coords, device=0, ilu_shift=0.05)
+
+
 # ---------------------------------------------------------------- edge cases
 @pytest.mark.parametrize("kind", ["tiny1d", "p1", "fullrank", "early_stop", "random_bfs", "complex_bfs"])
 def test_edge_cases(tmp_path, kind):

@@ -204,6 +204,31 @@ def test_k0_apply_is_block_ldu_D5():
     assert np.linalg.norm(Pc.apply(b) - Minv @ b) <= 1e-12 * np.linalg.norm(Minv @ b)
 
 
+@pytest.mark.parametrize("shift", [0.05, 0.5])
+def test_complex_shifted_ilu_NEXT3(shift):
+    """Complex shift of the block ILUs: with exact factors (ILUT tau = 0,
+    lfil = inf) every block's L U equals B + sigma I, sigma = i*shift*sum|a_ii|/n_A — the
+    textbook LU of the shifted block — and shift 0 gives the unshifted factors."""
+    prob = P.helmholtz_shifted((7, 6, 5))
+    A = prob.scipy()
+    st = D.tiny_structure(A, prob.coords, 1, 4, nlast=2)
+    Ah = D.permute_matrix(A, st["perm"]).toarray()
+    sigma = 1j * shift * np.abs(A.diagonal()).sum() / A.shape[0]
+    Pc = oracle.Precond(A, st, ilu=(oracle.ILUT, 0.0, 1 << 30), shift=shift)
+    blocks = [(0, q, st["blocks"][0]) for q in range(len(st["blocks"][0]) - 1)]
+    blocks += [(1, q, st["last_off"]) for q in range(len(st["last_off"]) - 1)]
+    for l, q, bl in blocks:
+        a, c = bl[q], bl[q + 1]
+        Lq = Pc.factor(l, q, 0).toarray() + np.eye(c - a)
+        Uq = Pc.factor(l, q, 1).toarray()
+        B = Ah[a:c, a:c] + sigma * np.eye(c - a)
+        assert np.abs(Lq @ Uq - B).max() <= 1e-12 * np.abs(B).max()
+    P0 = oracle.Precond(A, st, ilu=(oracle.ILU0, 0.0, 0), shift=0.0)
+    P1 = oracle.Precond(A, st, ilu=(oracle.ILU0, 0.0, 0))
+    r = P.rhs_vector(prob.n, True, 4)
+    assert np.array_equal(P0.apply(r), P1.apply(r))
+
+
 def test_apply_linearity_D6_and_ghat_definition():
     prob = P.helmholtz_shifted((6, 6, 3))
     A = prob.scipy()
