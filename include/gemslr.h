@@ -158,6 +158,19 @@ gemslr_status gemslr_spmv(gemslr_ctx *ctx, const void *x_dev, void *y_dev);
  * solves).  Device pointers, local permuted layout, x != y. */
 gemslr_status gemslr_apply_precond(gemslr_ctx *ctx, const void *x_dev, void *y_dev);
 
+/* Several right-hand sides (NEXT-4; the paper's GPU motivation, P:L1285-1286,
+ * P:L1326-1330).  x_dev, y_dev: device, column-major n_local x nrhs blocks with
+ * leading dimension ld >= n_local (column c at x_dev + c*ld scalars), local
+ * permuted layout, x != y.  Results equal nrhs calls of the single-vector
+ * function (up to summation order).  The SpMV reads A once for all columns; the
+ * apply runs the triangular solves of up to GEMSLR_MAX_RHS columns in one
+ * launch per stage (the columns share the factor stream), the E/W coupling per
+ * column.  One GPU only (STATE with a communicator); INVALID_ARG for nrhs < 1
+ * or ld < n_local. */
+#define GEMSLR_MAX_RHS 8
+gemslr_status gemslr_spmv_multi(gemslr_ctx *ctx, const void *x_dev, void *y_dev, int nrhs, int64_t ld);
+gemslr_status gemslr_apply_precond_multi(gemslr_ctx *ctx, const void *x_dev, void *y_dev, int nrhs, int64_t ld);
+
 /* solve(b, x0, tol, restart) -> (x, iterations, residual history): right-
  * preconditioned FGMRES(restart) with CGS2 (DESIGN.md readings
  * Q14/Q15).  b_dev: device, local permuted layout; x_dev: in x0, out x.

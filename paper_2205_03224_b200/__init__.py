@@ -22,9 +22,16 @@ GEMSLR_OK, GEMSLR_NOT_CONVERGED = 0, 1
 STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "INVALID_ARG", -2: "BAD_CSR", -3: "PARTITION", -4: "ZERO_PIVOT",
           -5: "LOWRANK", -6: "STATE", -7: "CUDA", -8: "NCCL", -9: "OOM"}
 ABI_FUNCTIONS = ["gemslr_create", "gemslr_nccl_unique_id", "gemslr_create_dist", "gemslr_create_hostcomm", "gemslr_halo_plan", "gemslr_set_allocator", "gemslr_set_coordinates", "gemslr_setup", "gemslr_layout",
-                 "gemslr_spmv", "gemslr_apply_precond", "gemslr_solve", "gemslr_solve_host", "gemslr_to_local",
+                 "gemslr_spmv", "gemslr_apply_precond", "gemslr_spmv_multi", "gemslr_apply_precond_multi",
+                 "gemslr_solve", "gemslr_solve_host", "gemslr_to_local",
                  "gemslr_to_natural", "gemslr_export_setup", "gemslr_stats", "gemslr_profile", "gemslr_last_error",
                  "gemslr_destroy"]
+
+
+def torch_empty_like(X):
+    """an output block with the same (row) stride as X: the C-ABI takes one leading dimension"""
+    import torch
+    return torch.empty_strided(X.shape, X.stride(), dtype=X.dtype, device=X.device)
 
 
 class GemslrError(RuntimeError):
@@ -59,6 +66,8 @@ def lib():
         L.gemslr_layout.argtypes = [vp, C.POINTER(i64), vp]
         L.gemslr_spmv.argtypes = [vp, vp, vp]
         L.gemslr_apply_precond.argtypes = [vp, vp, vp]
+        L.gemslr_spmv_multi.argtypes = [vp, vp, vp, C.c_int, i64]
+        L.gemslr_apply_precond_multi.argtypes = [vp, vp, vp, C.c_int, i64]
         sargs = [vp, vp, vp, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_int), vp, C.c_int, C.POINTER(C.c_int),
                  C.POINTER(C.c_double)]
         L.gemslr_solve.argtypes = sargs
@@ -232,6 +241,28 @@ class Solver:
         y = self._vec() if y is None else self._dev(y)
         self._check(lib().gemslr_apply_precond(self.h, _ptr(x), _ptr(y)), "apply_precond")
         return y
+
+    def _block(self, X):
+        assert X.is_cuda and X.dtype == self.torch_dtype and X.dim() == 2 and X.shape[1] == self.n_local \
+            and X.stride(1) == 1, "blocks are CUDA tensors of shape (nrhs, n_local), rows contiguous"
+        return X
+
+    def spmv_multi(self, X, Y=None):
+        """Y[c] = A X[c] for every row c of the (nrhs, n_local) block X (A read once)."""
+        X = self._block(X)
+        Y = torch_empty_like(X) if Y is None else self._block(Y)
+        assert Y.stride(0) == X.stride(0), "X and Y need the same leading dimension"
+        self._check(lib().gemslr_spmv_multi(self.h, _ptr(X), _ptr(Y), X.shape[0], X.stride(0)), "spmv_multi")
+        return Y
+
+    def apply_precond_multi(self, X, Y=None):
+        """Y[c] = M^{-1} X[c] for every row c of the (nrhs, n_local) block X (NEXT-4)."""
+        X = self._block(X)
+        Y = torch_empty_like(X) if Y is None else self._block(Y)
+        assert Y.stride(0) == X.stride(0), "X and Y need the same leading dimension"
+        self._check(lib().gemslr_apply_precond_multi(self.h, _ptr(X), _ptr(Y), X.shape[0], X.stride(0)),
+                    "apply_precond_multi")
+        return Y
 
     def solve(self, b, x0=None, rtol=1e-8, restart=50, maxit=1000):
         b = self._dev(b)

@@ -281,7 +281,10 @@ struct StageDev {
   D *rhs_up = nullptr;             // UP right-hand sides (zero except the F_l rows)
   const int *fpos = nullptr, *frow = nullptr;
   int64_t nf = -1;                 // rows with F_l entries (-1: not set up, use k_pack_rhs)
-  int64_t lslices = 0;
+  int64_t lslices = 0, uslices = 0;
+  // several right-hand sides (NEXT-4): per-column packed buffers, mcap columns
+  D *mL = nullptr, *mU = nullptr, *mUp = nullptr;
+  int mcap = 0;
   int64_t nchunks = 0, far = 0, nearc = 0;
   int64_t nnz = 0;         // real stored nonzeros (L + U incl. diagonal)
   int64_t padded = 0;      // stored entries incl. padding
@@ -369,6 +372,14 @@ struct Engine {
   void exchange(HaloDev<D> &h, const D *src, const int *doneflag);
   void allreduce(D *buf, size_t count);
   void apply_from(int l0, const D *in, D *out, const int *doneflag);
+  // several right-hand sides (NEXT-4, one GPU): column-major n x nr blocks, leading dimension ld
+  D *rM = nullptr, *tmpM = nullptr;
+  int64_t multi_cap = 0;                                            // nr * ld of rM / tmpM
+  bool multi_ok() const;
+  void ensure_multi(int nr, int64_t ld);
+  void apply_multi(const D *in, D *out, int64_t ld, int nr);
+  void spmv_multi(const D *x, D *y, int64_t ld, int nr);
+  void ew_column(LevelDev<D> &d, int l, const D *src, const D *z, D *dst);
   void spmv(const D *x, D *y, int mode, const D *b, const int *doneflag);
   void ghat(int l, D *bufA, D *bufB);
   void build_lowrank(const gemslr_params &prm, unsigned long long seed);
@@ -452,6 +463,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     d.Rg.rhsL = P.get<D>(std::max<int64_t>(S.reg.lslices * 32, 1));
     d.lrow = P.upload<int>(S.Lp.slice_row, s);
     d.lslices = S.reg.lslices;
+    d.uslices = S.reg.uslices;
     d.rhs_up = P.get<D>(std::max<int64_t>(S.reg.lslices * 32, 1));
     CK(cudaMemsetAsync(d.rhs_up, 0, std::max<int64_t>(S.reg.lslices * 32, 1) * sizeof(D), s));
     d.Rg.mid = P.get<D>(std::max<int64_t>(S.reg.uslices * 32, 1));
@@ -659,8 +671,10 @@ struct FArgs {
 
 template <typename D>
 static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *rhs, D *x, D *tmp,
-                            const FArgs<D> &fa, const int *doneflag, int kc, int lvl = 0) {
+                            const FArgs<D> &fa, const int *doneflag, int kc, int lvl = 0, int nr = 1, int64_t ldx = 0) {
   if (S.nblk <= 0 || S.rows == 0) return;
+  if (nr > 1 && !(S.reg && S.mcap >= nr && (mode == TRI_DOWN || S.nf >= 0)))
+    throw Error{GEMSLR_ERR_STATE, "several right-hand sides need the register-prefetched trisolve"};
   const CsrDev<D> *F = fa.F;
   const int64_t Fbase = fa.Fbase;
   const int64_t *Fp = F ? F->ptr : nullptr;
@@ -671,17 +685,27 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
     constexpr int NW = sizeof(D) == 8 ? 15 : 7;   // (NW + 1) warps a multiple of 4: full register budget
     const size_t smem = reg_smem_bytes<D>(S.Rg.ring, S.Rg.max_slices);
     RegDev<D> Rg = S.Rg;
+    Rg.ldx = Rg.rsL = Rg.rsU = 0;
+    D *rL = const_cast<D *>(S.Rg.rhsL), *rUp = S.rhs_up;
+    if (nr > 1) {                                                 // per-column packed buffers
+      rL = S.mL;
+      rUp = S.mUp;
+      Rg.mid = S.mU;
+      Rg.ldx = ldx;
+      Rg.rsL = Rg.rsU = std::max(S.lslices, S.uslices) * 32;
+    }
+    Rg.rhsL = rL;
     {
       Timed tp(ctx->prof, ctx->stream, KC_PACK);
       if (mode == TRI_DOWN) {
         const int64_t np = S.lslices * 32;
-        k_pack_gather<D><<<grid_for((np + 255) / 256, 4), 256, 0, ctx->stream>>>(np, S.lrow, rhs, const_cast<D *>(S.Rg.rhsL),
-                                                                                doneflag);
+        k_pack_gather<D><<<dim3(grid_for((np + 255) / 256, 4), nr), 256, 0, ctx->stream>>>(np, S.lrow, rhs, rL, doneflag,
+                                                                                          ldx, Rg.rsL);
       } else if (S.nf >= 0) {
-        Rg.rhsL = S.rhs_up;
+        Rg.rhsL = rUp;
         if (S.nf > 0)
-          k_pack_f<D><<<grid_for((S.nf + 255) / 256, 4), 256, 0, ctx->stream>>>(S.nf, S.fpos, S.frow, Fp, Fc, Fv, x, fa.nloc,
-                                                                                fa.yh, fa.nh, fa.yl, S.rhs_up, doneflag);
+          k_pack_f<D><<<dim3(grid_for((S.nf + 255) / 256, 4), nr), 256, 0, ctx->stream>>>(
+              S.nf, S.fpos, S.frow, Fp, Fc, Fv, x, fa.nloc, fa.yh, fa.nh, fa.yl, rUp, doneflag, ldx, Rg.rsL);
       } else {
         k_pack_rhs<D><<<pgrid, 256, 0, ctx->stream>>>(S.rows, S.row0, S.P.lpos, const_cast<D *>(S.Rg.rhsL), nullptr, Fp, Fc,
                                                       Fv, Fbase, x, fa.nloc, fa.yh, fa.nh, fa.yl, doneflag);
@@ -701,7 +725,7 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
     Rg.dbg = (kc == KC_TRI_DOWN && lvl == g_tri_dbg_level) ? g_tri_dbg : nullptr;
     static const int reg_flags = getenv("GEMSLR_REG_FLAGS") ? atoi(getenv("GEMSLR_REG_FLAGS")) : 0;
     Rg.flags = reg_flags;
-    auto go = [&](auto kern) { kern<<<S.nblk, 32 * (NW + 1), smem, ctx->stream>>>(Rg, mode, x, tmp, doneflag); };
+    auto go = [&](auto kern) { kern<<<dim3(S.nblk, nr), 32 * (NW + 1), smem, ctx->stream>>>(Rg, mode, x, tmp, doneflag); };
     switch (S.reg_w) {
       case 4: go(k_tri_reg<D, 4, NW>); break;
       case 8: go(k_tri_reg<D, 8, NW>); break;
@@ -871,6 +895,114 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     fa.yl = yl_full;
     launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP, l);
   }
+}
+
+// ----------------------------------------------------------------- several right-hand sides (NEXT-4)
+// apply / SpMV on n x nr blocks: the triangular
+// solves of all columns run in ONE launch per stage (grid nblk x nr, every CTA
+// streams the same factor records, so columns 2..nr read them from L2), the
+// SpMV reads A once for all columns; the E/W coupling runs per column.
+template <typename T>
+bool Engine<T>::multi_ok() const {
+  if (plan.nranks != 1) return false;
+  for (const auto &d : lev)
+    if (!(d.st.nblk == 0 || d.st.rows == 0 || (d.st.reg && d.st.nf >= 0))) return false;
+  return last.nblk == 0 || last.rows == 0 || last.reg;
+}
+
+template <typename T>
+void Engine<T>::ensure_multi(int nr, int64_t ld) {
+  Pool &P = ctx->pool;
+  cudaStream_t s = ctx->stream;
+  auto grow = [&](StageDev<D> &S) {
+    if (!S.reg || S.mcap >= nr) return;
+    const int64_t rs = std::max(S.lslices, S.uslices) * 32;
+    S.mL = P.get<D>(std::max<int64_t>(rs * nr, 1));
+    S.mU = P.get<D>(std::max<int64_t>(rs * nr, 1));
+    S.mUp = P.get<D>(std::max<int64_t>(rs * nr, 1));
+    CK(cudaMemsetAsync(S.mUp, 0, std::max<int64_t>(rs * nr, 1) * sizeof(D), s));   // UP rhs: zero off the F rows
+    S.mcap = nr;
+  };
+  for (auto &d : lev) grow(d.st);
+  grow(last);
+  if (multi_cap < (int64_t)nr * ld) {
+    rM = P.get<D>((size_t)nr * ld);
+    tmpM = P.get<D>((size_t)nr * ld);
+    multi_cap = (int64_t)nr * ld;
+  }
+}
+
+template <typename T>
+void Engine<T>::ew_column(LevelDev<D> &d, int l, const D *src, const D *z, D *dst) {
+  cudaStream_t s = ctx->stream;
+  Timed t(ctx->prof, s, KC_EW);
+  if (d.k > 0 && d.k <= 64) {
+    static int max_ctas = 0;
+    if (max_ctas == 0) {
+      int per = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ewx<D>, 256, 0));
+      max_ctas = std::max(1, per) * kNumSM;
+    }
+    const int grid = (int)std::min<int64_t>((std::max<int64_t>(d.s, 1) + 255) / 256, max_ctas);
+    int64_t a0 = d.s, a1 = d.o1, a5 = n, a11 = d.ldw;
+    const int64_t *a2 = d.E.ptr;
+    const int32_t *a3 = d.E.col;
+    const D *a4 = d.E.val, *zz = z, *zh = hE[l].rbuf, *sr = src, *Wp = d.W, *Gp = d.G;
+    D *ds = dst, *pt = partial, *so = tvec;
+    int kk = d.k;
+    unsigned *tk = tickets + 0;
+    int *fl = ewflag;
+    const int *dn = nullptr;
+    void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &dn};
+    CK(cudaLaunchCooperativeKernel((const void *)k_ewx<D>, dim3(grid), dim3(256), args, 0, s));
+    return;
+  }
+  const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 4);
+  k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, z, hE[l].rbuf, n, src, dst, d.W, d.ldw, d.k,
+                               partial, tickets + 0, tvec, nullptr);
+  CK(cudaGetLastError());
+  if (d.k > 0) {
+    k_waxpy<D><<<grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 8), 256, 0, s>>>(d.s, d.o1, d.W, d.ldw, d.k, d.G, tvec,
+                                                                                  dst, nullptr);
+    CK(cudaGetLastError());
+  }
+}
+
+template <typename T>
+void Engine<T>::apply_multi(const D *in, D *out, int64_t ld, int nr) {
+  ensure_multi(nr, ld);
+  const int L = (int)lev.size();
+  for (int l = 0; l < L; ++l) {
+    LevelDev<D> &d = lev[l];
+    const D *src = (l == 0) ? in : rM;
+    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmpM, FArgs<D>{}, nullptr, KC_TRI_DOWN, l, nr, ld);
+    if (d.s > 0)
+      for (int c = 0; c < nr; ++c) ew_column(d, l, src + (size_t)c * ld, out + (size_t)c * ld, rM + (size_t)c * ld);
+  }
+  const D *src = (L == 0) ? in : rM;
+  const int64_t lL = plan.lo[L];
+  launch_trisolve(ctx, last, TRI_DOWN, src + lL, out + lL, tmpM, FArgs<D>{}, nullptr, KC_TRI_LAST, 0, nr, ld);
+  for (int l = L - 1; l >= 0; --l) {
+    LevelDev<D> &d = lev[l];
+    FArgs<D> fa;
+    fa.F = &d.F;
+    fa.Fbase = d.o0;
+    fa.nloc = n;
+    launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmpM, fa, nullptr, KC_TRI_UP, l, nr, ld);
+  }
+}
+
+template <typename T>
+void Engine<T>::spmv_multi(const D *x, D *y, int64_t ld, int nr) {
+  Timed t(ctx->prof, ctx->stream, KC_SPMV);
+  const int grid = (int)std::max<int64_t>((nslices + 7) / 8, 1);
+  if (sell_wmax <= 8)
+    k_spmv_multi<D, 8><<<grid, 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, y, ld, nr);
+  else if (sell_wmax <= 16)
+    k_spmv_multi<D, 16><<<grid, 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, y, ld, nr);
+  else
+    for (int c = 0; c < nr; ++c) spmv(x + (size_t)c * ld, y + (size_t)c * ld, 0, nullptr, nullptr);
+  CK(cudaGetLastError());
 }
 
 // Ĝ_l v = E_l (L_l U_l)^{-1} F_l C_l^{-1} v.  bufA[J_l] holds v
@@ -1825,6 +1957,47 @@ gemslr_status gemslr_apply_precond(gemslr_ctx *c, const void *x, void *y) {
     if (c->dtype == GEMSLR_F64) c->ed->apply_from(0, (const double *)x, (double *)y, nullptr);
     else c->ez->apply_from(0, (const cd *)x, (cd *)y, nullptr);
     return GEMSLR_OK;
+  });
+}
+
+}  // extern "C"
+
+template <typename T>
+static gemslr_status multi_call(gemslr_ctx *c, Engine<T> &E, int which, const void *x, void *y, int nrhs, int64_t ld) {
+  using D = typename Dev<T>::type;
+  if (nrhs < 1 || ld < E.n) return fail(c, GEMSLR_ERR_INVALID_ARG, "nrhs < 1 or ld < n_local");
+  const D *xi = static_cast<const D *>(x);
+  D *yo = static_cast<D *>(y);
+  if (which == 0) {
+    E.spmv_multi(xi, yo, ld, nrhs);
+  } else if (E.multi_ok()) {
+    for (int c0 = 0; c0 < nrhs; c0 += GEMSLR_MAX_RHS)
+      E.apply_multi(xi + (size_t)c0 * ld, yo + (size_t)c0 * ld, ld, std::min(GEMSLR_MAX_RHS, nrhs - c0));
+  } else {                                                         // kernels without a column dimension
+    for (int q = 0; q < nrhs; ++q) E.apply_from(0, xi + (size_t)q * ld, yo + (size_t)q * ld, nullptr);
+  }
+  return GEMSLR_OK;
+}
+
+extern "C" {
+
+gemslr_status gemslr_spmv_multi(gemslr_ctx *c, const void *x, void *y, int nrhs, int64_t ld) {
+  gemslr_status st = need_device(c);
+  if (st) return st;
+  if (!x || !y || x == y) return fail(c, GEMSLR_ERR_INVALID_ARG, "null or aliased blocks");
+  if (c->comm.nranks > 1) return fail(c, GEMSLR_ERR_STATE, "several right-hand sides: one GPU only");
+  return guarded(c, [&]() -> gemslr_status {
+    return c->dtype == GEMSLR_F64 ? multi_call(c, *c->ed, 0, x, y, nrhs, ld) : multi_call(c, *c->ez, 0, x, y, nrhs, ld);
+  });
+}
+
+gemslr_status gemslr_apply_precond_multi(gemslr_ctx *c, const void *x, void *y, int nrhs, int64_t ld) {
+  gemslr_status st = need_device(c);
+  if (st) return st;
+  if (!x || !y || x == y) return fail(c, GEMSLR_ERR_INVALID_ARG, "null or aliased blocks");
+  if (c->comm.nranks > 1) return fail(c, GEMSLR_ERR_STATE, "several right-hand sides: one GPU only");
+  return guarded(c, [&]() -> gemslr_status {
+    return c->dtype == GEMSLR_F64 ? multi_call(c, *c->ed, 1, x, y, nrhs, ld) : multi_call(c, *c->ez, 1, x, y, nrhs, ld);
   });
 }
 

@@ -153,6 +153,36 @@ __global__ void __launch_bounds__(256) k_spmv_sell2(int64_t n, int64_t nslices, 
   }
 }
 
+// Several right-hand sides (NEXT-4): Y[:, c] = A X[:, c] for c < nr (column-major,
+// leading dimension ld).  A warp loads the columns and values of its SELL slice
+// once and gathers x for every right-hand side, so A is read once for all nr.
+template <typename T, int WM>
+__global__ void __launch_bounds__(256) k_spmv_multi(int64_t n, int64_t nslices, const int64_t *__restrict__ off,
+                                                    const int32_t *__restrict__ col, const T *__restrict__ val,
+                                                    const T *__restrict__ X, T *__restrict__ Y, int64_t ld, int nr) {
+  const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t o = off[s];
+  const int w = (int)((off[s + 1] - o) >> 5);
+  int c[WM];
+  T v[WM];
+#pragma unroll
+  for (int e = 0; e < WM; ++e) {
+    c[e] = e < w ? __ldg(col + o + 32 * e + lane) : -1;
+    v[e] = e < w ? ld_nc(val + o + 32 * e + lane) : dzero<T>();
+  }
+  const int64_t row = s * 32 + lane;
+  for (int q = 0; q < nr; ++q) {
+    const T *x = X + (size_t)q * ld;
+    T acc = dzero<T>();
+#pragma unroll
+    for (int e = 0; e < WM; ++e)
+      if (c[e] >= 0) acc += v[e] * ld_nc(x + c[e]);
+    if (row < n) Y[(size_t)q * ld + row] = acc;
+  }
+}
+
 // halo send buffer: buf[i] = src[idx[i]]
 template <typename T>
 __global__ void k_gather_idx(int64_t n, const int *__restrict__ idx, const T *__restrict__ src, T *__restrict__ buf,
@@ -576,6 +606,9 @@ struct RegDev {
   long long *dbg;          // debug trace (block 0): 8 words per slice, 2048 slices per sweep
   int flags;               // bit 0: no L2 prefetch helper (experiments)
   int max_slices;          // L + U records of the largest block (shared-memory level table)
+  // several right-hand sides (NEXT-4): column blockIdx.y works on x/tmp + col*ldx
+  // and rhsL/mid + col*rs (0 for one column); the factor records are shared
+  long long ldx, rsL, rsU;
 };
 constexpr int REG_L2_AHEAD = 12;
 template <typename T> __host__ __device__ inline size_t reg_smem_bytes(int ring, int max_slices) {
@@ -639,6 +672,12 @@ template <typename T, int W, int NW>
 __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
                                                             const int *__restrict__ done) {
   if (done && *done) return;
+  if (blockIdx.y) {                                                // right-hand side column blockIdx.y (NEXT-4)
+    x += (size_t)blockIdx.y * P.ldx;
+    tmp += (size_t)blockIdx.y * P.ldx;
+    P.rhsL += (size_t)blockIdx.y * P.rsL;
+    P.mid += (size_t)blockIdx.y * P.rsU;
+  }
   extern __shared__ __align__(128) unsigned char smem[];
   T *ring = reinterpret_cast<T *>(smem);
   volatile int *prog = reinterpret_cast<volatile int *>(smem + (size_t)P.ring * sizeof(T));
@@ -806,8 +845,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
 // positions of the UP buffer are zero from setup on.
 template <typename T>
 __global__ void __launch_bounds__(256) k_pack_gather(int64_t np, const int *__restrict__ lrow, const T *__restrict__ src,
-                                                     T *__restrict__ dst, const int *__restrict__ done) {
+                                                     T *__restrict__ dst, const int *__restrict__ done,
+                                                     int64_t lds = 0, int64_t ldd = 0) {
   if (done && *done) return;
+  src += (size_t)blockIdx.y * lds;                                 // column blockIdx.y (several right-hand sides)
+  dst += (size_t)blockIdx.y * ldd;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x) {
     const int r = lrow[p];
     dst[p] = r >= 0 ? src[r] : dzero<T>();
@@ -818,8 +860,11 @@ __global__ void __launch_bounds__(256) k_pack_f(int64_t nf, const int *__restric
                                                 const int64_t *__restrict__ Fptr, const int32_t *__restrict__ Fcol,
                                                 const T *__restrict__ Fval, const T *__restrict__ y, int64_t nloc,
                                                 const T *__restrict__ yh, int64_t nh, const T *__restrict__ yl,
-                                                T *__restrict__ dst, const int *__restrict__ done) {
+                                                T *__restrict__ dst, const int *__restrict__ done, int64_t ldy = 0,
+                                                int64_t ldd = 0) {
   if (done && *done) return;
+  y += (size_t)blockIdx.y * ldy;                                   // column blockIdx.y (one GPU: no halo / yl)
+  dst += (size_t)blockIdx.y * ldd;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += (int64_t)gridDim.x * blockDim.x) {
     const int li = frow[i];
     T v = dzero<T>();

@@ -187,6 +187,34 @@ def test_trisolve_kernels(tmp_path, name, dims, over, tri_kernel, expect):
         assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
 
 
+@pytest.mark.parametrize("name,dims,over", [("C5", (24, 24, 20), dict(subdomains=8, rank=4)),
+                                             ("C4", (16, 16, 14), dict(subdomains=8, rank=6))])
+def test_multiple_rhs_NEXT4(tmp_path, name, dims, over):
+    """Several right-hand sides: SpMV and apply on (nrhs, n) blocks, with a
+    leading dimension larger than n and more columns than one launch takes, equal the
+    oracle column by column."""
+    prob, b, xt, prm = P.make_config(name, dims=dims, **over)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    n = prob.n
+    perm = st["perm"]
+    for nr in (1, 3, 11):
+        big = torch.zeros((nr, n + 37), dtype=s.torch_dtype, device="cuda:0")
+        cols = [P.rhs_vector(n, prob.is_complex, 100 + c) for c in range(nr)]
+        for c in range(nr):
+            big[c, :n] = to_dev(s, cols[c])
+        X = big[:, :n]
+        Y = s.apply_precond_multi(X).cpu().numpy()
+        for c in range(nr):
+            assert rel(Y[c], Pc.apply(cols[c])) <= TOL, (nr, c)
+        Ys = s.spmv_multi(X).cpu().numpy()
+        for c in range(nr):
+            ynat = np.empty(n, dtype=Ys.dtype)
+            ynat[perm] = Ys[c]
+            xnat = np.empty(n, dtype=Ys.dtype)
+            xnat[perm] = cols[c]
+            assert rel(ynat, oracle.spmv(prob, xnat)) <= TOL
+
+
 def test_complex_shifted_ilu_NEXT3(tmp_path):
     """C4 recipe with the paper's complex ILU shift 0.05 i sum|a_ii|/n:
     apply parity against the oracle's own shifted factors, FGMRES iterations within ±1."""
