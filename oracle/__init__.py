@@ -48,6 +48,7 @@ def lib():
                                         C.c_int, C.c_double, C.c_int, C.c_double, C.c_char_p, C.c_int]
         L.or_precond_create.restype = vp
         L.or_precond_destroy.argtypes = [vp]
+        L.or_precond_set_root_its.argtypes = [vp, C.c_int]
         L.or_precond_set_lowrank.argtypes = [vp, C.c_int, C.c_int, vp, vp]
         L.or_precond_apply_from.argtypes = [vp, C.c_int, vp, vp]
         L.or_ghat.argtypes = [vp, C.c_int, vp, vp]
@@ -174,6 +175,10 @@ class Precond:
 
     def s(self, l):
         return int(self.n - self.o[l + 1])
+
+    def set_root_its(self, its):
+        """NEXT-1: `its` steps of right-preconditioned GMRES on Ŝ_0 at the root level (0 = single pass)."""
+        lib().or_precond_set_root_its(self.h, int(its))
 
     def set_lowrank(self, l, W, G):
         W = np.asfortranarray(W, dtype=self.dtype)

@@ -264,6 +264,19 @@ Ilu<T> factor(const Csr<T> &B, int type, double tau, int lfil, std::string &err)
 // own A: Â = Pᵀ A P, B_l, E_l, F_l (Q3), its own
 // ILU factors of every block.
 template <typename T>
+T dot(int64_t n, const T *x, const T *y) {  // Σ conj(x_i) y_i (reading Q30)
+  T s = T(0);
+  for (int64_t i = 0; i < n; ++i) s += conjv(x[i]) * y[i];
+  return s;
+}
+template <typename T>
+double nrm2(int64_t n, const T *x) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += abs2(x[i]);
+  return std::sqrt(s);
+}
+
+template <typename T>
 struct Precond {
   int64_t N = 0;
   int L = 0;
@@ -278,6 +291,31 @@ struct Precond {
   std::vector<std::vector<T>> W, G;              // W_l: s_l x k_l col-major; G_l: k_l x k_l col-major
 
   int64_t s(int l) const { return N - o[l + 1]; }
+  int root_its = 0;                              // NEXT-1: inner GMRES steps on Ŝ_0 (0 = single pass)
+  Csr<T> C0;                                     // Â[J_0, J_0] (root Schur complement products)
+
+  // rJ += W_l [(I - R_l)^-1 - I] W_l^H rJ   (G_l = (I - R_l)^-1 - I)
+  void lowrank_add(int l, T *rJ) const {
+    if (k[l] == 0) return;
+    const int64_t sl = s(l);
+    const int kl = k[l];
+    std::vector<T> sv(kl, T(0)), tv(kl, T(0));
+    for (int c = 0; c < kl; ++c) {                 // s = W^H z2
+      T acc = T(0);
+      for (int64_t i = 0; i < sl; ++i) acc += conjv(W[l][c * sl + i]) * rJ[i];
+      sv[c] = acc;
+    }
+    for (int a = 0; a < kl; ++a) {                 // t = G s
+      T acc = T(0);
+      for (int c = 0; c < kl; ++c) acc += G[l][c * kl + a] * sv[c];
+      tv[a] = acc;
+    }
+    for (int64_t i = 0; i < sl; ++i) {             // z2 += W t
+      T acc = T(0);
+      for (int c = 0; c < kl; ++c) acc += W[l][c * sl + i] * tv[c];
+      rJ[i] += acc;
+    }
+  }
 
   // B_l^{-1} approximated blockwise: x[I_l] = U^-1 L^-1 b[I_l] per block
   void block_solve(int l, const T *b, T *x) const {
@@ -298,6 +336,7 @@ struct Precond {
   // up sweep (c4).  Applies C_{l0-1}^{-1}: input r and output y live on
   // positions [o_{l0}, N) (l0 = 0 is the whole preconditioner M^{-1}).
   void apply_from(int l0, const T *r_in, T *y_out) const {
+    if (l0 == 0 && root_its > 0) { apply_root(r_in, y_out); return; }
     const int64_t base = o[l0];
     const int64_t n = N - base;
     std::vector<T> r(r_in, r_in + n);
@@ -344,6 +383,103 @@ struct Precond {
     std::copy(y.begin(), y.end(), y_out);
   }
 
+  // ---- NEXT-1: Alg. 2 at the root level with "right preconditioned GMRES" on
+  // the inexact Schur complement Ŝ_0 = C_0 - E_0 U_0^-1 L_0^-1 F_0 (P:L541-545,
+  // P:L557): z1 = U^-1 L^-1 b1; z2 = b2 - E_0 z1; y2 ≈ Ŝ_0^-1 z2 by root_its
+  // steps of GMRES right-preconditioned by P(v) = C_0^-1 (v + W_0 G_0 W_0^H v)
+  // (the rank-k branch of Alg. 2 lines 7-8 applied at l = 0; reading Q34);
+  // y1 = z1 - U^-1 L^-1 F_0 y2.
+  void schur0(const T *v, T *out) const {        // Ŝ_0 v
+    const int64_t nI = o[1] - o[0];
+    std::vector<T> t(nI, T(0)), u(nI, T(0));
+    spmv(C0, v, out);                            // C_0 v
+    spmv(F[0], v, t.data());
+    block_solve(0, t.data(), u.data());
+    spmv_sub(E[0], u.data(), out);               // - E_0 U^-1 L^-1 F_0 v
+  }
+  void prec0(const T *v, T *out) const {         // P(v) = C_0^-1 (v + W_0 G_0 W_0^H v)
+    std::vector<T> u(v, v + s(0));
+    lowrank_add(0, u.data());
+    apply_from(1, u.data(), out);
+  }
+  // GMRES(root_its), x0 = 0, right-preconditioned in the flexible form
+  // (x = Z y with Z_j = P(V_j)), CGS2 and Givens exactly as the outer c5; it
+  // stops early only on breakdown (h_{j+1,j} <= 1e-14 ||w before GS||).
+  void root_gmres(const T *b, T *x) const {
+    const int64_t n = s(0);
+    const int m = root_its;
+    std::fill(x, x + n, T(0));
+    const double beta = nrm2(n, b);
+    if (beta == 0.0) return;
+    std::vector<T> V((size_t)n * (m + 1)), Z((size_t)n * m), w(n), H((size_t)(m + 1) * m, T(0)), g(m + 1, T(0));
+    std::vector<double> cs(m);
+    std::vector<T> sn(m);
+    for (int64_t i = 0; i < n; ++i) V[i] = b[i] / beta;
+    g[0] = beta;
+    int jend = 0;
+    for (int j = 0; j < m; ++j) {
+      T *vj = V.data() + (size_t)j * n, *zj = Z.data() + (size_t)j * n;
+      prec0(vj, zj);
+      schur0(zj, w.data());
+      const double eta = nrm2(n, w.data());
+      std::vector<T> h(j + 1), h2(j + 1);
+      for (int i = 0; i <= j; ++i) h[i] = dot(n, V.data() + (size_t)i * n, w.data());
+      for (int i = 0; i <= j; ++i)
+        for (int64_t q = 0; q < n; ++q) w[q] -= V[(size_t)i * n + q] * h[i];
+      for (int i = 0; i <= j; ++i) h2[i] = dot(n, V.data() + (size_t)i * n, w.data());
+      for (int i = 0; i <= j; ++i)
+        for (int64_t q = 0; q < n; ++q) w[q] -= V[(size_t)i * n + q] * h2[i];
+      const double hnext = nrm2(n, w.data());
+      T *Hj = H.data() + (size_t)j * (m + 1);
+      for (int i = 0; i <= j; ++i) Hj[i] = h[i] + h2[i];
+      Hj[j + 1] = hnext;
+      for (int i = 0; i < j; ++i) {
+        T p = Hj[i], q = Hj[i + 1];
+        Hj[i] = cs[i] * p + conjv(sn[i]) * q;
+        Hj[i + 1] = -sn[i] * p + cs[i] * q;
+      }
+      T a = Hj[j];
+      double bb = absval(Hj[j + 1]), aa = absval(a), c;
+      T sr;
+      if (bb == 0.0) { c = 1.0; sr = T(0); }
+      else if (aa == 0.0) { c = 0.0; sr = T(1); }
+      else {
+        double t = std::sqrt(aa * aa + bb * bb);
+        c = aa / t;
+        sr = bb * conjv(a) / (aa * t);
+      }
+      cs[j] = c; sn[j] = sr;
+      T p = Hj[j], q = Hj[j + 1];
+      Hj[j] = c * p + conjv(sr) * q;
+      Hj[j + 1] = -sr * p + c * q;
+      T gp = g[j], gq = g[j + 1];
+      g[j] = c * gp + conjv(sr) * gq;
+      g[j + 1] = -sr * gp + c * gq;
+      jend = j + 1;
+      if (hnext <= 1e-14 * eta) break;
+      for (int64_t q2 = 0; q2 < n; ++q2) V[(size_t)(j + 1) * n + q2] = w[q2] / hnext;
+    }
+    std::vector<T> y(jend);
+    for (int i = jend - 1; i >= 0; --i) {          // H[0:jend, 0:jend] y = g
+      T acc = g[i];
+      for (int c2 = i + 1; c2 < jend; ++c2) acc -= H[(size_t)c2 * (m + 1) + i] * y[c2];
+      y[i] = acc / H[(size_t)i * (m + 1) + i];
+    }
+    for (int c2 = 0; c2 < jend; ++c2)              // x = Z y
+      for (int64_t i = 0; i < n; ++i) x[i] += Z[(size_t)c2 * n + i] * y[c2];
+  }
+  void apply_root(const T *r, T *y) const {
+    const int64_t nI = o[1] - o[0], n0 = s(0);
+    std::vector<T> z1(nI, T(0)), z2(r + nI, r + nI + n0), y2(n0), t(nI, T(0)), w(nI, T(0));
+    block_solve(0, r, z1.data());                  // z1 = U^-1 L^-1 b1
+    spmv_sub(E[0], z1.data(), z2.data());          // z2 = b2 - E_0 z1
+    root_gmres(z2.data(), y2.data());              // y2 ≈ Ŝ_0^-1 z2
+    spmv(F[0], y2.data(), t.data());
+    block_solve(0, t.data(), w.data());
+    for (int64_t i = 0; i < nI; ++i) y[i] = z1[i] - w[i];   // y1 = z1 - U^-1 L^-1 F_0 y2
+    std::copy(y2.begin(), y2.end(), y + nI);
+  }
+
   // Ĝ_l v = E_l (L_l U_l)^{-1} F_l C_l^{-1} v   (Q4)
   void ghat(int l, const T *v, T *out) const {
     const int64_t sl = s(l), nI = o[l + 1] - o[l];
@@ -369,18 +505,6 @@ struct FgmresOut {
   double max_est_gap = 0.0;    // max |estimate - explicit| / bnorm at cycle ends
 };
 
-template <typename T>
-T dot(int64_t n, const T *x, const T *y) {  // Σ conj(x_i) y_i (reading Q30)
-  T s = T(0);
-  for (int64_t i = 0; i < n; ++i) s += conjv(x[i]) * y[i];
-  return s;
-}
-template <typename T>
-double nrm2(int64_t n, const T *x) {
-  double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s += abs2(x[i]);
-  return std::sqrt(s);
-}
 
 template <typename T>
 FgmresOut<T> fgmres(const Csr<T> &A, precond_fn M, void *Muser, const T *b, T *x,
@@ -597,6 +721,7 @@ Precond<T> *build_precond(int64_t n, const int64_t *rowptr, const int32_t *col, 
       if (!err.empty()) { err += " (level " + std::to_string(l) + ", block " + std::to_string(q) + ")"; delete P; return nullptr; }
     }
     P->fac.push_back(std::move(f));
+    if (l == 0) P->C0 = submatrix(P->Ahat, P->o[1], n, P->o[1], n);
     P->E.push_back(submatrix(P->Ahat, P->o[l + 1], n, P->o[l], P->o[l + 1]));
     P->F.push_back(submatrix(P->Ahat, P->o[l], P->o[l + 1], P->o[l + 1], n));
   }
@@ -716,6 +841,12 @@ void or_precond_destroy(void *hv) {
   if (!h) return;
   if (h->is_cplx) delete static_cast<Precond<zc> *>(h->p); else delete static_cast<Precond<double> *>(h->p);
   delete h;
+}
+
+void or_precond_set_root_its(void *hv, int its) {
+  auto *h = static_cast<Handle *>(hv);
+  if (h->is_cplx) static_cast<Precond<zc> *>(h->p)->root_its = its;
+  else static_cast<Precond<double> *>(h->p)->root_its = its;
 }
 
 void or_precond_set_lowrank(void *hv, int l, int k, const void *W, const void *G) {

@@ -229,6 +229,40 @@ def test_complex_shifted_ilu_NEXT3(shift):
     assert np.array_equal(P0.apply(r), P1.apply(r))
 
 
+@pytest.mark.parametrize("cplx", [False, True])
+def test_root_gmres_NEXT1(cplx):
+    """Root-level inner GMRES on Ŝ_0 (Alg. 2 line 6): run to s_0 steps it solves
+    Ŝ_0 y2 = z2 exactly, so the apply equals the exact inverse of the block matrix
+    [[L U, F_0], [E_0, C_0]] built densely from the oracle's own block ILU(0) factors; the
+    map is homogeneous (apply(2b) = 2 apply(b)) but, with few steps, not additive."""
+    prob = P.helmholtz_shifted((8, 7)) if cplx else P.convdiff_upwind((9, 8))
+    A = prob.scipy()
+    st = D.tiny_structure(A, prob.coords, 2, 4, nlast=2)
+    Pc = oracle.Precond(A, st, ilu=(oracle.ILU0, 0.0, 0))
+    n, o1 = prob.n, st["level_off"][1]
+    s0 = n - o1
+    Pc.set_root_its(s0)
+    Ah = D.permute_matrix(A, st["perm"]).toarray()
+    LU = np.zeros((o1, o1), dtype=Ah.dtype)
+    bl = st["blocks"][0]
+    for q in range(len(bl) - 1):
+        a, c = bl[q], bl[q + 1]
+        LU[a:c, a:c] = (Pc.factor(0, q, 0).toarray() + np.eye(c - a)) @ Pc.factor(0, q, 1).toarray()
+    M = Ah.copy()
+    M[:o1, :o1] = LU
+    b = P.rhs_vector(n, cplx, 7)
+    y = Pc.apply(b)
+    ye = np.linalg.solve(M, b)
+    assert np.linalg.norm(y - ye) <= 1e-9 * np.linalg.norm(ye)
+    Pc.set_root_its(3)
+    y1 = Pc.apply(b)
+    assert np.linalg.norm(Pc.apply(2.0 * b) - 2.0 * y1) <= 1e-12 * np.linalg.norm(y1)
+    b2 = P.rhs_vector(n, cplx, 8)
+    assert np.linalg.norm(Pc.apply(b + b2) - y1 - Pc.apply(b2)) > 1e-8 * np.linalg.norm(y1)
+    Pc.set_root_its(0)
+    assert np.linalg.norm(Pc.apply(b + b2) - Pc.apply(b) - Pc.apply(b2)) <= 1e-12 * np.linalg.norm(y1)
+
+
 def test_apply_linearity_D6_and_ghat_definition():
     prob = P.helmholtz_shifted((6, 6, 3))
     A = prob.scipy()
