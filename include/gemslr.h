@@ -69,6 +69,10 @@ typedef struct {
   int cluster_ctas;         /* CTAs per thread-block cluster in the triangular solves; 0 = automatic        */
   int tri_kernel;           /* triangular-solve kernel: 0 = automatic (register-prefetched k_tri_reg where
                                the setup proves it applies), 1 = TMA-staged k_tri_pipe, 2 = level kernel     */
+  int root_inner_its;       /* NEXT-1: steps of right-preconditioned GMRES on the root Schur complement
+                               S_0 = C_0 - E_0 U_0^-1 L_0^-1 F_0 inside every apply (Alg. 2 line 6, P:L541-545;
+                               the experiments use 3 to 5); 0 = the single-pass low-rank branch
+                               (reading Q2).  The preconditioner is then nonlinear (use FGMRES).  One GPU. */
   double ilu_shift;         /* complex diagonal shift of the block ILUs: sigma = i*ilu_shift*sum|a_ii|/n added
                                to every B_l and C_last block before factoring (the paper uses
                                0.05); 0 = off; GEMSLR_C128 only (INVALID_ARG for GEMSLR_F64)               */

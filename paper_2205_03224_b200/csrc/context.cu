@@ -379,7 +379,15 @@ struct Engine {
   void ensure_multi(int nr, int64_t ld);
   void apply_multi(const D *in, D *out, int64_t ld, int nr);
   void spmv_multi(const D *x, D *y, int64_t ld, int nr);
-  void ew_column(LevelDev<D> &d, int l, const D *src, const D *z, D *dst);
+  void ew_column(LevelDev<D> &d, int l, const D *src, const D *z, D *dst, const int *doneflag = nullptr);
+  // NEXT-1: root-level inner GMRES on Ŝ_0 (one GPU)
+  int root_its = 0;
+  D *Vr = nullptr, *Zr = nullptr, *wr = nullptr, *ur = nullptr, *zerov = nullptr, *Hr = nullptr, *gr = nullptr,
+    *snr = nullptr, *yr = nullptr, *rres = nullptr;
+  double *csr = nullptr, *dblr = nullptr, *histr = nullptr;
+  int *intsr = nullptr, *doner = nullptr, *skipr = nullptr;
+  int64_t ldr = 0;
+  void root_gmres(const D *bJ, D *xJ, const int *doneflag);
   void spmv(const D *x, D *y, int mode, const D *b, const int *doneflag);
   void ghat(int l, D *bufA, D *bufB);
   void build_lowrank(const gemslr_params &prm, unsigned long long seed);
@@ -819,6 +827,26 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
   const int L = (int)lev.size();
   cudaStream_t s = ctx->stream;
   const bool dist = plan.nranks > 1;
+  if (l0 == 0 && root_its > 0 && L > 0 && !dist) {                // Alg. 2 with GMRES at the root (NEXT-1)
+    LevelDev<D> &d = lev[0];
+    launch_trisolve(ctx, d.st, TRI_DOWN, in, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, 0);   // z1
+    {
+      Timed t(ctx->prof, s, KC_EW);                              // z2 = b2 - E_0 z1 -> r[J_0]
+      const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 4);
+      k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, out, hE[0].rbuf, n, in, r, d.W, d.ldw, 0,
+                                   partial, tickets + 0, tvec, doneflag);
+      CK(cudaGetLastError());
+    }
+    root_gmres(r + d.o1, out + d.o1, doneflag);                   // y2 ≈ Ŝ_0^-1 z2
+    FArgs<D> fa;                                                   // y1 = z1 - U^-1 L^-1 F_0 y2
+    fa.F = &d.F;
+    fa.Fbase = d.o0;
+    fa.nloc = n;
+    fa.yh = hF[0].rbuf;
+    fa.nh = hF[0].nrecv;
+    launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP, 0);
+    return;
+  }
   for (int l = l0; l < L; ++l) {
     LevelDev<D> &d = lev[l];
     const D *src = (l == l0) ? in : r;
@@ -933,7 +961,7 @@ void Engine<T>::ensure_multi(int nr, int64_t ld) {
 }
 
 template <typename T>
-void Engine<T>::ew_column(LevelDev<D> &d, int l, const D *src, const D *z, D *dst) {
+void Engine<T>::ew_column(LevelDev<D> &d, int l, const D *src, const D *z, D *dst, const int *doneflag) {
   cudaStream_t s = ctx->stream;
   Timed t(ctx->prof, s, KC_EW);
   if (d.k > 0 && d.k <= 64) {
@@ -952,18 +980,18 @@ void Engine<T>::ew_column(LevelDev<D> &d, int l, const D *src, const D *z, D *ds
     int kk = d.k;
     unsigned *tk = tickets + 0;
     int *fl = ewflag;
-    const int *dn = nullptr;
+    const int *dn = doneflag;
     void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &dn};
     CK(cudaLaunchCooperativeKernel((const void *)k_ewx<D>, dim3(grid), dim3(256), args, 0, s));
     return;
   }
   const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 4);
   k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, z, hE[l].rbuf, n, src, dst, d.W, d.ldw, d.k,
-                               partial, tickets + 0, tvec, nullptr);
+                               partial, tickets + 0, tvec, doneflag);
   CK(cudaGetLastError());
   if (d.k > 0) {
     k_waxpy<D><<<grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 8), 256, 0, s>>>(d.s, d.o1, d.W, d.ldw, d.k, d.G, tvec,
-                                                                                  dst, nullptr);
+                                                                                  dst, doneflag);
     CK(cudaGetLastError());
   }
 }
@@ -1002,6 +1030,75 @@ void Engine<T>::spmv_multi(const D *x, D *y, int64_t ld, int nr) {
     k_spmv_multi<D, 16><<<grid, 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, y, ld, nr);
   else
     for (int c = 0; c < nr; ++c) spmv(x + (size_t)c * ld, y + (size_t)c * ld, 0, nullptr, nullptr);
+  CK(cudaGetLastError());
+}
+
+// ----------------------------------------------------------------- NEXT-1 root GMRES
+// y2 ≈ Ŝ_0^-1 z2 by root_its steps of GMRES (x0 = 0) right-preconditioned by
+// P(v) = C_0^-1 (v + W_0 G_0 W_0^H v) in the flexible form x = Z y, CGS2 and
+// Givens as the outer FGMRES, early stop only on breakdown (oracle.cpp
+// root_gmres).  Ŝ_0 t = C_0 t - E_0 U^-1 L^-1 F_0 t is formed as
+// rows J_0 of Â [-(LU)^-1 F_0 t ; t]: an UP trisolve of level 0 on the vector
+// [0 ; t] and a full SpMV.  Device-resident state, no host synchronisation (so
+// it is captured in the FGMRES graphs); the inner kernels check an inner done
+// flag that starts as the outer one.
+template <typename T>
+void Engine<T>::root_gmres(const D *bJ, D *xJ, const int *doneflag) {
+  cudaStream_t s = ctx->stream;
+  Pool &P = ctx->pool;
+  LevelDev<D> &d0 = lev[0];
+  const int m = root_its;
+  const int64_t o1 = d0.o1, s0 = n - o1;
+  if (!Vr) {
+    ldr = (n + 31) / 32 * 32;
+    Vr = P.get<D>((size_t)ldr * (m + 1));
+    Zr = P.get<D>((size_t)ldr * m);
+    wr = P.get<D>(ldr);
+    ur = P.get<D>(ldr);
+    zerov = P.get<D>(ldr);
+    Hr = P.get<D>((size_t)(m + 1) * m);
+    gr = P.get<D>(m + 1);
+    snr = P.get<D>(m);
+    yr = P.get<D>(m);
+    rres = P.get<D>(3 * (GS_MAXC + 2));
+    csr = P.get<double>(m);
+    dblr = P.get<double>(8);
+    histr = P.get<double>(m + 2);
+    intsr = P.get<int>(4);
+    doner = P.get<int>(1);
+    skipr = P.get<int>(1);
+    CK(cudaMemsetAsync(Zr, 0, (size_t)ldr * m * sizeof(D), s));
+    CK(cudaMemsetAsync(Vr, 0, (size_t)ldr * (m + 1) * sizeof(D), s));
+    CK(cudaMemsetAsync(zerov, 0, (size_t)ldr * sizeof(D), s));
+    CK(cudaMemsetAsync(ur, 0, (size_t)ldr * sizeof(D), s));
+  }
+  FgmDev<D> f{doner, intsr, dblr, histr, Hr, gr, csr, snr};
+  D *r1 = rres, *r2 = rres + (GS_MAXC + 2), *r3 = rres + 2 * (GS_MAXC + 2);
+  const int g1 = grid_for((s0 + 255) / 256, 4);
+  gs_pass(nullptr, 0, s0, 0, const_cast<D *>(bJ), 0, 0, nullptr, r1, 10, doneflag);   // ||z2||^2
+  CK(cudaMemsetAsync(Hr, 0, (size_t)(m + 1) * m * sizeof(D), s));
+  k_root_start<D><<<1, 32, 0, s>>>(f, m, r1, doneflag, skipr);
+  k_scale<D><<<g1, 256, 0, s>>>(s0, bJ, Vr + o1, dblr + 4, doner);                   // V_0 = z2 / beta
+  for (int j = 0; j < m; ++j) {
+    D *vj = Vr + (size_t)j * ldr, *zj = Zr + (size_t)j * ldr;
+    ew_column(d0, 0, vj, zerov, ur, doner);                                            // u = v + W G W^H v (E·0)
+    apply_from(1, ur, zj, doner);                                                       // Z_j = C_0^-1 u
+    CK(cudaMemsetAsync(zj, 0, (size_t)o1 * sizeof(D), s));                             // [0 ; Z_j]
+    FArgs<D> fa;
+    fa.F = &d0.F;
+    fa.Fbase = d0.o0;
+    fa.nloc = n;
+    launch_trisolve(ctx, d0.st, TRI_UP, (const D *)nullptr, zj, tmp, fa, doner, KC_TRI_UP, 0);   // [-(LU)^-1 F Z_j ; Z_j]
+    spmv(zj, wr, 0, nullptr, doner);                                                    // w[J_0] = Ŝ_0 Z_j
+    gs_pass(Vr + o1, ldr, s0, j + 1, wr + o1, 0, 1, nullptr, r1, 10, doner);
+    gs_pass(Vr + o1, ldr, s0, j + 1, wr + o1, 1, 1, r1, r2, 11, doner);
+    gs_pass(Vr + o1, ldr, s0, j + 1, wr + o1, 1, 0, r2, r3, 12, doner);
+    k_fgmres_col<D><<<1, 32, 0, s>>>(f, m, j, r1, r2, r3);
+    if (j + 1 < m) k_scale<D><<<g1, 256, 0, s>>>(s0, wr + o1, Vr + (size_t)(j + 1) * ldr + o1, dblr + 2, doner);
+  }
+  k_root_solve<D><<<1, 32, 0, s>>>(f, m, skipr, yr);
+  CK(cudaMemsetAsync(xJ, 0, (size_t)s0 * sizeof(D), s));
+  k_xupdate<D><<<g1, 256, 0, s>>>(s0, Zr + o1, ldr, m, yr, xJ);                      // y2 = Z y
   CK(cudaGetLastError());
 }
 
@@ -1862,6 +1959,7 @@ static gemslr_status do_setup(gemslr_ctx *c, std::unique_ptr<Engine<T>> &E, int6
   auto t2 = std::chrono::steady_clock::now();
   E->setup_dev_s = std::chrono::duration<double>(t2 - t1).count();
   E->build_lowrank(*prm, prm->seed);
+  E->root_its = prm->root_inner_its;                              // NEXT-1 (after the low rank: Arnoldi uses l0 >= 1)
   CK(cudaStreamSynchronize(c->stream));
   E->arnoldi_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
   return GEMSLR_OK;
@@ -1879,6 +1977,9 @@ gemslr_status gemslr_setup(gemslr_ctx *c, gemslr_dtype dtype, int64_t n, const i
       (prm->ilu != GEMSLR_ILU0 && prm->ilu != GEMSLR_ILUT) || prm->ilut_drop < 0)
     return fail(c, GEMSLR_ERR_INVALID_ARG, "levels < 1, subdomains < 1, rank < 0 or bad dtype/ilu");
   if (2 * prm->rank + 2 > GS_MAXC) return fail(c, GEMSLR_ERR_INVALID_ARG, "rank > 50 not supported (cycle 2k <= 102)");
+  if (prm->root_inner_its < 0 || prm->root_inner_its + 2 > GS_MAXC ||
+      (prm->root_inner_its > 0 && c->comm.nranks > 1))
+    return fail(c, GEMSLR_ERR_INVALID_ARG, "root_inner_its < 0, too large, or with several ranks (one GPU only)");
   if (prm->ilu_shift != 0.0 && (dtype != GEMSLR_C128 || !(prm->ilu_shift == prm->ilu_shift)))
     return fail(c, GEMSLR_ERR_INVALID_ARG, "ilu_shift needs complex arithmetic (GEMSLR_C128)");
   c->params = *prm;

@@ -1501,6 +1501,43 @@ __global__ void __launch_bounds__(256) k_fgmres_scale(FgmDev<T> f, int m, int j,
     vnext[i] = dscale(w[i], sc);
 }
 
+// ----------------------------------------------------------------- NEXT-1 root GMRES helpers
+// Start of the root-level inner GMRES (Alg. 2 line 6): beta = ||z2||
+// from the norm pass, the inner state reset, the inner done flag copied from the
+// outer one (an outer FGMRES that has finished skips the whole inner solve).
+template <typename T>
+__global__ void k_root_start(FgmDev<T> f, int m, const T *__restrict__ res, const int *__restrict__ outer_done,
+                             int *__restrict__ skip) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double b2;
+  if constexpr (sizeof(T) == sizeof(double)) b2 = res[0]; else b2 = res[0].x;
+  const double beta = sqrt(b2 > 0 ? b2 : 0.0);
+  const int od = outer_done ? *outer_done : 0;
+  *skip = od;
+  f.dbl[0] = beta > 0 ? beta : 1.0;     // "bnorm" of the inner residual history
+  f.dbl[1] = 0.0;                       // no tolerance test: a fixed number of steps (or breakdown)
+  f.dbl[4] = beta > 0 ? 1.0 / beta : 0.0;
+  f.ints[0] = 0;
+  f.ints[1] = 0;
+  f.ints[2] = 1 << 30;
+  for (int i = 0; i <= m; ++i) f.g[i] = dzero<T>();
+  if constexpr (sizeof(T) == sizeof(double)) f.g[0] = beta; else f.g[0] = T{beta, 0.0};
+  *f.done = (od || beta == 0.0) ? 1 : 0;
+}
+// y = H[0:jend, 0:jend]^{-1} g (upper triangular after the rotations), zero beyond jend
+template <typename T>
+__global__ void k_root_solve(FgmDev<T> f, int m, const int *__restrict__ skip, T *__restrict__ y) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (*skip) return;
+  const int jend = f.ints[0];
+  for (int i = m - 1; i >= 0; --i) {
+    if (i >= jend) { y[i] = dzero<T>(); continue; }
+    T acc = f.g[i];
+    for (int c = i + 1; c < jend; ++c) acc -= f.H[(int64_t)c * (m + 1) + i] * y[c];
+    y[i] = acc / f.H[(int64_t)i * (m + 1) + i];
+  }
+}
+
 // ----------------------------------------------------------------- utilities
 // y = x * scale[0] (scale may be a device scalar of 1/β); done-guarded
 template <typename T>

@@ -215,6 +215,26 @@ def test_multiple_rhs_NEXT4(tmp_path, name, dims, over):
             assert rel(ynat, oracle.spmv(prob, xnat)) <= TOL
 
 
+@pytest.mark.parametrize("name,dims,over", [("C5", (24, 24, 20), dict(subdomains=8, rank=4)),
+                                             ("C4", (16, 16, 14), dict(subdomains=8, rank=6)),
+                                             ("C3", (20, 18, 16), dict(subdomains=8, rank=0))])
+def test_root_gmres_NEXT1(tmp_path, name, dims, over):
+    """Root-level inner GMRES on Ŝ_0 (Alg. 2 line 6, 3 steps as in P:L1073-1074): apply
+    parity against the oracle's root GMRES, FGMRES iterations within ±1, true residual."""
+    prob, b, xt, prm = P.make_config(name, dims=dims, **over)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path, root_inner_its=3)
+    Pc.set_root_its(3)
+    for seed in (2, 3):
+        r = P.rhs_vector(prob.n, prob.is_complex, seed)
+        assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
+    out = s.solve(to_dev(s, b[st["perm"]]), rtol=prm["rtol"], restart=prm["restart"])
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"])
+    assert out["status"] == 0 and abs(out["its"] - ref["its"]) <= 1, (out["its"], ref["its"])
+    xg = np.empty(prob.n, dtype=b.dtype)
+    xg[st["perm"]] = out["x"].cpu().numpy()
+    assert np.linalg.norm(b - oracle.spmv(prob, xg)) <= prm["rtol"] * np.linalg.norm(b)
+
+
 def test_complex_shifted_ilu_NEXT3(tmp_path):
     """C4 recipe with the paper's complex ILU shift 0.05 i sum|a_ii|/n:
     apply parity against the oracle's own shifted factors, FGMRES iterations within ±1."""
