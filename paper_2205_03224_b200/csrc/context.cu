@@ -1162,7 +1162,16 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
         done2 = false;
       }
     } else {
-      done2 = false;
+      // complex: lane groups (2 x 32 or 4 x 26 columns per row tile)
+      auto go3 = [&](auto kern, int rw) {
+        const int grid = grid_for((nn + 8 * rw - 1) / (8 * rw), 1);
+        kern<<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv,
+                                            doneflag);
+      };
+      if (ncols <= 48) done2 = false;                             // k_gs<2,6> measured faster here
+      else if (ncols <= 64) go3(k_gs2g<D, 2, 32>, 16);
+      else if (ncols <= 104) go3(k_gs2g<D, 4, 26>, 8);
+      else done2 = false;
     }
   }
   if (done2) {

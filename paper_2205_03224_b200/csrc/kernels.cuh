@@ -1416,6 +1416,104 @@ __global__ void __launch_bounds__(256, 2) k_gs2h(int64_t n, const T *__restrict_
   if (tid == 0) *ticket = 0;
 }
 
+// Grouped warp tiles for many columns (complex restart-100 cycles): a warp covers
+// RW = 32 / G rows; lane group g (RW lanes) holds columns [g*C, g*C + C) of those
+// rows.  Update: partial sums combined over the groups by log2(G) shuffles; dot:
+// per group a transpose-butterfly over its RW lanes (RW - 1 shuffles per RW
+// columns; afterwards lane sub of group g holds column g*C + q*RW + sub).
+template <int RW, typename T>
+__device__ inline void tbfly_n(T (&x)[RW], int sub) {
+#pragma unroll
+  for (int o = RW / 2; o >= 1; o >>= 1) {
+    const bool up = (sub & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const T send = up ? x[k] : x[k + o];
+      const T keep = up ? x[k + o] : x[k];
+      x[k] = keep + shfl_x(send, o);
+    }
+  }
+}
+template <typename T, int G, int C>
+__global__ void __launch_bounds__(256, 1) k_gs2g(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
+                                                int dot, const T *__restrict__ h_in, T *__restrict__ partial,
+                                                unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
+  if (done && *done) return;
+  constexpr int RW = 32 / G, NQ = (C + RW - 1) / RW, NC = G * C;
+  __shared__ T sh[NC];
+  __shared__ T red[8][NC + 1];
+  __shared__ bool amlast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = lane / RW, sub = lane % RW;
+  for (int c = tid; c < NC; c += blockDim.x) sh[c] = (upd && c < ncols) ? h_in[c] : dzero<T>();
+  __syncthreads();
+  T acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = dzero<T>();
+  double nrm = 0.0;
+  const int64_t ntiles = (n + RW - 1) / RW;
+  const T *Vg = V + (int64_t)(grp * C) * ldv;
+  const int nc = ncols - grp * C;
+  for (int64_t tile = (int64_t)blockIdx.x * 8 + warp; tile < ntiles; tile += (int64_t)gridDim.x * 8) {
+    const int64_t r = tile * RW + sub;
+    const bool ok = r < n;
+    T v[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) v[k] = (k < nc && ok) ? ld_nc(Vg + k * ldv + r) : dzero<T>();
+    T wi = ok ? w[r] : dzero<T>();
+    if (upd) {
+      T u0 = dzero<T>(), u1 = dzero<T>();
+#pragma unroll
+      for (int k = 0; k < C; k += 2) {
+        u0 += v[k] * sh[grp * C + k];
+        if (k + 1 < C) u1 += v[k + 1 < C ? k + 1 : 0] * sh[grp * C + (k + 1 < C ? k + 1 : 0)];
+      }
+      T u = u0 + u1;
+#pragma unroll
+      for (int o = RW; o < 32; o <<= 1) u = u + shfl_x(u, o);
+      wi = wi - u;
+      if (ok && grp == 0) w[r] = wi;
+    }
+    if (grp == 0) nrm += dabs2(wi);
+    if (dot) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        T x[RW];
+#pragma unroll
+        for (int k = 0; k < RW; ++k) x[k] = (q * RW + k < C) ? dconj(v[q * RW + k < C ? q * RW + k : 0]) * wi : dzero<T>();
+        tbfly_n<RW>(x, sub);
+        acc[q] += x[0];
+      }
+    }
+  }
+  const int nres = dot ? ncols + 1 : 1;
+  nrm = warp_sum(nrm);
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+    if (q * RW + sub < C) red[warp][grp * C + q * RW + sub] = acc[q];
+  if (lane == 0) {
+    T t = dzero<T>();
+    if constexpr (sizeof(T) == sizeof(double)) t = nrm; else t = T{nrm, 0.0};
+    red[warp][NC] = t;
+  }
+  __syncthreads();
+  for (int c = tid; c < nres; c += blockDim.x) {
+    const int src = (c == nres - 1) ? NC : c;
+    T t = dzero<T>();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += red[q][src];
+    partial[(int64_t)c * gridDim.x + blockIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) amlast = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!amlast) return;
+  __threadfence();
+  reduce_partials(partial, (int)gridDim.x, nres, res);
+  if (tid == 0) *ticket = 0;
+}
+
 // ----------------------------------------------------------------- FGMRES column (1 thread)
 template <typename T>
 struct FgmDev {
