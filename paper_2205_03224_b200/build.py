@@ -17,6 +17,8 @@ OUT = os.path.join(HERE, "libgemslr.so")
 BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# GEMSLR_TRACE=1: compile the clock64 trace of k_tri_reg in (tools/trace_reg.py)
+TRACE = ["-DGEMSLR_TRACE"] if os.environ.get("GEMSLR_TRACE") == "1" else []
 
 CPP = ["partition.cpp", "ilu.cpp", "schedule.cpp", "hostplan.cpp", "schur.cpp"]
 CU = ["context.cu"]
@@ -57,7 +59,7 @@ def build(force=False, verbose=False):
     for f in CU:
         o = os.path.join(BUILD, f + ".o")
         r = _run([NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-fopenmp",
-                  *inc, "-c", os.path.join(SRC, f), "-o", o])
+                  *TRACE, *inc, "-c", os.path.join(SRC, f), "-o", o])
         if verbose:
             sys.stderr.write(r.stderr)
         with open(os.path.join(BUILD, f + ".ptxas.txt"), "w") as fh:

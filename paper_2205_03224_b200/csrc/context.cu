@@ -15,6 +15,8 @@
 #include <cstring>
 #include <memory>
 #include <random>
+#include <set>
+#include <type_traits>
 #include <string>
 #include <dlfcn.h>
 #include <sys/stat.h>
@@ -275,6 +277,7 @@ struct StageDev {
   PipeDev<D> P{};
   bool reg = false;        // register-prefetched kernel (k_tri_reg), preferred when available
   int reg_w = 0;           // record width W (4, 8, 10, 12 or 16)
+  int reg_nw = 0;          // consumer warps of k_tri_reg (reg_nw_for)
   RegDev<D> Rg{};
   int64_t reg_bytes = 0;   // record bytes of both sweeps
   const int *lrow = nullptr;       // per packed L position: the row (-1 padding), DOWN gather
@@ -419,6 +422,31 @@ struct Ctx {
 };
 
 // ----------------------------------------------------------------- upload
+// Consumer warps of k_tri_reg for a stage.  A warp's record loads are issued
+// right after its slice and waited for at its next one, NW slices later, i.e.
+// NW / K levels later with K slices per level: stages with many slices per
+// level (the level-0 subdomains) need more warps to cover the L2 latency, stages
+// with 1-2 slices per level pay for the wider barriers.  K = all slices / all
+// levels of the stage's blocks.  GEMSLR_REG_NW overrides (experiments).
+template <typename D, typename T>
+static int reg_nw_for(const RegPack<T> &R) {
+  static const int env = getenv("GEMSLR_REG_NW") ? atoi(getenv("GEMSLR_REG_NW")) : 0;
+  const int nb = (int)(R.binfo.size() / REG_BINFO_INTS);
+  int64_t sl = 0, lv = 0;
+  for (int b = 0; b < nb; ++b) {
+    const int32_t *bi = &R.binfo[(size_t)b * REG_BINFO_INTS];
+    sl += bi[1] + bi[4];
+    lv += bi[2] + bi[5];
+  }
+  const double K = lv > 0 ? (double)sl / (double)lv : 1.0;
+  if (sizeof(D) == 8) {
+    if (env == 15 || env == 23) return env;
+    return K >= 3.0 ? 23 : 15;
+  }
+  if (env == 7 || env == 15) return env;
+  return K >= 3.0 ? 15 : 7;
+}
+
 template <typename D, typename T>
 static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int cps_override, int tri_kernel) {
   StageDev<D> d;
@@ -462,6 +490,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     static_assert(REG_BINFO == REG_BINFO_INTS, "binfo layout");
     d.reg = true;
     d.reg_w = S.reg.W;
+    d.reg_nw = reg_nw_for<D>(S.reg);
     d.Rg.data = P.upload<unsigned char>(S.reg.data, s);
     d.Rg.slev = P.upload<unsigned short>(S.reg.slev, s);
     d.Rg.max_slices = S.reg.max_block_slices;
@@ -690,7 +719,6 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
   const D *Fv = F ? F->val : nullptr;
   const int pgrid = grid_for((S.rows + 255) / 256, 4);
   if (S.reg) {
-    constexpr int NW = sizeof(D) == 8 ? 15 : 7;   // (NW + 1) warps a multiple of 4: full register budget
     const size_t smem = reg_smem_bytes<D>(S.Rg.ring, S.Rg.max_slices);
     RegDev<D> Rg = S.Rg;
     Rg.ldx = Rg.rsL = Rg.rsU = 0;
@@ -720,26 +748,35 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
       }
     }
     Timed t(ctx->prof, ctx->stream, kc, lvl);
-    static bool attr = false;
-    if (!attr) {
-      const int smax = 232448 - 1024;   // room for the static shared block info
-      CK(cudaFuncSetAttribute(k_tri_reg<D, 4, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-      CK(cudaFuncSetAttribute(k_tri_reg<D, 8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-      CK(cudaFuncSetAttribute(k_tri_reg<D, 10, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-      CK(cudaFuncSetAttribute(k_tri_reg<D, 12, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-      CK(cudaFuncSetAttribute(k_tri_reg<D, 16, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-      attr = true;
-    }
     Rg.dbg = (kc == KC_TRI_DOWN && lvl == g_tri_dbg_level) ? g_tri_dbg : nullptr;
     static const int reg_flags = getenv("GEMSLR_REG_FLAGS") ? atoi(getenv("GEMSLR_REG_FLAGS")) : 0;
     Rg.flags = reg_flags;
-    auto go = [&](auto kern) { kern<<<dim3(S.nblk, nr), 32 * (NW + 1), smem, ctx->stream>>>(Rg, mode, x, tmp, doneflag); };
-    switch (S.reg_w) {
-      case 4: go(k_tri_reg<D, 4, NW>); break;
-      case 8: go(k_tri_reg<D, 8, NW>); break;
-      case 10: go(k_tri_reg<D, 10, NW>); break;
-      case 12: go(k_tri_reg<D, 12, NW>); break;
-      default: go(k_tri_reg<D, 16, NW>); break;
+    auto go = [&](auto kern, int nw) {
+      static std::set<const void *> attr;                          // once per instance
+      if (attr.insert((const void *)kern).second)
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024));   // room for the static block info
+      kern<<<dim3(S.nblk, nr), 32 * (nw + 1), smem, ctx->stream>>>(Rg, mode, x, tmp, doneflag);
+    };
+    auto by_w = [&](auto nwc, auto nbc) {
+      constexpr int NW = decltype(nwc)::value, NB = decltype(nbc)::value;
+      switch (S.reg_w) {
+        case 4: go(k_tri_reg<D, 4, NW, NB>, NW); break;
+        case 8: go(k_tri_reg<D, 8, NW, NB>, NW); break;
+        case 10: go(k_tri_reg<D, 10, NW, NB>, NW); break;
+        case 12: go(k_tri_reg<D, 12, NW, NB>, NW); break;
+        default: go(k_tri_reg<D, 16, NW, NB>, NW); break;
+      }
+    };
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    // (NW + 1) warps a multiple of 4; two record buffers where the register
+    // budget of NW + 1 warps holds them, one for the wide variants (measured, C5/C4)
+    if constexpr (sizeof(D) == 8) {
+      if (S.reg_nw == 23) by_w(std::integral_constant<int, 23>{}, I1{});
+      else by_w(std::integral_constant<int, 15>{}, I2{});
+    } else {
+      if (S.reg_nw == 15) by_w(std::integral_constant<int, 15>{}, I1{});
+      else by_w(std::integral_constant<int, 7>{}, I2{});
     }
     CK(cudaGetLastError());
     return;

@@ -582,13 +582,15 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
 // sweep (level order) go round-robin to the consumer warps: slice s -> warp
 // s mod NW, so a warp's next slice is NW slices on and its record (values,
 // 16-bit ring slots, output position, 1/u_ii) is loaded straight into registers
-// two slices ahead — no shared-memory staging of the factor stream, whose
-// 128 B/clk port was the floor of k_tri_pipe.  Levels are separated by one
-// named barrier among the consumer warps; a dependency is a shared-memory load
-// from the ring of the last `ring` solution values (the setup proves every
-// dependency is still in the window, RegPack::far == 0).  The helper warp keeps
-// the records of the next REG_L2_AHEAD levels in L2 (cp.async.bulk.prefetch.L2),
-// paced by the level counter the consumers publish.
+// right after the warp's current slice — no shared-memory staging of the factor
+// stream, whose 128 B/clk port was the floor of k_tri_pipe.  Levels are
+// separated by named barriers among the consumer warps; a dependency is a
+// shared-memory load from the ring of the last `ring` solution values (the
+// setup proves every dependency is still in the window, RegPack::far == 0).
+// The helper warp keeps the records of the next REG_L2_AHEAD levels in L2
+// (cp.async.bulk.prefetch.L2), paced by the level counter the consumers publish.
+// NB record buffers per warp (2, or 1 for the wide NW = 23 variant whose
+// register budget is 80).
 // DOWN: x[rows] = U^-1 L^-1 rhs (rhsL = rhs packed in L order by k_pack_rhs)
 // UP:   x[rows] -= U^-1 L^-1 (F_l y_J) (rhsL = F_l y_J packed by k_pack_rhs)
 // The L results go to `mid` at their packed U position: the U sweep's right-hand
@@ -611,6 +613,11 @@ struct RegDev {
   long long ldx, rsL, rsU;
 };
 constexpr int REG_L2_AHEAD = 12;
+#ifdef GEMSLR_TRACE
+constexpr bool kRegTrace = true;         // clock64 trace of block 0 (tools/trace_reg.py; build with GEMSLR_TRACE=1)
+#else
+constexpr bool kRegTrace = false;
+#endif
 template <typename T> __host__ __device__ inline size_t reg_smem_bytes(int ring, int max_slices) {
   return (size_t)ring * sizeof(T) + 16 + (((size_t)max_slices * 2 + 15) & ~(size_t)15);
 }
@@ -621,10 +628,11 @@ __device__ inline void prefetch_l2_bulk(const void *p, unsigned bytes) {
 }
 // Level v of a sweep ends at named barrier 1 + v % 15 (15 ids in rotation).
 // A warp that computes in level v + 1 SYNCS there (arrive + wait); every other
-// warp only ARRIVES (bar.arrive, no wait) — right after its last slice of level
-// v, so its prefetch loads and global stores overlap the following levels.  A warp can
-// run at most NW - 1 levels ahead of the slowest (its next slice is NW slices
-// on), so with NW <= 15 no barrier id is reused before its instance completes.
+// warp only ARRIVES (bar.arrive, no wait) — right after its slice, before its
+// global stores and record loads, so those overlap the following levels.  A
+// warp may arrive at level v only once instance v - 15 of the id is complete:
+// with NW <= 15 that always holds (a warp runs at most NW - 1 levels ahead);
+// wider variants sync instead of arriving when they would get further ahead.
 template <int NW> __device__ inline void reg_arrive(int v) {
   asm volatile("bar.arrive %0, %1;" ::"r"(1 + v % 15), "n"(32 * NW) : "memory");
 }
@@ -651,15 +659,6 @@ struct RegBuf {
   T rhs, dg;
   int out;
   __device__ T val(int e) const { return vec_get<T>(v[e / VE], e % VE); }
-  // Wait here for this buffer's loads.  ptxas puts all prefetch loads on one
-  // scoreboard slot, and a read of a loaded register waits for EVERY load on
-  // that slot; settling the next buffer before the other one is refilled
-  // keeps the two-slice prefetch depth (the wait then covers only this
-  // buffer's loads, issued a slice earlier, after this warp's barrier arrival).
-  __device__ void settle() const {
-    unsigned long long t;
-    asm volatile("mov.b64 %0, %1;" : "=l"(t) : "l"(__double_as_longlong(v[0].x)));
-  }
   __device__ unsigned slot(int e) const {
     const uint4 &q = c[e / 8];
     const int k = (e % 8) / 2;
@@ -668,7 +667,7 @@ struct RegBuf {
   }
 };
 
-template <typename T, int W, int NW>
+template <typename T, int W, int NW, int NB = 2>
 __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
                                                             const int *__restrict__ done) {
   if (done && *done) return;
@@ -723,7 +722,6 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
     }
     return;
   }
-  static_assert(NW <= 15, "barrier ids rotate over 15 named barriers");
   using Buf = RegBuf<T, W>;
   constexpr int NV = Buf::NV, W8 = Buf::W8;
   int base_lev = 0;                                                // levels of earlier sweeps (for prog)
@@ -753,15 +751,32 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
         B.rhs = ld_nc(P.rhsL + ri);
       }
     };
-    int cur = 0;
+    // Level barriers.  cur = the next level this warp has not yet arrived at;
+    // known = the last level it saw complete.  Level v ends at named barrier
+    // 1 + v % 15, so arriving at v needs instance v - 15 complete (known >= v - 15):
+    // with NW <= 15 that always holds (a warp is at most NW - 1 levels ahead);
+    // with more warps a warp that would get further ahead syncs instead.
+    int cur = 0, known = -1;
+    auto pass = [&](bool may_block) {                              // arrive at level cur (no slice of this warp in it)
+      if (NW > 15 && cur - known >= 15) {
+        if (!may_block) return false;
+        reg_sync<NW>(cur);
+        known = cur;
+      } else {
+        reg_arrive<NW>(cur);
+      }
+      ++cur;
+      return true;
+    };
     auto compute = [&](const Buf &B, int s) {
-      const bool tr = P.dbg && blockIdx.x == 0 && lane == 0 && s < 2048;
+      const bool tr = kRegTrace && P.dbg && blockIdx.x == 0 && lane == 0 && s < 2048;
       long long *tp = tr ? P.dbg + 8 * (sw * 2048 + s) : nullptr;
       if (tr) { tp[0] = clock64(); tp[7] = warp; }
       const int lv = lvt[lvbase + s];
-      for (; cur < lv - 1; ++cur) reg_arrive<NW>(cur);             // levels with no slice of this warp
+      while (cur < lv - 1) pass(true);                             // levels with no slice of this warp
       if (cur < lv) {                                               // wait for level lv - 1 to complete
         reg_sync<NW>(cur);
+        known = cur;
         ++cur;
         if (warp == 0 && lane == 0) *prog = base_lev + cur;
       }
@@ -784,12 +799,14 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
       if (tr) { const double pr = dabs2(acc); tp[1] = clock64() + (pr != pr ? 1 : 0); }
       if (upper) acc = acc * B.dg;
       if (B.out >= 0) ring[(s * 32 + lane) & (R - 1)] = acc;
-      // done with level lv: signal without waiting, unless this warp's next
-      // slice is in level lv + 1 (then its next compute syncs at barrier lv);
-      // the global stores below are read only after the sweep-transition barrier
-      if (s + NW >= ns || lvt[lvbase + s + NW] > lv + 1) {
-        reg_arrive<NW>(lv);
-        cur = lv + 1;
+      // Done with level lv: arrive now at lv and at every later level before
+      // this warp's next slice's (bar.arrive does not wait), so the stores and
+      // the record loads below never delay a level; the level right before the
+      // next slice's is synced on in the next compute.  The global stores are
+      // read only after the sweep-transition barrier.
+      {
+        const int nxt = s + NW < ns ? lvt[lvbase + s + NW] : nlev;
+        while (cur < nxt - 1 && pass(false)) {}
       }
       if (B.out >= 0) {
         if (!upper) P.mid[B.out] = acc;
@@ -798,23 +815,29 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
       }
       if (tr) tp[3] = clock64();
     };
-    // slices s (buffer A) and s + NW (B) in registers
-    int s = warp;
+    // One record buffer per warp, refilled right after its slice with the
+    // warp's next slice (NW slices on).  ptxas tracks every global load on one
+    // scoreboard and the first read of a loaded register waits for all of them,
+    // so a second buffer would not deepen the prefetch: the lead is one slice
+    // period of the warp, which more consumer warps lengthen (NW > 15 for
+    // stages with many slices per level).
     Buf A, B;
+    int s = warp;
     load(A, s);
-    load(B, s + NW);
+    if (NB == 2) load(B, s + NW);
+#pragma unroll 1
     while (s < ns) {
       compute(A, s);
-      if (s + NW < ns) B.settle();
-      load(A, s + 2 * NW);
+      load(A, s + NB * NW);
       s += NW;
-      if (s >= ns) break;
-      compute(B, s);
-      if (s + NW < ns) A.settle();
-      load(B, s + 2 * NW);
-      s += NW;
+      if (NB == 2) {
+        if (s >= ns) break;
+        compute(B, s);
+        load(B, s + 2 * NW);
+        s += NW;
+      }
     }
-    for (; cur < nlev; ++cur) reg_arrive<NW>(cur);
+    while (cur < nlev) pass(true);
     base_lev += nlev;
     __threadfence_block();
     reg_sync_all<NW>();                                            // sweep transition: mid / tmp visible, ring free
