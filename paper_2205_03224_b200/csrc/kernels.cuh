@@ -589,8 +589,8 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
 // setup proves every dependency is still in the window, RegPack::far == 0).
 // The helper warp keeps the records of the next REG_L2_AHEAD levels in L2
 // (cp.async.bulk.prefetch.L2), paced by the level counter the consumers publish.
-// NB record buffers per warp (2, or 1 for the wide NW = 23 variant whose
-// register budget is 80).
+// NB record buffers per warp (see the slice loop): 2 with NW = 15, or 1 with
+// the wide NW = 23 variant, whose register budget is 80.
 // DOWN: x[rows] = U^-1 L^-1 rhs (rhsL = rhs packed in L order by k_pack_rhs)
 // UP:   x[rows] -= U^-1 L^-1 (F_l y_J) (rhsL = F_l y_J packed by k_pack_rhs)
 // The L results go to `mid` at their packed U position: the U sweep's right-hand
@@ -667,7 +667,7 @@ struct RegBuf {
   }
 };
 
-template <typename T, int W, int NW, int NB = 2>
+template <typename T, int W, int NW, int NB>
 __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
                                                             const int *__restrict__ done) {
   if (done && *done) return;
@@ -754,8 +754,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
     // Level barriers.  cur = the next level this warp has not yet arrived at;
     // known = the last level it saw complete.  Level v ends at named barrier
     // 1 + v % 15, so arriving at v needs instance v - 15 complete (known >= v - 15):
-    // with NW <= 15 that always holds (a warp is at most NW - 1 levels ahead);
-    // with more warps a warp that would get further ahead syncs instead.
+    // with NW <= 15 that always holds (a warp's next slice is NW slices on, so
+    // it is at most NW - 1 levels ahead); with more warps a warp that would get
+    // further ahead syncs instead of arriving.
     int cur = 0, known = -1;
     auto pass = [&](bool may_block) {                              // arrive at level cur (no slice of this warp in it)
       if (NW > 15 && cur - known >= 15) {
@@ -768,11 +769,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
       ++cur;
       return true;
     };
-    auto compute = [&](const Buf &B, int s) {
-      const bool tr = kRegTrace && P.dbg && blockIdx.x == 0 && lane == 0 && s < 2048;
-      long long *tp = tr ? P.dbg + 8 * (sw * 2048 + s) : nullptr;
-      if (tr) { tp[0] = clock64(); tp[7] = warp; }
-      const int lv = lvt[lvbase + s];
+    auto wait_level = [&](int lv) {                                // this warp computes in level lv next
       while (cur < lv - 1) pass(true);                             // levels with no slice of this warp
       if (cur < lv) {                                               // wait for level lv - 1 to complete
         reg_sync<NW>(cur);
@@ -780,7 +777,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
         ++cur;
         if (warp == 0 && lane == 0) *prog = base_lev + cur;
       }
-      if (tr) { const int pv = *prog; tp[2] = clock64() + (pv == -7 ? 1 : 0); tp[6] = lv; }
+    };
+    // x_i = (rhs_i - sum_j a_ij x_j) [/ u_ii]: W ring gathers, four partial sums
+    auto solve = [&](const Buf &B, int s) {
+      const bool tr = kRegTrace && P.dbg && blockIdx.x == 0 && lane == 0 && s < 2048;
+      long long *tp = tr ? P.dbg + 8 * (sw * 2048 + s) : nullptr;
+      if (tr) { const int pv = *prog; tp[2] = clock64() + (pv == -7 ? 1 : 0); tp[6] = lvt[lvbase + s]; tp[7] = warp; tp[0] = tp[2]; }
       if (tr) {
         const double pr = dabs2(B.val(0)) + dabs2(B.val(W - 1)) + (double)B.slot(0) + (double)B.slot(W - 1) + dabs2(B.rhs);
         tp[4] = clock64() + (pr != pr ? 1 : 0);
@@ -796,43 +798,57 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
         if (e + 3 < W) a3 -= B.val(e + 3) * ring[B.slot(e + 3)];
       }
       acc = (acc + a1) + (a2 + a3);
-      if (tr) { const double pr = dabs2(acc); tp[1] = clock64() + (pr != pr ? 1 : 0); }
+      if (tr) { const double pr = dabs2(acc); tp[1] = clock64() + (pr != pr ? 1 : 0); tp[3] = tp[1]; }
       if (upper) acc = acc * B.dg;
+      return acc;
+    };
+    auto publish = [&](const Buf &B, int s, const T &acc) {
       if (B.out >= 0) ring[(s * 32 + lane) & (R - 1)] = acc;
-      // Done with level lv: arrive now at lv and at every later level before
-      // this warp's next slice's (bar.arrive does not wait), so the stores and
-      // the record loads below never delay a level; the level right before the
-      // next slice's is synced on in the next compute.  The global stores are
-      // read only after the sweep-transition barrier.
-      {
-        const int nxt = s + NW < ns ? lvt[lvbase + s + NW] : nlev;
-        while (cur < nxt - 1 && pass(false)) {}
-      }
+    };
+    // Done with the current level: arrive now at it and at every later level
+    // before the level of this warp's next slice nx (bar.arrive does not wait),
+    // so the stores and the record loads that follow never delay a level; the
+    // level right before nx's is synced on when nx is computed.
+    auto depart = [&](int nx) {
+      const int nxt = nx < ns ? lvt[lvbase + nx] : nlev;
+      while (cur < nxt - 1 && pass(false)) {}
+    };
+    // The global stores are read only after the sweep-transition barrier.
+    auto store = [&](const Buf &B, const T &acc) {
       if (B.out >= 0) {
         if (!upper) P.mid[B.out] = acc;
         else if (mode == TRI_UP) tmp[B.out] = acc;                 // x -= tmp after the sweep
         else x[B.out] = acc;
       }
-      if (tr) tp[3] = clock64();
     };
-    // One record buffer per warp, refilled right after its slice with the
-    // warp's next slice (NW slices on).  ptxas tracks every global load on one
+    // The warp's slices are NW apart.  Its record loads are issued right after
+    // a slice and waited for at the next: ptxas tracks every global load on one
     // scoreboard and the first read of a loaded register waits for all of them,
-    // so a second buffer would not deepen the prefetch: the lead is one slice
-    // period of the warp, which more consumer warps lengthen (NW > 15 for
-    // stages with many slices per level).
+    // so the prefetch lead is about one slice period of the warp whatever the
+    // buffering; more consumer warps lengthen it.  NB = 1: one buffer, refilled
+    // with the next slice (the NW = 23 variant, 80 registers).  NB = 2: two
+    // buffers alternating, refilled two slices ahead (NW = 15; measured best
+    // for stages with 1-2 slices per level).
     Buf A, B;
     int s = warp;
     load(A, s);
     if (NB == 2) load(B, s + NW);
 #pragma unroll 1
     while (s < ns) {
-      compute(A, s);
+      wait_level(lvt[lvbase + s]);
+      const T a0 = solve(A, s);
+      publish(A, s, a0);
+      depart(s + NW);
+      store(A, a0);
       load(A, s + NB * NW);
       s += NW;
       if (NB == 2) {
         if (s >= ns) break;
-        compute(B, s);
+        wait_level(lvt[lvbase + s]);
+        const T a1 = solve(B, s);
+        publish(B, s, a1);
+        depart(s + NW);
+        store(B, a1);
         load(B, s + 2 * NW);
         s += NW;
       }
