@@ -755,7 +755,7 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
       static std::set<const void *> attr;                          // once per instance
       if (attr.insert((const void *)kern).second)
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024));   // room for the static block info
-      kern<<<dim3(S.nblk, nr), 32 * (nw + 1), smem, ctx->stream>>>(Rg, mode, x, tmp, doneflag);
+      kern<<<dim3(S.nblk, nr), 32 * nw, smem, ctx->stream>>>(Rg, mode, x, tmp, doneflag);
     };
     auto by_w = [&](auto nwc, auto nbc) {
       constexpr int NW = decltype(nwc)::value, NB = decltype(nbc)::value;
@@ -769,8 +769,8 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
     };
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
-    // (NW + 1) warps a multiple of 4; two record buffers where the register
-    // budget of NW + 1 warps holds them, one for the wide variants (measured, C5/C4)
+    // two record buffers where the register budget of NW warps holds them, one
+    // for the wide variants (measured, C5/C4)
     if constexpr (sizeof(D) == 8) {
       if (S.reg_nw == 23) by_w(std::integral_constant<int, 23>{}, I1{});
       else by_w(std::integral_constant<int, 15>{}, I2{});

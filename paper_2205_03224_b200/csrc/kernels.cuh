@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
 }
 
 // ----------------------------------------------------------------- K4/K5/K9 register-prefetched
-// One CTA per block, NW consumer warps + one L2-prefetch warp.  The slices of a
+// One CTA per block, NW warps.  The slices of a
 // sweep (level order) go round-robin to the consumer warps: slice s -> warp
 // s mod NW, so a warp's next slice is NW slices on and its record (values,
 // 16-bit ring slots, output position, 1/u_ii) is loaded straight into registers
@@ -587,10 +587,10 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
 // separated by named barriers among the consumer warps; a dependency is a
 // shared-memory load from the ring of the last `ring` solution values (the
 // setup proves every dependency is still in the window, RegPack::far == 0).
-// The helper warp keeps the records of the next REG_L2_AHEAD levels in L2
-// (cp.async.bulk.prefetch.L2), paced by the level counter the consumers publish.
+// (An L2-prefetch helper warp, paced by a level counter, was measured: no gain
+// on level 0 and 1.8x slower levels 1/2 of C5 while it polls; removed.)
 // NB record buffers per warp (see the slice loop): 2 with NW = 15, or 1 with
-// the wide NW = 23 variant, whose register budget is 80.
+// the wide NW = 23 variant, whose register budget is 88.
 // DOWN: x[rows] = U^-1 L^-1 rhs (rhsL = rhs packed in L order by k_pack_rhs)
 // UP:   x[rows] -= U^-1 L^-1 (F_l y_J) (rhsL = F_l y_J packed by k_pack_rhs)
 // The L results go to `mid` at their packed U position: the U sweep's right-hand
@@ -606,13 +606,12 @@ struct RegDev {
   T *mid;
   int ring;
   long long *dbg;          // debug trace (block 0): 8 words per slice, 2048 slices per sweep
-  int flags;               // bit 0: no L2 prefetch helper (experiments)
+  int flags;               // experiment bits (GEMSLR_REG_FLAGS), 0 in production
   int max_slices;          // L + U records of the largest block (shared-memory level table)
   // several right-hand sides (NEXT-4): column blockIdx.y works on x/tmp + col*ldx
   // and rhsL/mid + col*rs (0 for one column); the factor records are shared
   long long ldx, rsL, rsU;
 };
-constexpr int REG_L2_AHEAD = 12;
 #ifdef GEMSLR_TRACE
 constexpr bool kRegTrace = true;         // clock64 trace of block 0 (tools/trace_reg.py; build with GEMSLR_TRACE=1)
 #else
@@ -623,9 +622,6 @@ template <typename T> __host__ __device__ inline size_t reg_smem_bytes(int ring,
 }
 constexpr int REG_BINFO = 12;            // ints per block in RegDev::binfo (= REG_BINFO_INTS)
 
-__device__ inline void prefetch_l2_bulk(const void *p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 // Level v of a sweep ends at named barrier 1 + v % 15 (15 ids in rotation).
 // A warp that computes in level v + 1 SYNCS there (arrive + wait); every other
 // warp only ARRIVES (bar.arrive, no wait) — right after its slice, before its
@@ -638,6 +634,12 @@ template <int NW> __device__ inline void reg_arrive(int v) {
 }
 template <int NW> __device__ inline void reg_sync(int v) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + v % 15), "n"(32 * NW) : "memory");
+}
+template <int NW> __device__ inline void reg_arrive_id(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(32 * NW) : "memory");
+}
+template <int NW> __device__ inline void reg_sync_id(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(32 * NW) : "memory");
 }
 template <int NW> __device__ inline void reg_sync_all() { asm volatile("bar.sync 0, %0;" ::"n"(32 * NW) : "memory"); }
 
@@ -668,7 +670,7 @@ struct RegBuf {
 };
 
 template <typename T, int W, int NW, int NB>
-__global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
+__global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
                                                             const int *__restrict__ done) {
   if (done && *done) return;
   if (blockIdx.y) {                                                // right-hand side column blockIdx.y (NEXT-4)
@@ -679,7 +681,6 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
   }
   extern __shared__ __align__(128) unsigned char smem[];
   T *ring = reinterpret_cast<T *>(smem);
-  volatile int *prog = reinterpret_cast<volatile int *>(smem + (size_t)P.ring * sizeof(T));
   unsigned short *lvt = reinterpret_cast<unsigned short *>(smem + (size_t)P.ring * sizeof(T) + 16);
   const int R = P.ring;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -705,26 +706,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
     for (; i < nl; i += nt) lvt[i] = P.slev[f + i];
   }
   for (int i = tid; i < R; i += blockDim.x) ring[i] = dzero<T>();
-  if (tid == 0) *prog = 0;
   __syncthreads();
   const size_t RB = (size_t)P.rec_bytes;
-  if (warp == NW) {                                                // ---- L2 prefetch helper (one lane)
-    if (lane != 0 || (P.flags & 1)) return;
-    int passed = 0;                                                // levels issued over both sweeps
-    for (int sw = 0; sw < 2; ++sw) {
-      const int nlev = bi[3 * sw + 2];
-      const int *lo = P.lev_off + bi[6 + sw];
-      for (int v = 0; v < nlev; ++v, ++passed) {
-        while (passed > *prog + REG_L2_AHEAD) __nanosleep(200);
-        const long long a = (long long)lo[v] * (long long)RB, e = (long long)lo[v + 1] * (long long)RB;
-        for (long long q = a; q < e; q += 65536) prefetch_l2_bulk(P.data + q, (unsigned)min(65536LL, e - q));
-      }
-    }
-    return;
-  }
   using Buf = RegBuf<T, W>;
   constexpr int NV = Buf::NV, W8 = Buf::W8;
-  int base_lev = 0;                                                // levels of earlier sweeps (for prog)
 #pragma unroll 1
   for (int sw = 0; sw < 2; ++sw) {
     const bool upper = sw == 1;
@@ -757,32 +742,34 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
     // with NW <= 15 that always holds (a warp's next slice is NW slices on, so
     // it is at most NW - 1 levels ahead); with more warps a warp that would get
     // further ahead syncs instead of arriving.
-    int cur = 0, known = -1;
+    // cid = 1 + cur % 15, kept incrementally (no division on the critical path).
+    int cur = 0, known = -1, cid = 1;
     auto pass = [&](bool may_block) {                              // arrive at level cur (no slice of this warp in it)
       if (NW > 15 && cur - known >= 15) {
         if (!may_block) return false;
-        reg_sync<NW>(cur);
+        reg_sync_id<NW>(cid);
         known = cur;
       } else {
-        reg_arrive<NW>(cur);
+        reg_arrive_id<NW>(cid);
       }
       ++cur;
+      cid = cid == 15 ? 1 : cid + 1;
       return true;
     };
     auto wait_level = [&](int lv) {                                // this warp computes in level lv next
       while (cur < lv - 1) pass(true);                             // levels with no slice of this warp
       if (cur < lv) {                                               // wait for level lv - 1 to complete
-        reg_sync<NW>(cur);
+        reg_sync_id<NW>(cid);
         known = cur;
         ++cur;
-        if (warp == 0 && lane == 0) *prog = base_lev + cur;
+        cid = cid == 15 ? 1 : cid + 1;
       }
     };
     // x_i = (rhs_i - sum_j a_ij x_j) [/ u_ii]: W ring gathers, four partial sums
     auto solve = [&](const Buf &B, int s) {
       const bool tr = kRegTrace && P.dbg && blockIdx.x == 0 && lane == 0 && s < 2048;
       long long *tp = tr ? P.dbg + 8 * (sw * 2048 + s) : nullptr;
-      if (tr) { const int pv = *prog; tp[2] = clock64() + (pv == -7 ? 1 : 0); tp[6] = lvt[lvbase + s]; tp[7] = warp; tp[0] = tp[2]; }
+      if (tr) { tp[2] = clock64(); tp[6] = lvt[lvbase + s]; tp[7] = warp; tp[0] = tp[2]; }
       if (tr) {
         const double pr = dabs2(B.val(0)) + dabs2(B.val(W - 1)) + (double)B.slot(0) + (double)B.slot(W - 1) + dabs2(B.rhs);
         tp[4] = clock64() + (pr != pr ? 1 : 0);
@@ -806,13 +793,16 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
       if (B.out >= 0) ring[(s * 32 + lane) & (R - 1)] = acc;
     };
     // Done with the current level: arrive now at it and at every later level
-    // before the level of this warp's next slice nx (bar.arrive does not wait),
+    // before nxt, the level of this warp's next slice (bar.arrive does not wait),
     // so the stores and the record loads that follow never delay a level; the
     // level right before nx's is synced on when nx is computed.
-    auto depart = [&](int nx) {
-      const int nxt = nx < ns ? lvt[lvbase + nx] : nlev;
-      while (cur < nxt - 1 && pass(false)) {}
+    auto depart = [&](int nxt) {
+      if (cur < nxt - 1 && pass(false)) {                          // the current level: straight-line arrival
+#pragma unroll 1
+        while (cur < nxt - 1 && pass(false)) {}
+      }
     };
+    auto level_of = [&](int t) { return t < ns ? (int)lvt[lvbase + t] : nlev; };
     // The global stores are read only after the sweep-transition barrier.
     auto store = [&](const Buf &B, const T &acc) {
       if (B.out >= 0) {
@@ -835,29 +825,29 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_tri_reg(RegDev<T> P, int m
     if (NB == 2) load(B, s + NW);
 #pragma unroll 1
     while (s < ns) {
+      int nxt = level_of(s + NW);                                  // read before the barrier: off the critical path
       wait_level(lvt[lvbase + s]);
       const T a0 = solve(A, s);
       publish(A, s, a0);
-      depart(s + NW);
+      depart(nxt);
       store(A, a0);
       load(A, s + NB * NW);
       s += NW;
       if (NB == 2) {
         if (s >= ns) break;
+        nxt = level_of(s + NW);
         wait_level(lvt[lvbase + s]);
         const T a1 = solve(B, s);
         publish(B, s, a1);
-        depart(s + NW);
+        depart(nxt);
         store(B, a1);
         load(B, s + 2 * NW);
         s += NW;
       }
     }
     while (cur < nlev) pass(true);
-    base_lev += nlev;
     __threadfence_block();
     reg_sync_all<NW>();                                            // sweep transition: mid / tmp visible, ring free
-    if (warp == 0 && lane == 0) *prog = base_lev;
   }
   if (mode == TRI_UP) {                                            // y1 = z1 - U^-1 L^-1 F y2 (Alg. 2 l.9)
     constexpr int U = 8;                                           // 8 independent rows in flight per thread
