@@ -66,6 +66,16 @@ __device__ inline cd ld_cg(const cd *p) {
   return {v.x, v.y};
 }
 __device__ inline double ld_nc(const double *p) { return __ldg(p); }
+__device__ inline double2 ld_na(const double2 *p) {             // read-only, no L1 allocation
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ inline uint4 ld_na(const uint4 *p) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
 __device__ inline cd ld_nc(const cd *p) {
   double2 v = __ldg(reinterpret_cast<const double2 *>(p));
   return {v.x, v.y};
@@ -724,9 +734,9 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
       const uint4 *cp = reinterpret_cast<const uint4 *>(rec + (size_t)W * 32 * sizeof(T)) + lane;
       const int *op = reinterpret_cast<const int *>(rec + (size_t)W * 32 * sizeof(T) + (size_t)W8 * 512);   // out[]
 #pragma unroll
-      for (int k = 0; k < NV; ++k) B.v[k] = __ldg(vp + 32 * k);
+      for (int k = 0; k < NV; ++k) B.v[k] = ld_na(vp + 32 * k);   // streamed once: no L1 allocation (-3 % on C5 level 0)
 #pragma unroll
-      for (int j = 0; j < W8; ++j) B.c[j] = __ldg(cp + 32 * j);
+      for (int j = 0; j < W8; ++j) B.c[j] = ld_na(cp + 32 * j);
       B.out = __ldg(op + lane);
       const size_t ri = (size_t)(gbase + s) * 32 + lane;
       if (upper) {

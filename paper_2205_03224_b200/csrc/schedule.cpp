@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // Level schedules of the triangular substitutions (built once at setup) and
 // their SELL-32 packing for the sm_100a trisolve kernel.
 //
@@ -52,6 +54,22 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
     {
       std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
       for (int64_t i = 0; i < n; ++i) rows[pos[lev[i]]++] = i;
+    }
+    if (upper) {
+      // Inside a U level, order the rows by their L level (ascending row within
+      // it), the order of the L packing: the rows of one L slice that share a U
+      // level become adjacent in the U packing, so the L sweep's stores of its
+      // results at their U positions coalesce.  Any order inside a level is valid.
+      const Csr<T> &Lm = fac[b].L;
+      std::vector<int32_t> ll(n, 0);
+      for (int64_t i = 0; i < n; ++i) {
+        int32_t v = 0;
+        for (int64_t p = Lm.ptr[i]; p < Lm.ptr[i + 1]; ++p) v = std::max(v, ll[Lm.col[p]] + 1);
+        ll[i] = v;
+      }
+      for (int32_t v = 0; v < nlev; ++v)
+        std::stable_sort(rows.begin() + cnt[v], rows.begin() + cnt[v + 1],
+                         [&](int64_t a, int64_t c) { return ll[a] < ll[c]; });
     }
     auto len = [&](int64_t i) { return M.ptr[i + 1] - M.ptr[i]; };
     (void)len;
