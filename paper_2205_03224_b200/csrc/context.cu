@@ -1186,8 +1186,9 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
     // count up to 32 columns (≈ 90 % of HBM), the column-split k_gs from 33 to
     // 48, the half-warp k_gs2h above (k_gs <1,13> is 2x slower there)
     done2 = true;
-    if (ncols <= 8) go2(k_gs2<D, 8>);
-    else if (ncols <= 16) go2(k_gs2<D, 16>);
+    constexpr int TU8 = sizeof(D) == 8 ? 4 : 1, TU16 = sizeof(D) == 8 ? 2 : 1;   // tiles in flight per warp (complex: registers)
+    if (ncols <= 8) go2(k_gs2<D, 8, TU8, true>);
+    else if (ncols <= 16) go2(k_gs2<D, 16, TU16, true>);
     else if (ncols <= 24) go2(k_gs2<D, 24>);
     else if (ncols <= 32) go2(k_gs2<D, 32>);
     else if constexpr (sizeof(D) == 8) {

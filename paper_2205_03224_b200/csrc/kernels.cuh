@@ -1286,58 +1286,96 @@ __device__ inline void tbfly32(T (&x)[32], int lane) {              // lane i <-
     }
   }
 }
-template <typename T, int NC>
-__global__ void __launch_bounds__(256, NC * sizeof(T) > 256 ? 1 : 2) k_gs2(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
+// TU tiles per warp iteration (their loads all in flight: with few columns one
+// tile is too little memory-level parallelism — k_gs2<8> ran at 0.7-3 TB/s with
+// TU = 1).  LA: the dots are accumulated per lane over all of the warp's tiles
+// and reduced over the lanes once at the end (NC <= 16, registers allow); else
+// the transpose butterfly per TU tiles.
+template <typename T, int NC, int TU = 1, bool LA = false>
+__global__ void __launch_bounds__(256, NC * TU * sizeof(T) > 256 ? 1 : 2) k_gs2(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
                                               int dot, const T *__restrict__ h_in, T *__restrict__ partial,
                                               unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
   if (done && *done) return;
-  constexpr int NCH = (NC + 31) / 32;                              // 32-column butterfly chunks
+  constexpr int NCH = LA ? 0 : (NC + 31) / 32;                     // 32-column butterfly chunks
+  constexpr int NA = LA ? NC : 1;                                  // per-lane accumulators
   __shared__ T sh[NC];
   __shared__ T red[8][NC + 1];
   __shared__ bool amlast;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int c = tid; c < NC; c += blockDim.x) sh[c] = (upd && c < ncols) ? h_in[c] : dzero<T>();
   __syncthreads();
-  T acc[NCH];
+  T acc[NCH > 0 ? NCH : 1];
 #pragma unroll
-  for (int q = 0; q < NCH; ++q) acc[q] = dzero<T>();
+  for (int q = 0; q < (NCH > 0 ? NCH : 1); ++q) acc[q] = dzero<T>();
+  T la[NA];
+#pragma unroll
+  for (int c = 0; c < NA; ++c) la[c] = dzero<T>();
   double nrm = 0.0;
   const int64_t ntiles = (n + 31) / 32;
-  for (int64_t tile = (int64_t)blockIdx.x * 8 + warp; tile < ntiles; tile += (int64_t)gridDim.x * 8) {
-    const int64_t r = tile * 32 + lane;
-    const bool ok = r < n;
-    T v[NC];
+  for (int64_t t0 = ((int64_t)blockIdx.x * 8 + warp) * TU; t0 < ntiles; t0 += (int64_t)gridDim.x * 8 * TU) {
+    T v[TU][NC], wi[TU];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) v[c] = (c < ncols && ok) ? ld_nc(V + c * ldv + r) : dzero<T>();
-    T wi = ok ? w[r] : dzero<T>();
-    if (upd) {
-      T u0 = dzero<T>(), u1 = dzero<T>();
+    for (int u = 0; u < TU; ++u) {
+      const int64_t r = (t0 + u) * 32 + lane;
+      const bool ok = r < n;
 #pragma unroll
-      for (int c = 0; c < NC; c += 2) {
-        u0 += v[c] * sh[c];
-        if (c + 1 < NC) u1 += v[c + 1 < NC ? c + 1 : 0] * sh[c + 1 < NC ? c + 1 : 0];
-      }
-      wi = wi - (u0 + u1);
-      if (ok) w[r] = wi;
+      for (int c = 0; c < NC; ++c) v[u][c] = (c < ncols && ok) ? ld_nc(V + c * ldv + r) : dzero<T>();
+      wi[u] = ok ? w[r] : dzero<T>();
     }
-    nrm += dabs2(wi);
+#pragma unroll
+    for (int u = 0; u < TU; ++u) {
+      const int64_t r = (t0 + u) * 32 + lane;
+      if (upd) {
+        T u0 = dzero<T>(), u1 = dzero<T>();
+#pragma unroll
+        for (int c = 0; c < NC; c += 2) {
+          u0 += v[u][c] * sh[c];
+          if (c + 1 < NC) u1 += v[u][c + 1 < NC ? c + 1 : 0] * sh[c + 1 < NC ? c + 1 : 0];
+        }
+        wi[u] = wi[u] - (u0 + u1);
+        if (r < n) w[r] = wi[u];
+      }
+      nrm += dabs2(wi[u]);
+    }
     if (dot) {
+      if constexpr (LA) {
 #pragma unroll
-      for (int q = 0; q < NCH; ++q) {
-        T x[32];
+        for (int u = 0; u < TU; ++u)
 #pragma unroll
-        for (int k = 0; k < 32; ++k) x[k] = (32 * q + k < NC) ? dconj(v[32 * q + k < NC ? 32 * q + k : 0]) * wi : dzero<T>();
-        tbfly32(x, lane);
-        acc[q] += x[0];
+          for (int c = 0; c < NC; ++c) la[c] += dconj(v[u][c]) * wi[u];
+      } else {
+#pragma unroll
+        for (int q = 0; q < NCH; ++q) {
+          T x[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const int c = 32 * q + k < NC ? 32 * q + k : 0;
+            T t = dzero<T>();
+#pragma unroll
+            for (int u = 0; u < TU; ++u) t += dconj(v[u][c]) * wi[u];
+            x[k] = (32 * q + k < NC) ? t : dzero<T>();
+          }
+          tbfly32(x, lane);
+          acc[q] += x[0];
+        }
       }
     }
   }
-  // lane i of warp w holds column 32 q + i of this warp; warp 0 the norm too
+  // lane i of warp w holds column 32 q + i of this warp (LA: every lane a part of
+  // every column, summed over the lanes here); warp 0 the norm too
   const int nres = dot ? ncols + 1 : 1;
   nrm = warp_sum(nrm);
+  if constexpr (LA) {
 #pragma unroll
-  for (int q = 0; q < NCH; ++q)
-    if (32 * q + lane < NC) red[warp][32 * q + lane] = acc[q];
+    for (int c = 0; c < NC; ++c) {
+      const T t = warp_sum(la[c]);
+      if (lane == c) red[warp][c] = t;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < NCH; ++q)
+      if (32 * q + lane < NC) red[warp][32 * q + lane] = acc[q];
+  }
   if (lane == 0) {
     T t = dzero<T>();
     if constexpr (sizeof(T) == sizeof(double)) t = nrm; else t = T{nrm, 0.0};
