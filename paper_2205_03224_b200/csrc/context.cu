@@ -692,6 +692,25 @@ void Engine<T>::allreduce(D *buf, size_t count) {
 }
 
 // ----------------------------------------------------------------- launches
+// Launch with programmatic stream serialization (PDL): the kernel's CTAs may be
+// scheduled while its predecessor runs; the kernel's pdl_wait() orders its
+// reads after the predecessor (kernels.cuh).  GEMSLR_NO_PDL=1 launches normally.
+template <typename... KA, typename... A>
+static void launch_pdl(void (*kern)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A &&...args) {
+  static const bool on = getenv("GEMSLR_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
+}
+
 static int grid_for(int64_t units, int per_sm) {
   int64_t g = std::min<int64_t>(units, (int64_t)kNumSM * per_sm);
   return (int)std::max<int64_t>(g, 1);
@@ -735,13 +754,14 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
       Timed tp(ctx->prof, ctx->stream, KC_PACK);
       if (mode == TRI_DOWN) {
         const int64_t np = S.lslices * 32;
-        k_pack_gather<D><<<dim3(grid_for((np + 255) / 256, 4), nr), 256, 0, ctx->stream>>>(np, S.lrow, rhs, rL, doneflag,
-                                                                                          ldx, Rg.rsL);
+        launch_pdl(k_pack_gather<D>, dim3(grid_for((np + 255) / 256, 4), nr), dim3(256), 0, ctx->stream, np,
+                   (const int *)S.lrow, rhs, rL, doneflag, (int64_t)ldx, (int64_t)Rg.rsL);
       } else if (S.nf >= 0) {
         Rg.rhsL = rUp;
         if (S.nf > 0)
-          k_pack_f<D><<<dim3(grid_for((S.nf + 255) / 256, 4), nr), 256, 0, ctx->stream>>>(
-              S.nf, S.fpos, S.frow, Fp, Fc, Fv, x, fa.nloc, fa.yh, fa.nh, fa.yl, rUp, doneflag, ldx, Rg.rsL);
+          launch_pdl(k_pack_f<D>, dim3(grid_for((S.nf + 255) / 256, 4), nr), dim3(256), 0, ctx->stream, (int64_t)S.nf,
+                     (const int *)S.fpos, (const int *)S.frow, Fp, Fc, Fv, (const D *)x, (int64_t)fa.nloc, fa.yh,
+                     (int64_t)fa.nh, fa.yl, rUp, doneflag, (int64_t)ldx, (int64_t)Rg.rsL);
       } else {
         k_pack_rhs<D><<<pgrid, 256, 0, ctx->stream>>>(S.rows, S.row0, S.P.lpos, const_cast<D *>(S.Rg.rhsL), nullptr, Fp, Fc,
                                                       Fv, Fbase, x, fa.nloc, fa.yh, fa.nh, fa.yl, doneflag);
@@ -755,7 +775,7 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
       static std::set<const void *> attr;                          // once per instance
       if (attr.insert((const void *)kern).second)
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024));   // room for the static block info
-      kern<<<dim3(S.nblk, nr), 32 * nw, smem, ctx->stream>>>(Rg, mode, x, tmp, doneflag);
+      launch_pdl(kern, dim3(S.nblk, nr), dim3(32 * nw), smem, ctx->stream, Rg, mode, x, tmp, doneflag);
     };
     auto by_w = [&](auto nwc, auto nbc) {
       constexpr int NW = decltype(nwc)::value, NB = decltype(nbc)::value;
@@ -839,11 +859,11 @@ void Engine<T>::spmv(const D *x, D *y, int mode, const D *b, const int *doneflag
     constexpr int SPW = 2;
     const int g2 = (int)std::max<int64_t>((nslices + 8 * SPW - 1) / (8 * SPW), 1);
     if (hA.nrecv > 0)
-      k_spmv_sell2<D, true, SPW, 8><<<g2, 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, hA.rbuf, y,
-                                                                 mode, b, doneflag);
+      launch_pdl(k_spmv_sell2<D, true, SPW, 8>, dim3(g2), dim3(256), 0, ctx->stream, n, nslices, sell_off, sell_col,
+                 sell_val, x, hA.rbuf, y, mode, b, doneflag);
     else
-      k_spmv_sell2<D, false, SPW, 8><<<g2, 256, 0, ctx->stream>>>(n, nslices, sell_off, sell_col, sell_val, x, hA.rbuf, y,
-                                                                  mode, b, doneflag);
+      launch_pdl(k_spmv_sell2<D, false, SPW, 8>, dim3(g2), dim3(256), 0, ctx->stream, n, nslices, sell_off, sell_col,
+                 sell_val, x, hA.rbuf, y, mode, b, doneflag);
     CK(cudaGetLastError());
     return;
   }
@@ -1173,12 +1193,14 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
   // 13 values of V in flight per thread whatever the number of columns
   auto go = [&](auto kern, int tr) {
     const int grid = grid_for((nn + 32 * tr - 1) / (32 * tr), 3);
-    kern<<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv, doneflag);
+    launch_pdl(kern, dim3(grid), dim3(256), 0, ctx->stream, nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial,
+               tickets + ticket, resv, doneflag);
   };
   static const bool old_gs = getenv("GEMSLR_OLD_GS") != nullptr;
   auto go2 = [&](auto kern) {
     const int grid = grid_for((nn + 255) / 256, ncols * (int)sizeof(D) <= 256 ? 2 : 1);
-    kern<<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv, doneflag);
+    launch_pdl(kern, dim3(grid), dim3(256), 0, ctx->stream, nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial,
+               tickets + ticket, resv, doneflag);
   };
   bool done2 = false;
   if (!old_gs) {
@@ -1194,8 +1216,8 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
     else if constexpr (sizeof(D) == 8) {
       if (ncols > 48 && ncols <= 64) {
         const int grid = grid_for((nn + 127) / 128, 2);
-        k_gs2h<D><<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv,
-                                                 doneflag);
+        launch_pdl(k_gs2h<D>, dim3(grid), dim3(256), 0, ctx->stream, nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial,
+                   tickets + ticket, resv, doneflag);
       } else {
         done2 = false;
       }
@@ -1203,8 +1225,8 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
       // complex: lane groups (2 x 32 or 4 x 26 columns per row tile)
       auto go3 = [&](auto kern, int rw) {
         const int grid = grid_for((nn + 8 * rw - 1) / (8 * rw), 1);
-        kern<<<grid, 256, 0, ctx->stream>>>(nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial, tickets + ticket, resv,
-                                            doneflag);
+        launch_pdl(kern, dim3(grid), dim3(256), 0, ctx->stream, nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial,
+                   tickets + ticket, resv, doneflag);
       };
       if (ncols <= 48) done2 = false;                             // k_gs<2,6> measured faster here
       else if (ncols <= 64) go3(k_gs2g<D, 2, 32>, 16);
@@ -1601,8 +1623,8 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
       gs_pass(V, ldv, n, jj + 1, w, 1, 0, res2, res3, 9, done);     // w -= V h2 ; ||w||^2
       {
         Timed t(ctx->prof, st, KC_FGM);                          // Givens column + v_{j+1} = w / h_{j+1}
-        k_fgmres_scale<D><<<grid_for((n + 255) / 256, 4), 256, 0, st>>>(f, m, jj, res1, res2, res3, n, w,
-                                                                        V + (size_t)(jj + 1) * ldv);
+        launch_pdl(k_fgmres_scale<D>, dim3(grid_for((n + 255) / 256, 4)), dim3(256), 0, st, f, m, jj, res1, res2, res3,
+                   n, w, V + (size_t)(jj + 1) * ldv);
         CK(cudaGetLastError());
       }
     };

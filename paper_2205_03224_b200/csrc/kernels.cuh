@@ -21,6 +21,15 @@
 
 namespace gemslr {
 
+// Programmatic dependent launch (the FGMRES iteration's kernels are launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization): a kernel lets its
+// successor's CTAs be scheduled at once and waits for its predecessor's
+// completion (and memory flush) before reading anything it produced.  Both are
+// no-ops for a normal launch.
+__device__ inline void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ inline void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+
 constexpr int PIPE_SB_DEV = 30 * 1024;    // = PIPE_SB
 constexpr int PIPE_NW_DEV = 8;            // = PIPE_NW
 
@@ -128,6 +137,8 @@ __global__ void __launch_bounds__(256) k_spmv_sell2(int64_t n, int64_t nslices, 
                                                     const int32_t *__restrict__ col, const T *__restrict__ val,
                                                     const T *__restrict__ x, const T *__restrict__ xh, T *__restrict__ y,
                                                     int mode, const T *__restrict__ b, const int *__restrict__ done) {
+  pdl_launch();
+  pdl_wait();
   if (done && *done) return;
   const int64_t s0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * SPW;
   if (s0 >= nslices) return;
@@ -682,7 +693,7 @@ struct RegBuf {
 template <typename T, int W, int NW, int NB>
 __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
                                                             const int *__restrict__ done) {
-  if (done && *done) return;
+  pdl_launch();
   if (blockIdx.y) {                                                // right-hand side column blockIdx.y (NEXT-4)
     x += (size_t)blockIdx.y * P.ldx;
     tmp += (size_t)blockIdx.y * P.ldx;
@@ -717,6 +728,8 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
   }
   for (int i = tid; i < R; i += blockDim.x) ring[i] = dzero<T>();
   __syncthreads();
+  pdl_wait();                                                      // the prologue above reads setup data only
+  if (done && *done) return;
   const size_t RB = (size_t)P.rec_bytes;
   using Buf = RegBuf<T, W>;
   constexpr int NV = Buf::NV, W8 = Buf::W8;
@@ -886,6 +899,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_pack_gather(int64_t np, const int *__restrict__ lrow, const T *__restrict__ src,
                                                      T *__restrict__ dst, const int *__restrict__ done,
                                                      int64_t lds = 0, int64_t ldd = 0) {
+  pdl_launch();
+  pdl_wait();
   if (done && *done) return;
   src += (size_t)blockIdx.y * lds;                                 // column blockIdx.y (several right-hand sides)
   dst += (size_t)blockIdx.y * ldd;
@@ -901,6 +916,8 @@ __global__ void __launch_bounds__(256) k_pack_f(int64_t nf, const int *__restric
                                                 const T *__restrict__ yh, int64_t nh, const T *__restrict__ yl,
                                                 T *__restrict__ dst, const int *__restrict__ done, int64_t ldy = 0,
                                                 int64_t ldd = 0) {
+  pdl_launch();
+  pdl_wait();
   if (done && *done) return;
   y += (size_t)blockIdx.y * ldy;                                   // column blockIdx.y (one GPU: no halo / yl)
   dst += (size_t)blockIdx.y * ldd;
@@ -1045,6 +1062,8 @@ __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const i
                                              const T *src, T *dst, const T *__restrict__ W, int64_t ldw, int k,
                                              const T *__restrict__ G, T *__restrict__ partial, unsigned *ticket,
                                              T *sout, int *flag, const int *__restrict__ done) {
+  pdl_launch();
+  pdl_wait();
   if (done && *done) return;
   __shared__ T sv[256];
   __shared__ T st[64];
@@ -1174,6 +1193,8 @@ template <typename T, int TR, int NPW>
 __global__ void __launch_bounds__(256) k_gs(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
                                             int dot, const T *__restrict__ h_in, T *__restrict__ partial,
                                             unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
+  pdl_launch();
+  pdl_wait();
   if (done && *done) return;
   __shared__ T su[8][32 * TR];
   __shared__ T sh[GS_MAXC];
@@ -1295,6 +1316,8 @@ template <typename T, int NC, int TU = 1, bool LA = false>
 __global__ void __launch_bounds__(256, NC * TU * sizeof(T) > 256 ? 1 : 2) k_gs2(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
                                               int dot, const T *__restrict__ h_in, T *__restrict__ partial,
                                               unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
+  pdl_launch();
+  pdl_wait();
   if (done && *done) return;
   constexpr int NCH = LA ? 0 : (NC + 31) / 32;                     // 32-column butterfly chunks
   constexpr int NA = LA ? NC : 1;                                  // per-lane accumulators
@@ -1421,6 +1444,8 @@ template <typename T>
 __global__ void __launch_bounds__(256, 2) k_gs2h(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
                                                int dot, const T *__restrict__ h_in, T *__restrict__ partial,
                                                unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
+  pdl_launch();
+  pdl_wait();
   if (done && *done) return;
   __shared__ T sh[64];
   __shared__ T red[8][65];
@@ -1515,6 +1540,8 @@ template <typename T, int G, int C>
 __global__ void __launch_bounds__(256, 1) k_gs2g(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
                                                 int dot, const T *__restrict__ h_in, T *__restrict__ partial,
                                                 unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
+  pdl_launch();
+  pdl_wait();
   if (done && *done) return;
   constexpr int RW = 32 / G, NQ = (C + RW - 1) / RW, NC = G * C;
   __shared__ T sh[NC];
@@ -1666,6 +1693,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_fgmres_scale(FgmDev<T> f, int m, int j, const T *__restrict__ res1,
                                                       const T *__restrict__ res2, const T *__restrict__ res3, int64_t n,
                                                       const T *__restrict__ w, T *__restrict__ vnext) {
+  pdl_launch();
+  pdl_wait();
   if (*f.done) return;
   double hn2;
   if constexpr (sizeof(T) == sizeof(double)) hn2 = res3[0]; else hn2 = res3[0].x;
