@@ -282,6 +282,8 @@ struct StageDev {
   int64_t reg_bytes = 0;   // record bytes of both sweeps
   const int *lrow = nullptr;       // per packed L position: the row (-1 padding), DOWN gather
   D *rhs_up = nullptr;             // UP right-hand sides (zero except the F_l rows)
+  const int *urow = nullptr;       // per packed U position: the row (-1 padding)
+  D *xU = nullptr;                 // UP: the level's x in U-packed order (k_pack_f), updated in place by k_tri_reg
   const int *fpos = nullptr, *frow = nullptr;
   int64_t nf = -1;                 // rows with F_l entries (-1: not set up, use k_pack_rhs)
   int64_t lslices = 0, uslices = 0;
@@ -504,6 +506,8 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     d.rhs_up = P.get<D>(std::max<int64_t>(S.reg.lslices * 32, 1));
     CK(cudaMemsetAsync(d.rhs_up, 0, std::max<int64_t>(S.reg.lslices * 32, 1) * sizeof(D), s));
     d.Rg.mid = P.get<D>(std::max<int64_t>(S.reg.uslices * 32, 1));
+    d.urow = P.upload<int>(S.Up.slice_row, s);
+    d.xU = P.get<D>(std::max<int64_t>(S.reg.uslices * 32, 1));
     d.Rg.ring = S.reg.ring;
     d.reg_bytes = (int64_t)S.reg.data.size();
     if (!d.pipe) d.P.lpos = P.upload<int>(S.reg.lpos, s);
@@ -758,10 +762,16 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
                    (const int *)S.lrow, rhs, rL, doneflag, (int64_t)ldx, (int64_t)Rg.rsL);
       } else if (S.nf >= 0) {
         Rg.rhsL = rUp;
-        if (S.nf > 0)
-          launch_pdl(k_pack_f<D>, dim3(grid_for((S.nf + 255) / 256, 4), nr), dim3(256), 0, ctx->stream, (int64_t)S.nf,
+        // one column: k_tri_reg updates x in place from its U-packed copy xU
+        // (no tmp, no x -= tmp pass); several columns keep the tmp path
+        const bool inpl = nr == 1 && S.xU != nullptr;
+        const int64_t npu = inpl ? S.uslices * 32 : 0;
+        if (inpl) Rg.xU = S.xU;
+        const int64_t work = std::max<int64_t>(S.nf, npu);
+        if (work > 0)
+          launch_pdl(k_pack_f<D>, dim3(grid_for((work + 255) / 256, 4), nr), dim3(256), 0, ctx->stream, (int64_t)S.nf,
                      (const int *)S.fpos, (const int *)S.frow, Fp, Fc, Fv, (const D *)x, (int64_t)fa.nloc, fa.yh,
-                     (int64_t)fa.nh, fa.yl, rUp, doneflag, (int64_t)ldx, (int64_t)Rg.rsL);
+                     (int64_t)fa.nh, fa.yl, rUp, doneflag, (int64_t)ldx, (int64_t)Rg.rsL, npu, S.urow, S.xU);
       } else {
         k_pack_rhs<D><<<pgrid, 256, 0, ctx->stream>>>(S.rows, S.row0, S.P.lpos, const_cast<D *>(S.Rg.rhsL), nullptr, Fp, Fc,
                                                       Fv, Fbase, x, fa.nloc, fa.yh, fa.nh, fa.yl, doneflag);

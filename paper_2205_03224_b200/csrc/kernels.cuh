@@ -625,6 +625,7 @@ struct RegDev {
   const int *lev_off;
   const T *rhsL;
   T *mid;
+  const T *xU;             // UP, one column: the level's x in U-packed order (k_pack_f); else null (tmp path)
   int ring;
   long long *dbg;          // debug trace (block 0): 8 words per slice, 2048 slices per sweep
   int flags;               // experiment bits (GEMSLR_REG_FLAGS), 0 in production
@@ -679,7 +680,7 @@ struct RegBuf {
   static constexpr int W8 = (W + 7) / 8;         // 16-byte slot loads (8 x uint16)
   double2 v[NV];
   uint4 c[W8];
-  T rhs, dg;
+  T rhs, dg, xo;
   int out;
   __device__ T val(int e) const { return vec_get<T>(v[e / VE], e % VE); }
   __device__ unsigned slot(int e) const {
@@ -730,6 +731,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
   __syncthreads();
   pdl_wait();                                                      // the prologue above reads setup data only
   if (done && *done) return;
+  const bool inplace = mode == TRI_UP && P.xU != nullptr;
   const size_t RB = (size_t)P.rec_bytes;
   using Buf = RegBuf<T, W>;
   constexpr int NV = Buf::NV, W8 = Buf::W8;
@@ -755,6 +757,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
       if (upper) {
         B.dg = ld_nc(reinterpret_cast<const T *>(op + 32) + lane);
         B.rhs = ld_cg(P.mid + ri);                                 // written by this CTA's L sweep
+        if (inplace) B.xo = ld_nc(P.xU + ri);
       } else {
         B.rhs = ld_nc(P.rhsL + ri);
       }
@@ -830,6 +833,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
     auto store = [&](const Buf &B, const T &acc) {
       if (B.out >= 0) {
         if (!upper) P.mid[B.out] = acc;
+        else if (inplace) x[B.out] = B.xo - acc;                   // y1 = z1 - U^-1 L^-1 F y2 (Alg. 2 l.9)
         else if (mode == TRI_UP) tmp[B.out] = acc;                 // x -= tmp after the sweep
         else x[B.out] = acc;
       }
@@ -872,7 +876,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
     __threadfence_block();
     reg_sync_all<NW>();                                            // sweep transition: mid / tmp visible, ring free
   }
-  if (mode == TRI_UP) {                                            // y1 = z1 - U^-1 L^-1 F y2 (Alg. 2 l.9)
+  if (mode == TRI_UP && !inplace) {                                // y1 = z1 - U^-1 L^-1 F y2 (Alg. 2 l.9)
     constexpr int U = 8;                                           // 8 independent rows in flight per thread
     const int i0 = bi[8], i1 = bi[9];
     int i = i0 + tid;
@@ -915,12 +919,19 @@ __global__ void __launch_bounds__(256) k_pack_f(int64_t nf, const int *__restric
                                                 const T *__restrict__ Fval, const T *__restrict__ y, int64_t nloc,
                                                 const T *__restrict__ yh, int64_t nh, const T *__restrict__ yl,
                                                 T *__restrict__ dst, const int *__restrict__ done, int64_t ldy = 0,
-                                                int64_t ldd = 0) {
+                                                int64_t ldd = 0, int64_t npu = 0, const int *__restrict__ urow = nullptr,
+                                                T *__restrict__ xu = nullptr) {
   pdl_launch();
   pdl_wait();
   if (done && *done) return;
   y += (size_t)blockIdx.y * ldy;                                   // column blockIdx.y (one GPU: no halo / yl)
   dst += (size_t)blockIdx.y * ldd;
+  // the level's current values x[rows] in U-packed order (k_tri_reg UP writes
+  // x[row] = xu - U^-1 L^-1 F y in place; one column)
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npu; p += (int64_t)gridDim.x * blockDim.x) {
+    const int r = urow[p];
+    xu[p] = r >= 0 ? y[r] : dzero<T>();
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += (int64_t)gridDim.x * blockDim.x) {
     const int li = frow[i];
     T v = dzero<T>();
