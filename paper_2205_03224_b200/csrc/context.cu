@@ -308,6 +308,9 @@ struct LevelDev {
   int64_t o0 = 0, o1 = 0, s = 0;
   StageDev<D> st;
   CsrDev<D> E, F;
+  // one GPU, register trisolve: E_l's columns as U-packed positions of the level's
+  // stage, so E_l z1 reads z1 from the U-packed copy the DOWN trisolve writes (xpm)
+  const int32_t *Ecol_p = nullptr;
   int k = 0;
   D *W = nullptr;          // s x k column-major, ld = ldw
   int64_t ldw = 0;
@@ -622,6 +625,22 @@ void Engine<T>::upload(cudaStream_t s) {
         d.st.frow = P.upload<int>(frow, s);
         d.st.nf = (int64_t)fpos.size();
       }
+      if (plan.nranks == 1 && d.st.xU && d.st.nf >= 0) {        // the UP then reads z1 from xU (k_pack_f path)
+        const auto &Eh = plan.E[l];
+        std::vector<int32_t> upos(S.reg.lpos.size(), -1);
+        for (size_t q = 0; q < S.Up.slice_row.size(); ++q) {
+          const int64_t row = (int64_t)S.Up.slice_row[q] - R0;
+          if (S.Up.slice_row[q] >= 0 && row >= 0 && row < (int64_t)upos.size()) upos[row] = (int32_t)q;
+        }
+        std::vector<int32_t> ecp(Eh.col.size());
+        bool eok = true;
+        for (size_t q = 0; q < Eh.col.size() && eok; ++q) {
+          const int64_t row = (int64_t)Eh.col[q] - R0;
+          if (row < 0 || row >= (int64_t)upos.size() || upos[row] < 0) eok = false;
+          else ecp[q] = upos[row];
+        }
+        if (eok && !ecp.empty()) d.Ecol_p = P.upload<int32_t>(ecp, s);
+      }
     }
     hE[l] = upload_halo<D>(P, s, plan.hE[l]);
     hF[l] = upload_halo<D>(P, s, plan.hF[l]);
@@ -730,8 +749,12 @@ struct FArgs {
 };
 
 template <typename D>
+// xpm (one right-hand side, register kernel): DOWN writes the level's result to
+// the U-packed buffer S.xU instead of x (coalesced stores; E_l z1 reads it there,
+// Engine::apply_from); UP then takes x's old values from S.xU as they are.
 static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *rhs, D *x, D *tmp,
-                            const FArgs<D> &fa, const int *doneflag, int kc, int lvl = 0, int nr = 1, int64_t ldx = 0) {
+                            const FArgs<D> &fa, const int *doneflag, int kc, int lvl = 0, int nr = 1, int64_t ldx = 0,
+                            bool xpm = false) {
   if (S.nblk <= 0 || S.rows == 0) return;
   if (nr > 1 && !(S.reg && S.mcap >= nr && (mode == TRI_DOWN || S.nf >= 0)))
     throw Error{GEMSLR_ERR_STATE, "several right-hand sides need the register-prefetched trisolve"};
@@ -754,6 +777,7 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
       Rg.rsL = Rg.rsU = std::max(S.lslices, S.uslices) * 32;
     }
     Rg.rhsL = rL;
+    if (xpm && mode == TRI_DOWN && nr == 1) Rg.xP = S.xU;
     {
       Timed tp(ctx->prof, ctx->stream, KC_PACK);
       if (mode == TRI_DOWN) {
@@ -765,7 +789,7 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
         // one column: k_tri_reg updates x in place from its U-packed copy xU
         // (no tmp, no x -= tmp pass); several columns keep the tmp path
         const bool inpl = nr == 1 && S.xU != nullptr;
-        const int64_t npu = inpl ? S.uslices * 32 : 0;
+        const int64_t npu = inpl && !xpm ? S.uslices * 32 : 0;      // xpm: S.xU already holds z1 (DOWN)
         if (inpl) Rg.xU = S.xU;
         const int64_t work = std::max<int64_t>(S.nf, npu);
         if (work > 0)
@@ -917,8 +941,12 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
   for (int l = l0; l < L; ++l) {
     LevelDev<D> &d = lev[l];
     const D *src = (l == l0) ? in : r;
-    // z1 = U_l^-1 L_l^-1 b1  -> out[I_l]
-    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, l);
+    // z1 = U_l^-1 L_l^-1 b1  -> out[I_l] (xpm: U-packed in d.st.xU, read by E_l and the UP)
+    const bool xpm = !dist && d.Ecol_p != nullptr;
+    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, l, 1, 0, xpm);
+    const D *zsrc = xpm ? (const D *)d.st.xU : (const D *)out;
+    const int32_t *ecol = xpm ? d.Ecol_p : d.E.col;
+    const int64_t znloc = xpm ? INT64_MAX : n;                     // packed positions may exceed n: no halo part
     if (d.s > 0 || dist) {
       exchange(hE[l], out, doneflag);                              // z1 entries of E_l's exterior columns
       if (!dist && d.k > 0 && d.k <= 64) {                         // one cooperative launch: K6 + K7 + K8
@@ -930,10 +958,10 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
           max_ctas = std::max(1, per) * kNumSM;
         }
         const int grid = (int)std::min<int64_t>((std::max<int64_t>(d.s, 1) + 255) / 256, max_ctas);
-        int64_t a0 = d.s, a1 = d.o1, a5 = n, a11 = d.ldw;
+        int64_t a0 = d.s, a1 = d.o1, a5 = znloc, a11 = d.ldw;
         const int64_t *a2 = d.E.ptr;
-        const int32_t *a3 = d.E.col;
-        const D *a4 = d.E.val, *zz = out, *zh = hE[l].rbuf, *sr = src, *Wp = d.W, *Gp = d.G;
+        const int32_t *a3 = ecol;
+        const D *a4 = d.E.val, *zz = zsrc, *zh = hE[l].rbuf, *sr = src, *Wp = d.W, *Gp = d.G;
         D *ds = r, *pt = partial, *so = tvec;
         int kk = d.k;
         unsigned *tk = tickets + 0;
@@ -947,7 +975,7 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
       {
         Timed t(ctx->prof, s, KC_EW);
         const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 4);
-        k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, out, hE[l].rbuf, n, src, r, d.W, d.ldw, d.k,
+        k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, ecol, d.E.val, zsrc, hE[l].rbuf, znloc, src, r, d.W, d.ldw, d.k,
                                      partial, tickets + 0, tvec, doneflag);
         CK(cudaGetLastError());
       }
@@ -988,7 +1016,8 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     fa.yh = hF[l].rbuf;
     fa.nh = hF[l].nrecv;
     fa.yl = yl_full;
-    launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP, l);
+    launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP, l, 1, 0,
+                    !dist && d.Ecol_p != nullptr);
   }
 }
 

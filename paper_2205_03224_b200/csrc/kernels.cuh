@@ -626,6 +626,7 @@ struct RegDev {
   const T *rhsL;
   T *mid;
   const T *xU;             // UP, one column: the level's x in U-packed order (k_pack_f); else null (tmp path)
+  T *xP;                   // DOWN, one column: write the result in U-packed order here instead of x[row]
   int ring;
   long long *dbg;          // debug trace (block 0): 8 words per slice, 2048 slices per sweep
   int flags;               // experiment bits (GEMSLR_REG_FLAGS), 0 in production
@@ -830,7 +831,11 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
     };
     auto level_of = [&](int t) { return t < ns ? (int)lvt[lvbase + t] : nlev; };
     // The global stores are read only after the sweep-transition barrier.
-    auto store = [&](const Buf &B, const T &acc) {
+    auto store = [&](const Buf &B, const T &acc, int s) {
+      if (upper && P.xP) {                                         // coalesced: U-packed position of the row
+        P.xP[(size_t)(gbase + s) * 32 + lane] = acc;
+        return;
+      }
       if (B.out >= 0) {
         if (!upper) P.mid[B.out] = acc;
         else if (inplace) x[B.out] = B.xo - acc;                   // y1 = z1 - U^-1 L^-1 F y2 (Alg. 2 l.9)
@@ -857,7 +862,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
       const T a0 = solve(A, s);
       publish(A, s, a0);
       depart(nxt);
-      store(A, a0);
+      store(A, a0, s);
       load(A, s + NB * NW);
       s += NW;
       if (NB == 2) {
@@ -867,7 +872,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
         const T a1 = solve(B, s);
         publish(B, s, a1);
         depart(nxt);
-        store(B, a1);
+        store(B, a1, s);
         load(B, s + 2 * NW);
         s += NW;
       }
