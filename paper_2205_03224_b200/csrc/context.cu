@@ -311,6 +311,10 @@ struct LevelDev {
   // one GPU, register trisolve: E_l's columns as U-packed positions of the level's
   // stage, so E_l z1 reads z1 from the U-packed copy the DOWN trisolve writes (xpm)
   const int32_t *Ecol_p = nullptr;
+  // one GPU: k_ewx also writes the first npk rows of r_J (the next stage's rows)
+  // at their packed L positions pkpos in that stage's right-hand-side buffer
+  int64_t npk = 0;
+  const int *pkpos = nullptr;
   int k = 0;
   D *W = nullptr;          // s x k column-major, ld = ldw
   int64_t ldw = 0;
@@ -647,6 +651,28 @@ void Engine<T>::upload(cudaStream_t s) {
   }
   hA = upload_halo<D>(P, s, plan.hA);
   last = upload_stage<D>(P, s, plan.last_stage, ctx->params.cluster_ctas, ctx->params.tri_kernel);
+  if (plan.nranks == 1) {                                          // packed next-stage right-hand sides from k_ewx
+    for (int l = 0; l < L; ++l) {
+      LevelDev<D> &d = lev[l];
+      const Stage<T> &NS = (l + 1 < L) ? plan.stage[l + 1] : plan.last_stage;
+      StageDev<D> &nd = (l + 1 < L) ? lev[l + 1].st : last;
+      if (!nd.reg || NS.blk.empty() || d.s <= 0) continue;
+      const int64_t R0n = NS.blk.front();
+      const int64_t npk = ((l + 1 < L) ? plan.lo[l + 2] : n) - d.o1;
+      if (npk <= 0 || npk > d.s) continue;
+      std::vector<int32_t> pos(npk);
+      bool ok = true;
+      for (int64_t i = 0; i < npk && ok; ++i) {
+        const int64_t row = d.o1 + i - R0n;
+        if (row < 0 || row >= (int64_t)NS.reg.lpos.size() || NS.reg.lpos[row] < 0) ok = false;
+        else pos[i] = NS.reg.lpos[row];
+      }
+      if (!ok) continue;
+      d.pkpos = P.upload<int>(pos, s);
+      d.npk = npk;
+      CK(cudaMemsetAsync(const_cast<D *>(nd.Rg.rhsL), 0, std::max<int64_t>(nd.lslices * 32, 1) * sizeof(D), s));
+    }
+  }
   if (plan.nranks > 1) {
     rl_full = P.get<D>(plan.slast + 1);
     yl_full = P.get<D>(plan.slast + 1);
@@ -754,7 +780,7 @@ template <typename D>
 // Engine::apply_from); UP then takes x's old values from S.xU as they are.
 static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *rhs, D *x, D *tmp,
                             const FArgs<D> &fa, const int *doneflag, int kc, int lvl = 0, int nr = 1, int64_t ldx = 0,
-                            bool xpm = false) {
+                            bool xpm = false, bool rhs_packed = false) {
   if (S.nblk <= 0 || S.rows == 0) return;
   if (nr > 1 && !(S.reg && S.mcap >= nr && (mode == TRI_DOWN || S.nf >= 0)))
     throw Error{GEMSLR_ERR_STATE, "several right-hand sides need the register-prefetched trisolve"};
@@ -779,9 +805,13 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
     Rg.rhsL = rL;
     if (xpm && mode == TRI_DOWN && nr == 1) Rg.xP = S.xU;
     {
-      Timed tp(ctx->prof, ctx->stream, KC_PACK);
-      if (mode == TRI_DOWN) {
+      // (profiler: a pack is timed and counted only when a kernel is launched)
+      auto tp = [&]() { return Timed(ctx->prof, ctx->stream, KC_PACK); };
+      if (mode == TRI_DOWN && rhs_packed && nr == 1) {
+        // the packed right-hand side was written by the previous k_ewx (npk / pkpos)
+      } else if (mode == TRI_DOWN) {
         const int64_t np = S.lslices * 32;
+        const Timed tt = tp();
         launch_pdl(k_pack_gather<D>, dim3(grid_for((np + 255) / 256, 4), nr), dim3(256), 0, ctx->stream, np,
                    (const int *)S.lrow, rhs, rL, doneflag, (int64_t)ldx, (int64_t)Rg.rsL);
       } else if (S.nf >= 0) {
@@ -792,11 +822,14 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
         const int64_t npu = inpl && !xpm ? S.uslices * 32 : 0;      // xpm: S.xU already holds z1 (DOWN)
         if (inpl) Rg.xU = S.xU;
         const int64_t work = std::max<int64_t>(S.nf, npu);
-        if (work > 0)
+        if (work > 0) {
+          const Timed tt = tp();
           launch_pdl(k_pack_f<D>, dim3(grid_for((work + 255) / 256, 4), nr), dim3(256), 0, ctx->stream, (int64_t)S.nf,
                      (const int *)S.fpos, (const int *)S.frow, Fp, Fc, Fv, (const D *)x, (int64_t)fa.nloc, fa.yh,
                      (int64_t)fa.nh, fa.yl, rUp, doneflag, (int64_t)ldx, (int64_t)Rg.rsL, npu, S.urow, S.xU);
+        }
       } else {
+        const Timed tt = tp();
         k_pack_rhs<D><<<pgrid, 256, 0, ctx->stream>>>(S.rows, S.row0, S.P.lpos, const_cast<D *>(S.Rg.rhsL), nullptr, Fp, Fc,
                                                       Fv, Fbase, x, fa.nloc, fa.yh, fa.nh, fa.yl, doneflag);
       }
@@ -938,12 +971,14 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP, 0);
     return;
   }
+  bool packed = false;                                             // this level's rhs already packed by k_ewx
   for (int l = l0; l < L; ++l) {
     LevelDev<D> &d = lev[l];
     const D *src = (l == l0) ? in : r;
     // z1 = U_l^-1 L_l^-1 b1  -> out[I_l] (xpm: U-packed in d.st.xU, read by E_l and the UP)
     const bool xpm = !dist && d.Ecol_p != nullptr;
-    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, l, 1, 0, xpm);
+    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, l, 1, 0, xpm, packed);
+    packed = false;
     const D *zsrc = xpm ? (const D *)d.st.xU : (const D *)out;
     const int32_t *ecol = xpm ? d.Ecol_p : d.E.col;
     const int64_t znloc = xpm ? INT64_MAX : n;                     // packed positions may exceed n: no halo part
@@ -967,8 +1002,14 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
         unsigned *tk = tickets + 0;
         int *fl = ewflag;
         const int *dn = doneflag;
-        void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &dn};
+        StageDev<D> &nst = (l + 1 < L) ? lev[l + 1].st : last;
+        int64_t npk = d.npk;
+        const int *pkp = d.pkpos;
+        D *pkd = const_cast<D *>(nst.Rg.rhsL);
+        void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &dn,
+                        &npk, &pkp, &pkd};
         CK(cudaLaunchCooperativeKernel((const void *)k_ewx<D>, dim3(grid), dim3(256), args, 0, s));
+        packed = npk > 0;
         continue;
       }
       // z2 = b2 - E_l z1 ; this rank's part of s = W^H z2
@@ -995,7 +1036,8 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
   const D *src = (l0 == L) ? in : r;
   const int64_t lL = plan.lo[L], nown = n - lL;
   if (!dist) {
-    launch_trisolve(ctx, last, TRI_DOWN, src + lL, out + lL, tmp, FArgs<D>{}, doneflag, KC_TRI_LAST);
+    launch_trisolve(ctx, last, TRI_DOWN, src + lL, out + lL, tmp, FArgs<D>{}, doneflag, KC_TRI_LAST, 0, 1, 0, false,
+                    packed);
   } else {
     CK(cudaMemsetAsync(rl_full, 0, plan.slast * sizeof(D), s));
     if (nown > 0)
@@ -1077,7 +1119,11 @@ void Engine<T>::ew_column(LevelDev<D> &d, int l, const D *src, const D *z, D *ds
     unsigned *tk = tickets + 0;
     int *fl = ewflag;
     const int *dn = doneflag;
-    void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &dn};
+    int64_t npk = 0;                                               // no next-stage packing here
+    const int *pkp = nullptr;
+    D *pkd = nullptr;
+    void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &dn,
+                    &npk, &pkp, &pkd};
     CK(cudaLaunchCooperativeKernel((const void *)k_ewx<D>, dim3(grid), dim3(256), args, 0, s));
     return;
   }

@@ -1077,7 +1077,8 @@ __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const i
                                              const T *__restrict__ z, const T *__restrict__ zh, int64_t nloc,
                                              const T *src, T *dst, const T *__restrict__ W, int64_t ldw, int k,
                                              const T *__restrict__ G, T *__restrict__ partial, unsigned *ticket,
-                                             T *sout, int *flag, const int *__restrict__ done) {
+                                             T *sout, int *flag, const int *__restrict__ done, int64_t npk = 0,
+                                             const int *__restrict__ pkpos = nullptr, T *__restrict__ pk = nullptr) {
   pdl_launch();
   pdl_wait();
   if (done && *done) return;
@@ -1164,7 +1165,9 @@ __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const i
     if (i < s) {
       T a = dzero<T>();
       for (int c = 0; c < k; ++c) a += ld_nc(W + c * ldw + i) * st[c];
-      dst[rowbase + i] = ld_cg(dst + rowbase + i) + a;
+      const T v = ld_cg(dst + rowbase + i) + a;
+      dst[rowbase + i] = v;
+      if (i < npk) pk[pkpos[i]] = v;                               // the next stage's packed right-hand side
     }
   }
 }
