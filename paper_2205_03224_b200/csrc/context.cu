@@ -1769,16 +1769,19 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
         iteration(j);
       }
       // the done flag of iteration j reaches pinned host memory asynchronously;
-      // the host reads it two iterations later, so the GPU always has the next
-      // iterations queued (a synchronous copy would drain the stream)
+      // the host reads it kLag iterations later, so the GPU always has the next
+      // iterations queued (a synchronous copy would drain the stream; with a lag
+      // of 2 a host hiccup of ~2 ms starved the GPU in some bench runs).  After
+      // convergence at most kLag queued iterations run, every kernel exiting at once.
+      constexpr int kLag = 6;
       CK(cudaMemcpyAsync(hflags + j, done, sizeof(int), cudaMemcpyDeviceToHost, s));
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       CK(cudaEventRecord(e, s));
       evs.push_back(e);
-      if (j >= 2) {
-        CK(cudaEventSynchronize(evs[j - 2]));
-        if (((volatile int *)hflags)[j - 2]) break;
+      if (j >= kLag) {
+        CK(cudaEventSynchronize(evs[j - kLag]));
+        if (((volatile int *)hflags)[j - kLag]) break;
       }
     }
     CK(cudaStreamSynchronize(s));
