@@ -981,14 +981,25 @@ __global__ void __launch_bounds__(256) k_pack_rhs(int64_t nrows, int64_t row0, c
 // Deterministic last-CTA reduction of per-CTA partials stored column-major
 // (partial[c * G + q], q = CTA): warp w sums the columns w, w+8, ...; lane l
 // adds the CTAs l, l+32, ... (coalesced, fixed order), then a fixed shuffle tree.
+// The loads of a column (up to 16 per lane) are all issued before the sum, so
+// a column costs one L2 round trip (the tail of every CGS2 pass with dots).
 template <typename T>
 __device__ inline void reduce_partials(const T *partial, int G, int ncol, T *out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int c = warp; c < ncol; c += nw) {
     T s = dzero<T>();
     const T *p = partial + (int64_t)c * G;
-#pragma unroll 4
-    for (int q = lane; q < G; q += 32) s += ld_cg(p + q);
+    int q0 = 0;
+    for (; q0 < G; q0 += 512) {
+      T v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int q = q0 + lane + 32 * u;
+        v[u] = q < G ? ld_cg(p + q) : dzero<T>();
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += v[u];
+    }
     s = warp_sum(s);
     if (lane == 0) out[c] = s;
   }
