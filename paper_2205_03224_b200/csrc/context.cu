@@ -1322,7 +1322,26 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
   if (done2) {
   } else if (ncols <= 8) go(k_gs<D, 8, 1>, 8);
   else if (ncols <= 24) go(k_gs<D, 4, 3>, 4);
-  else if (ncols <= 48) go(k_gs<D, 2, 6>, 2);
+  else if (ncols <= 48) {
+    // 33-48 columns, per pass (ncu on C5, 40-column cycle): dots only k_gs<4,6> (88 us at
+    // 33 columns), update + dots k_gs<2,6> (127), update + norm the warp-tile k_gs2<48> (105;
+    // k_gs's update needs a cross-warp sum per row tile through shared memory)
+    if constexpr (sizeof(D) == 8) {
+      if (!upd) {
+        const int grid = grid_for((nn + 127) / 128, 2);            // 97 registers: 2 CTAs per SM
+        launch_pdl(k_gs<D, 4, 6>, dim3(grid), dim3(256), 0, ctx->stream, nn, Vb, ldvv, ncols, wv, upd, dot, h_in,
+                   partial, tickets + ticket, resv, doneflag);
+      } else if (dot) {
+        go(k_gs<D, 2, 6>, 2);
+      } else {
+        const int grid = grid_for((nn + 255) / 256, 1);
+        launch_pdl(k_gs2<D, 48, 1, false>, dim3(grid), dim3(256), 0, ctx->stream, nn, Vb, ldvv, ncols, wv, upd, dot,
+                   h_in, partial, tickets + ticket, resv, doneflag);
+      }
+    } else {
+      go(k_gs<D, 2, 6>, 2);
+    }
+  }
   else go(k_gs<D, 1, 13>, 1);
   CK(cudaGetLastError());
   allreduce(resv, dot ? ncols + 1 : 1);                          // dots and norms over ranks
