@@ -453,7 +453,7 @@ static int reg_nw_for(const RegPack<T> &R) {
     return K >= 3.0 ? 23 : 15;
   }
   if (env == 7 || env == 15) return env;
-  return K >= 3.0 ? 15 : 7;
+  return 15;                                                       // complex: 15 warps, one buffer (C4: every level)
 }
 
 template <typename D, typename T>
