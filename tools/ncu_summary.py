@@ -30,9 +30,24 @@ def launches(path, out):
         k = short(r[ik])
         m = r[imn] if imn is not None else 'gpu__time_duration.sum'
         per.setdefault(lid, (k, {}))[1][m] = float(r[iv].replace(',', ''))
+    # Iterations queued after the done flag run as no-ops (every kernel exits at
+    # once; the host reads the flag 6 iterations late): an iteration ends with
+    # its k_fgmres_scale, which moves ~2 vectors when real; drop whole no-op
+    # iterations so shares and per-launch figures describe real work.
+    items = list(per.items())
+    keep, seg = [], []
+    for lid, (k, m) in items:
+        seg.append((lid, (k, m)))
+        if k.startswith('k_fgmres_scale'):
+            b = m.get('dram__bytes_read.sum', 0.0) + m.get('dram__bytes_write.sum', 0.0)
+            if b >= 1e6 or 'dram__bytes_read.sum' not in m:
+                keep.extend(seg)
+            seg = []
+    keep.extend(seg)
+    dropped = len(items) - len(keep)
     tot, cnt, dram = collections.defaultdict(float), collections.Counter(), collections.defaultdict(float)
     tri = []
-    for lid, (k, m) in per.items():
+    for lid, (k, m) in keep:
         t = m.get('gpu__time_duration.sum', 0.0)
         unit_ns = 1.0
         tot[k] += t * unit_ns
@@ -46,16 +61,16 @@ def launches(path, out):
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         lines.append(f"| {k} | {cnt[k]} | {v / 1e3:.1f} | {v / 1e3 / cnt[k]:.2f} | {100 * v / T:.1f}% | {dram[k] / cnt[k] / 1e6:.2f} |")
     lines.append(f"\nTotal {T / 1e3:.1f} µs over {sum(cnt.values())} launches (ncu, `--clock-control none`, "
-                 "serialised cold-cache launches: compare shares, not absolute times).")
+                 "serialised cold-cache launches: compare shares, not absolute times; "
+                 f"{dropped} launches of iterations queued after the done flag, which exit at once, left out).")
     cls = {}
     if tri and len(tri) % 7 == 0:
         names = ['down_l0', 'down_l1', 'down_l2', 'last', 'up_l2', 'up_l1', 'up_l0']
         import statistics
         for i, nm in enumerate(names):
-            sel = tri[i::7]                              # median: the last iterations of a solve exit early (done flag)
+            sel = tri[i::7]
             cls[nm] = (statistics.median(t for t, _ in sel), statistics.median(b for _, b in sel))
-        lines.append("\nTriangular-solve launches by position in the apply (median per launch; kernels of the "
-                     "iterations queued after the done flag exit at once):\n")
+        lines.append("\nTriangular-solve launches by position in the apply (median per launch):\n")
         lines.append("| launch | µs | DRAM MB |\n|---|---|---|")
         for nm, (t, b) in cls.items():
             lines.append(f"| {nm} | {t / 1e3:.1f} | {b / 1e6:.1f} |")
