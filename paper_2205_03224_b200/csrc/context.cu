@@ -836,8 +836,6 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
     }
     Timed t(ctx->prof, ctx->stream, kc, lvl);
     Rg.dbg = (kc == KC_TRI_DOWN && lvl == g_tri_dbg_level) ? g_tri_dbg : nullptr;
-    static const int reg_flags = getenv("GEMSLR_REG_FLAGS") ? atoi(getenv("GEMSLR_REG_FLAGS")) : 0;
-    Rg.flags = reg_flags;
     auto go = [&](auto kern, int nw) {
       static std::set<const void *> attr;                          // once per instance
       if (attr.insert((const void *)kern).second)

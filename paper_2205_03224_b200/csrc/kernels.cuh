@@ -629,7 +629,6 @@ struct RegDev {
   T *xP;                   // DOWN, one column: write the result in U-packed order here instead of x[row]
   int ring;
   long long *dbg;          // debug trace (block 0): 8 words per slice, 2048 slices per sweep
-  int flags;               // experiment bits (GEMSLR_REG_FLAGS), 0 in production
   int max_slices;          // L + U records of the largest block (shared-memory level table)
   // several right-hand sides (NEXT-4): column blockIdx.y works on x/tmp + col*ldx
   // and rhsL/mid + col*rs (0 for one column); the factor records are shared
