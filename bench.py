@@ -232,6 +232,21 @@ def run_ours(args):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": dd["GBps"], "peak": peak, "unit": "GB/s",
                 "frac": dd["frac"], "traffic": round(traffic) if traffic else None, "peak_source": peak_src,
                 "bytes_per_launch": round(gb[dom] / dd["launches"]), "us_per_launch": dd["us_per_launch"]}
+    # The triangular solves are bound by their level depth, not by HBM:
+    # the latency account of the dominant class — level-barrier rounds per launch set
+    # (the deepest block of every stage, L + U sweeps) and the SM cycles each took,
+    # against the floor tools/ubench/levels.cu measures for one round (one dependent
+    # gather + DFMA chain + barrier hand-off, ~250 cycles at 1-2 slices per level).
+    if dom.startswith("trisolve") and dom != "trisolve_last":
+        try:
+            depth = sum(st["stage"]["depth_L"] + st["stage"]["depth_U"] for st in stats["stages"])
+            per_set = dd["ms_total"] * 1e3 / (dd["launches"] / max(len(stats["stages"]), 1))   # us per apply
+            mhz = (clocks or {}).get("sm_mhz") or 1965.0
+            roofline["latency"] = {"levels_per_apply": depth, "us_per_apply": round(per_set, 1),
+                                   "cycles_per_level": round(per_set * mhz / depth, 1),
+                                   "floor_cycles_per_level": 250, "floor_source": "tools/ubench/levels.cu (K = 1-2)"}
+        except Exception:
+            pass
     launches = int(sum(d["count"] for d in kern.values()))
     # end-to-end: host vectors in natural order through gemslr_solve_host
     # inputs and outputs in pinned host memory (the copies run at link speed)
