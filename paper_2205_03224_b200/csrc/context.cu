@@ -31,7 +31,19 @@
 
 namespace gemslr {
 
-static constexpr int kNumSM = 148;
+// SMs of the current device (cudaDevAttrMultiProcessorCount; sizes the grids and
+// the cooperative k_ewx launch, so a partitioned GPU — MIG, MPS limits — still works)
+static int num_sm() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
 long long *g_tri_dbg = nullptr;   // debug: per-chunk clock64 trace of block 0 (gemslr_debug_trace)
 int g_tri_dbg_level = 0;          // level whose down launch is traced
 static_assert(PIPE_SB == PIPE_SB_DEV && PIPE_NW == PIPE_NW_DEV, "pipeline constants");
@@ -372,6 +384,7 @@ struct Engine {
   std::vector<cudaGraphExec_t> graphs;   // FGMRES iteration j captured once (one GPU)
   int graph_m = -1;
   const D *graph_V = nullptr;
+  const double *graph_hist = nullptr;  // captured k_fgmres_scale nodes write hist: a new buffer needs new graphs
   cudaStream_t cap_stream = nullptr;
   ~Engine() {
     if (hflags) cudaFreeHost(hflags);
@@ -529,7 +542,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     const double depth = std::max(1, std::max(d.depthL, d.depthU));
     const double rows_per_level = (double)d.rows / d.nblk / depth;
     int want = (int)std::ceil(rows_per_level / 256.0);
-    int avail = std::max(1, kNumSM / d.nblk);
+    int avail = std::max(1, num_sm() / d.nblk);
     cps = std::min(std::min(want, avail), 8);
     int p2 = 1;
     while (p2 * 2 <= cps) p2 *= 2;
@@ -681,7 +694,7 @@ void Engine<T>::upload(cudaStream_t s) {
   r = P.get<D>(n + 1);
   tmp = P.get<D>(n + 1);
   tvec = P.get<D>(64 * 8);
-  partial_cap = (size_t)kNumSM * 8 * (GS_MAXC + 2);
+  partial_cap = (size_t)num_sm() * 8 * (GS_MAXC + 2);
   partial = P.get<D>(partial_cap);
   res = P.get<D>(4 * (GS_MAXC + 2));
   tickets = P.get<unsigned>(16);
@@ -700,7 +713,7 @@ void Engine<T>::exchange(HaloDev<D> &h, const D *src, const int *doneflag) {
   Comm &C = ctx->comm;
   const int w = (int)(sizeof(D) / sizeof(double));
   if (h.nsend > 0) {
-    const int grid = (int)std::min<int64_t>((h.nsend + 255) / 256, 4 * kNumSM);
+    const int grid = (int)std::min<int64_t>((h.nsend + 255) / 256, 4 * num_sm());
     k_gather_idx<D><<<grid, 256, 0, ctx->stream>>>(h.nsend, h.sidx, src, h.sbuf, doneflag);
     CK(cudaGetLastError());
   }
@@ -761,8 +774,59 @@ static void launch_pdl(void (*kern)(KA...), dim3 grid, dim3 block, size_t smem, 
 }
 
 static int grid_for(int64_t units, int per_sm) {
-  int64_t g = std::min<int64_t>(units, (int64_t)kNumSM * per_sm);
+  int64_t g = std::min<int64_t>(units, (int64_t)num_sm() * per_sm);
   return (int)std::max<int64_t>(g, 1);
+}
+
+// The k_ew / k_ewx instance for k low-rank columns: NACC = ceil(k / 8) accumulators
+// per warp, rounded up to 1, 2, 3, 4, 6 or 8 (k <= 64).
+template <typename F>
+static void with_nacc(int k, F &&f) {
+  if (k > EW_MAXK) throw Error{GEMSLR_ERR_INVALID_ARG, "low rank k > 64 in the E/W coupling"};
+  if (k <= 8) f(std::integral_constant<int, 1>{});
+  else if (k <= 16) f(std::integral_constant<int, 2>{});
+  else if (k <= 24) f(std::integral_constant<int, 3>{});
+  else if (k <= 32) f(std::integral_constant<int, 4>{});
+  else if (k <= 48) f(std::integral_constant<int, 6>{});
+  else f(std::integral_constant<int, 8>{});
+}
+
+// K6 + K7 (rows J_l: dst = src - E z ; this rank's part of s = W^H dst into sout)
+template <typename D>
+static void launch_ew(cudaStream_t st, int64_t s, int64_t rowbase, const int64_t *Eptr, const int32_t *Ecol,
+                      const D *Eval, const D *z, const D *zh, int64_t nloc, const D *src, D *dst, const D *W,
+                      int64_t ldw, int k, D *partial, unsigned *ticket, D *sout, const int *done) {
+  const int grid = grid_for((std::max<int64_t>(s, 1) + 255) / 256, 4);
+  with_nacc(k, [&](auto nc) {
+    k_ew<D, decltype(nc)::value><<<grid, 256, 0, st>>>(s, rowbase, Eptr, Ecol, Eval, z, zh, nloc, src, dst, W, ldw, k,
+                                                        partial, ticket, sout, done);
+  });
+  CK(cudaGetLastError());
+}
+
+// K6 + K7 + K8 in one cooperative launch (k_ewx): every CTA must be co-resident,
+// so the grid is capped by the occupancy of the instance on this device.
+template <typename D>
+static void launch_ewx(cudaStream_t st, int64_t s, int64_t rowbase, const int64_t *Eptr, const int32_t *Ecol,
+                       const D *Eval, const D *z, const D *zh, int64_t nloc, const D *src, D *dst, const D *W,
+                       int64_t ldw, int k, const D *G, D *partial, unsigned *ticket, D *sout, int *flag,
+                       const int *done, int64_t npk, const int *pkpos, D *pk) {
+  with_nacc(k, [&](auto nc) {
+    auto kern = k_ewx<D, decltype(nc)::value>;
+    static int max_ctas[64] = {0};                                  // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev = (dev >= 0 && dev < 64) ? dev : 0;
+    if (max_ctas[dev] == 0) {
+      int per = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, 0));
+      max_ctas[dev] = std::max(1, per) * num_sm();
+    }
+    const int grid = (int)std::min<int64_t>((std::max<int64_t>(s, 1) + 255) / 256, max_ctas[dev]);
+    void *args[] = {&s, &rowbase, &Eptr, &Ecol, &Eval, &z, &zh, &nloc, &src, &dst, &W, &ldw, &k, &G, &partial,
+                    &ticket, &sout, &flag, &done, &npk, &pkpos, &pk};
+    CK(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(256), args, 0, st));
+  });
 }
 
 // F_l product arguments of an UP launch: y_J from the local vector, the halo
@@ -954,10 +1018,8 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     launch_trisolve(ctx, d.st, TRI_DOWN, in, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, 0);   // z1
     {
       Timed t(ctx->prof, s, KC_EW);                              // z2 = b2 - E_0 z1 -> r[J_0]
-      const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 4);
-      k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, out, hE[0].rbuf, n, in, r, d.W, d.ldw, 0,
-                                   partial, tickets + 0, tvec, doneflag);
-      CK(cudaGetLastError());
+      launch_ew<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, out, hE[0].rbuf, n, in, r, d.W, d.ldw, 0, partial,
+                   tickets + 0, tvec, doneflag);
     }
     root_gmres(r + d.o1, out + d.o1, doneflag);                   // y2 ≈ Ŝ_0^-1 z2
     FArgs<D> fa;                                                   // y1 = z1 - U^-1 L^-1 F_0 y2
@@ -982,41 +1044,19 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     const int64_t znloc = xpm ? INT64_MAX : n;                     // packed positions may exceed n: no halo part
     if (d.s > 0 || dist) {
       exchange(hE[l], out, doneflag);                              // z1 entries of E_l's exterior columns
-      if (!dist && d.k > 0 && d.k <= 64) {                         // one cooperative launch: K6 + K7 + K8
+      if (!dist && d.k > 0) {                                      // one cooperative launch: K6 + K7 + K8
         Timed t(ctx->prof, s, KC_EW);
-        static int max_ctas = 0;
-        if (max_ctas == 0) {
-          int per = 0;
-          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ewx<D>, 256, 0));
-          max_ctas = std::max(1, per) * kNumSM;
-        }
-        const int grid = (int)std::min<int64_t>((std::max<int64_t>(d.s, 1) + 255) / 256, max_ctas);
-        int64_t a0 = d.s, a1 = d.o1, a5 = znloc, a11 = d.ldw;
-        const int64_t *a2 = d.E.ptr;
-        const int32_t *a3 = ecol;
-        const D *a4 = d.E.val, *zz = zsrc, *zh = hE[l].rbuf, *sr = src, *Wp = d.W, *Gp = d.G;
-        D *ds = r, *pt = partial, *so = tvec;
-        int kk = d.k;
-        unsigned *tk = tickets + 0;
-        int *fl = ewflag;
-        const int *dn = doneflag;
         StageDev<D> &nst = (l + 1 < L) ? lev[l + 1].st : last;
-        int64_t npk = d.npk;
-        const int *pkp = d.pkpos;
-        D *pkd = const_cast<D *>(nst.Rg.rhsL);
-        void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &dn,
-                        &npk, &pkp, &pkd};
-        CK(cudaLaunchCooperativeKernel((const void *)k_ewx<D>, dim3(grid), dim3(256), args, 0, s));
-        packed = npk > 0;
+        launch_ewx<D>(s, d.s, d.o1, d.E.ptr, ecol, d.E.val, zsrc, hE[l].rbuf, znloc, src, r, d.W, d.ldw, d.k, d.G,
+                      partial, tickets + 0, tvec, ewflag, doneflag, d.npk, d.pkpos, const_cast<D *>(nst.Rg.rhsL));
+        packed = d.npk > 0;
         continue;
       }
       // z2 = b2 - E_l z1 ; this rank's part of s = W^H z2
       {
         Timed t(ctx->prof, s, KC_EW);
-        const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 4);
-        k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, ecol, d.E.val, zsrc, hE[l].rbuf, znloc, src, r, d.W, d.ldw, d.k,
-                                     partial, tickets + 0, tvec, doneflag);
-        CK(cudaGetLastError());
+        launch_ew<D>(s, d.s, d.o1, d.E.ptr, ecol, d.E.val, zsrc, hE[l].rbuf, znloc, src, r, d.W, d.ldw, d.k, partial,
+                     tickets + 0, tvec, doneflag);
       }
       if (d.k > 0) {                                              // u2 + z2, G s formed in every CTA
         if (dist) {
@@ -1100,40 +1140,13 @@ template <typename T>
 void Engine<T>::ew_column(LevelDev<D> &d, int l, const D *src, const D *z, D *dst, const int *doneflag) {
   cudaStream_t s = ctx->stream;
   Timed t(ctx->prof, s, KC_EW);
-  if (d.k > 0 && d.k <= 64) {
-    static int max_ctas = 0;
-    if (max_ctas == 0) {
-      int per = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ewx<D>, 256, 0));
-      max_ctas = std::max(1, per) * kNumSM;
-    }
-    const int grid = (int)std::min<int64_t>((std::max<int64_t>(d.s, 1) + 255) / 256, max_ctas);
-    int64_t a0 = d.s, a1 = d.o1, a5 = n, a11 = d.ldw;
-    const int64_t *a2 = d.E.ptr;
-    const int32_t *a3 = d.E.col;
-    const D *a4 = d.E.val, *zz = z, *zh = hE[l].rbuf, *sr = src, *Wp = d.W, *Gp = d.G;
-    D *ds = dst, *pt = partial, *so = tvec;
-    int kk = d.k;
-    unsigned *tk = tickets + 0;
-    int *fl = ewflag;
-    const int *dn = doneflag;
-    int64_t npk = 0;                                               // no next-stage packing here
-    const int *pkp = nullptr;
-    D *pkd = nullptr;
-    void *args[] = {&a0, &a1, &a2, &a3, &a4, &zz, &zh, &a5, &sr, &ds, &Wp, &a11, &kk, &Gp, &pt, &tk, &so, &fl, &dn,
-                    &npk, &pkp, &pkd};
-    CK(cudaLaunchCooperativeKernel((const void *)k_ewx<D>, dim3(grid), dim3(256), args, 0, s));
+  if (d.k > 0) {
+    launch_ewx<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, z, hE[l].rbuf, n, src, dst, d.W, d.ldw, d.k, d.G, partial,
+                  tickets + 0, tvec, ewflag, doneflag, 0, nullptr, nullptr);   // no next-stage packing here
     return;
   }
-  const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 4);
-  k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, z, hE[l].rbuf, n, src, dst, d.W, d.ldw, d.k,
-                               partial, tickets + 0, tvec, doneflag);
-  CK(cudaGetLastError());
-  if (d.k > 0) {
-    k_waxpy<D><<<grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 8), 256, 0, s>>>(d.s, d.o1, d.W, d.ldw, d.k, d.G, tvec,
-                                                                                  dst, doneflag);
-    CK(cudaGetLastError());
-  }
+  launch_ew<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, z, hE[l].rbuf, n, src, dst, d.W, d.ldw, 0, partial, tickets + 0,
+               tvec, doneflag);
 }
 
 template <typename T>
@@ -1263,10 +1276,8 @@ void Engine<T>::ghat(int l, D *bufA, D *bufB) {
   launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, bufB, tmp, fa, nullptr, KC_TRI_UP);
   // bufB[J_l] = 0 - E_l (-u) = E_l u   (K6+K7 with k = 0, src = 0)
   exchange(hE[l], bufB, nullptr);
-  const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 4);
-  k_ew<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.E.ptr, d.E.col, d.E.val, bufB, hE[l].rbuf, n, (const D *)nullptr, bufB,
-                               (const D *)nullptr, 0, 0, partial, tickets + 1, tvec, nullptr);
-  CK(cudaGetLastError());
+  launch_ew<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, bufB, hE[l].rbuf, n, (const D *)nullptr, bufB,
+               (const D *)nullptr, 0, 0, partial, tickets + 1, tvec, nullptr);
 }
 
 template <typename T>
@@ -1732,11 +1743,12 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
     };
     static const bool no_graph = getenv("GEMSLR_NO_GRAPH") != nullptr;
     const bool use_graph = !no_graph && plan.nranks == 1 && !ctx->prof.on;
-    if (use_graph && (graph_m != m || graph_V != V)) {
+    if (use_graph && (graph_m != m || graph_V != V || graph_hist != hist)) {
       for (auto &ge : graphs) if (ge) cudaGraphExecDestroy(ge);
       graphs.assign(m, nullptr);
       graph_m = m;
       graph_V = V;
+      graph_hist = hist;
     }
     auto capture = [&](int jj) {                                 // capture on a private stream, replay on ours
       if (!cap_stream) CK(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
@@ -2150,7 +2162,7 @@ gemslr_status gemslr_setup(gemslr_ctx *c, gemslr_dtype dtype, int64_t n, const i
   if (prm->levels < 1 || prm->subdomains < 1 || prm->rank < 0 || (dtype != GEMSLR_F64 && dtype != GEMSLR_C128) ||
       (prm->ilu != GEMSLR_ILU0 && prm->ilu != GEMSLR_ILUT) || prm->ilut_drop < 0)
     return fail(c, GEMSLR_ERR_INVALID_ARG, "levels < 1, subdomains < 1, rank < 0 or bad dtype/ilu");
-  if (2 * prm->rank + 2 > GS_MAXC) return fail(c, GEMSLR_ERR_INVALID_ARG, "rank > 50 not supported (cycle 2k <= 102)");
+  if (2 * prm->rank + 2 > GS_MAXC) return fail(c, GEMSLR_ERR_INVALID_ARG, "rank > 51 not supported (Arnoldi cycle 2k + 1 <= 103 columns)");
   if (prm->root_inner_its < 0 || prm->root_inner_its + 2 > GS_MAXC ||
       (prm->root_inner_its > 0 && c->comm.nranks > 1))
     return fail(c, GEMSLR_ERR_INVALID_ARG, "root_inner_its < 0, too large, or with several ranks (one GPU only)");

@@ -1032,8 +1032,10 @@ __device__ inline void reduce_partials(const T *partial, int G, int ncol, T *out
 // the last CTA reduces the partials in CTA order into this rank's part of
 // s = W^H r_J (summed over ranks by an all-reduce).
 // CTA = 8 warps; a tile is 256 rows; warp w owns the columns c ≡ w (mod 8).
-constexpr int EW_NACC = 6;   // k <= 48
-template <typename T>
+// NACC accumulators per warp: k <= 8 NACC (instances 1, 2, 3, 4, 6, 8: k <= 64,
+// chosen per level by ew_nacc on the host; the rank check of gemslr_setup keeps k <= 52).
+constexpr int EW_MAXK = 64;
+template <typename T, int NACC>
 __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const int64_t *__restrict__ Eptr,
                                             const int32_t *__restrict__ Ecol, const T *__restrict__ Eval,
                                             const T *__restrict__ z, const T *__restrict__ zh, int64_t nloc,
@@ -1044,9 +1046,9 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
   __shared__ T sv[256];
   __shared__ bool amlast;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  T acc[EW_NACC];
+  T acc[NACC];
 #pragma unroll
-  for (int a = 0; a < EW_NACC; ++a) acc[a] = dzero<T>();
+  for (int a = 0; a < NACC; ++a) acc[a] = dzero<T>();
   const int64_t ntiles = (s + 255) / 256;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * 256 + tid;
@@ -1061,7 +1063,7 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
       sv[tid] = v;
       __syncthreads();
 #pragma unroll
-      for (int a = 0; a < EW_NACC; ++a) {
+      for (int a = 0; a < NACC; ++a) {
         const int c = warp + 8 * a;
         if (c < k) {
 #pragma unroll
@@ -1076,7 +1078,7 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
   }
   if (k == 0) return;
 #pragma unroll
-  for (int a = 0; a < EW_NACC; ++a) {
+  for (int a = 0; a < NACC; ++a) {
     const int c = warp + 8 * a;
     T r = warp_sum(acc[a]);
     if (lane == 0 && c < k) partial[(int64_t)c * gridDim.x + blockIdx.x] = r;
@@ -1100,7 +1102,7 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
 // The flag is a generation counter in device memory: every CTA reads it before
 // taking its ticket, the last CTA (which takes the final ticket, so after every
 // read) advances it — no host-side epoch, so the launch can live in a CUDA graph.
-template <typename T>
+template <typename T, int NACC>
 __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const int64_t *__restrict__ Eptr,
                                              const int32_t *__restrict__ Ecol, const T *__restrict__ Eval,
                                              const T *__restrict__ z, const T *__restrict__ zh, int64_t nloc,
@@ -1116,9 +1118,9 @@ __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const i
   __shared__ bool amlast;
   __shared__ int gen0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  T acc[EW_NACC];
+  T acc[NACC];
 #pragma unroll
-  for (int a = 0; a < EW_NACC; ++a) acc[a] = dzero<T>();
+  for (int a = 0; a < NACC; ++a) acc[a] = dzero<T>();
   const int64_t ntiles = (s + 255) / 256;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * 256 + tid;
@@ -1132,7 +1134,7 @@ __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const i
     sv[tid] = v;
     __syncthreads();
 #pragma unroll
-    for (int a = 0; a < EW_NACC; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       const int c = warp + 8 * a;
       if (c < k) {
 #pragma unroll
@@ -1145,7 +1147,7 @@ __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const i
     __syncthreads();
   }
 #pragma unroll
-  for (int a = 0; a < EW_NACC; ++a) {
+  for (int a = 0; a < NACC; ++a) {
     const int c = warp + 8 * a;
     T r = warp_sum(acc[a]);
     if (lane == 0 && c < k) partial[(int64_t)c * gridDim.x + blockIdx.x] = r;

@@ -118,6 +118,47 @@ def test_ilut_drops_relative_to_row_norm():
     assert f.L.nnz == 1 and f.L[1, 0] == pytest.approx(1e-6)
 
 
+def _csr(rows, n):
+    M = np.zeros((n, n))
+    for i, r in enumerate(rows):
+        for j, v in r.items():
+            M[i, j] = v
+    return sp.csr_matrix(M)
+
+
+def test_ilut_keeps_the_lfil_largest_with_ties_to_smaller_column():
+    """Saad's ILUT (reading Q9) keeps the lfil LARGEST |w_j| of the L part
+    and of the U part, ties to the smaller column — hand-computed rows where the largest
+    are not the first columns (identity rows elsewhere: no elimination, no fill)."""
+    lo = _csr([{0: 1}, {1: 1}, {2: 1}, {3: 1}, {0: 0.1, 1: 0.5, 2: -0.3, 3: -0.5, 4: 1}], 5)
+    for lfil, keep in ((1, [1]), (2, [1, 3]), (3, [1, 2, 3]), (4, [0, 1, 2, 3])):
+        f = oracle.Ilu(lo, oracle.ILUT, tau=1e-3, lfil=lfil)
+        L = f.L.toarray()
+        assert sorted(np.nonzero(L[4])[0].tolist()) == keep, (lfil, L[4])
+        assert np.array_equal(L[4, keep], lo.toarray()[4, keep])
+        assert np.array_equal(f.U.toarray(), np.eye(5))
+    up = _csr([{0: 1, 1: 0.2, 2: -0.7, 3: 0.7, 4: 0.4}, {1: 1}, {2: 1}, {3: 1}, {4: 1}], 5)
+    for lfil, keep in ((1, [0, 2]), (2, [0, 2, 3]), (3, [0, 2, 3, 4])):
+        f = oracle.Ilu(up, oracle.ILUT, tau=1e-3, lfil=lfil)
+        U = f.U.toarray()
+        assert sorted(np.nonzero(U[0])[0].tolist()) == keep, (lfil, U[0])
+        assert np.array_equal(U[0, keep], up.toarray()[0, keep])
+        assert f.L.nnz == 0
+
+
+def test_ilut_selects_after_elimination():
+    """The lfil selection acts on the eliminated row w (Saad's order, reading Q9): a dropped
+    L multiplier still updated the row before it was dropped.  Hand-computed:
+    row 2 = [1, 0.6, 4]: w_0 = 1/2 = 0.5 (then w_2 = 4 - 0.5*3 = 2.5), w_1 = 0.6;
+    lfil = 1 keeps l_21 = 0.6 (the larger, not the first), u_22 = 2.5."""
+    A = _csr([{0: 2, 2: 3}, {1: 1}, {0: 1, 1: 0.6, 2: 4}], 3)
+    f = oracle.Ilu(A, oracle.ILUT, tau=1e-3, lfil=1)
+    assert np.array_equal(f.L.toarray(), np.array([[0, 0, 0], [0, 0, 0], [0, 0.6, 0]]))
+    assert np.array_equal(f.U.toarray(), np.array([[2, 0, 3], [0, 1, 0], [0, 0, 2.5]]))
+    f = oracle.Ilu(A, oracle.ILUT, tau=1e-3, lfil=2)             # both kept: exact LU
+    assert np.abs(((f.L + sp.identity(3)) @ f.U - A).toarray()).max() < 1e-15
+
+
 # ---------------------------------------------------------------- apply (c4)
 def _exact_precond(prob, levels, p):
     A = prob.scipy()
@@ -144,6 +185,42 @@ def test_exact_mode_apply_is_inverse_D2(kind, dims, levels, p):
     yn = Pc.apply_natural(b)
     refn = np.linalg.solve(A.toarray(), b)
     assert np.linalg.norm(yn - refn) <= 1e-10 * np.linalg.norm(refn)
+
+
+def _rand_unitary(s, cplx, seed):
+    r = rng(seed)
+    M = r.standard_normal((s, s)) + (1j * r.standard_normal((s, s)) if cplx else 0)
+    Q, _ = np.linalg.qr(M)
+    return Q
+
+
+@pytest.mark.parametrize("kind,dims,levels,p", [("hz", (5, 5, 4), 2, 2), ("hz", (8, 7), 1, 4),
+                                                ("cd", (6, 6, 4), 2, 4)])
+def test_exact_mode_rotated_basis_D2(kind, dims, levels, p):
+    """Exact mode with W = Q, a random unitary (orthogonal for real A), and R = Q^H Ĝ Q:
+    the correction W[(I-R)^{-1} - I]W^H = (I - Ĝ)^{-1} - I is basis-invariant
+    (P:L401-404), so the apply is still Â^{-1}.  With a non-identity complex W a missing
+    conjugate in s = W^H z2, or a transposed W or G, breaks the identity (W = I hides it).
+    The same for the root preconditioner P = C_0^{-1}(I + W_0 G_0 W_0^H) = Ŝ_0^{-1} of
+    NEXT-1 (lowrank_add): one root GMRES step is then exact."""
+    prob = {"cd": P.convdiff_upwind, "hz": P.helmholtz_shifted}[kind](dims)
+    A = prob.scipy()
+    st = D.tiny_structure(A, prob.coords, levels, p, nlast=1)
+    Pc = oracle.Precond(A, st, ilu=(oracle.ILUT, 0.0, 10**6))
+    L = len(st["level_off"]) - 1
+    for l in range(L - 1, -1, -1):
+        Gm = D.dense_ghat(Pc, l)
+        Q = _rand_unitary(Gm.shape[0], prob.is_complex, 40 + l)
+        assert np.abs(Q - np.eye(Gm.shape[0])).max() > 0.1
+        I = np.eye(Gm.shape[0])
+        R = Q.conj().T @ Gm @ Q
+        Pc.set_lowrank(l, Q, np.linalg.inv(I - R) - I)
+    Ah = D.permute_matrix(A, st["perm"]).toarray()
+    b = P.rhs_vector(prob.n, prob.is_complex, 7)
+    ref = np.linalg.solve(Ah, b)
+    assert np.linalg.norm(Pc.apply(b) - ref) <= 1e-10 * np.linalg.norm(ref)
+    Pc.set_root_its(1)
+    assert np.linalg.norm(Pc.apply(b) - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
 def test_ilu0_fullrank_is_exact_on_interface_D2():

@@ -1,0 +1,57 @@
+"""Mutation check of the oracle pins (CPU): each mutation of oracle/oracle.cpp below
+must turn at least one test of tests/test_oracle_pins.py red.  The original file is
+restored (and liboracle.so rebuilt) afterwards.
+
+  python tools/mutation_check.py
+"""
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "oracle", "oracle.cpp")
+
+MUTATIONS = {
+    "apply: s = W^T z2 (conjugate dropped)": (
+        "\n          for (int64_t i = 0; i < sl; ++i) acc += conjv(W[l][c * sl + i]) * rJ[i];",
+        "\n          for (int64_t i = 0; i < sl; ++i) acc += W[l][c * sl + i] * rJ[i];"),
+    "root preconditioner: s = W^T z2 (conjugate dropped)": (
+        "\n      for (int64_t i = 0; i < sl; ++i) acc += conjv(W[l][c * sl + i]) * rJ[i];",
+        "\n      for (int64_t i = 0; i < sl; ++i) acc += W[l][c * sl + i] * rJ[i];"),
+    "ILUT: keep the first lfil columns": (
+        "    std::sort(lo.begin(), lo.end(), bigger);\n    std::sort(up.begin(), up.end(), bigger);",
+        "    std::sort(lo.begin(), lo.end(), [](auto &a, auto &b) { return a.second < b.second; });\n"
+        "    std::sort(up.begin(), up.end(), [](auto &a, auto &b) { return a.second < b.second; });"),
+    "ILUT: ties to the larger column": (
+        "      return a.second < b.second;\n    };",
+        "      return a.second > b.second;\n    };"),
+    "apply: t = G^T s": (
+        "\n          for (int c = 0; c < kl; ++c) acc += G[l][c * kl + a] * sv[c];",
+        "\n          for (int c = 0; c < kl; ++c) acc += G[l][a * kl + c] * sv[c];"),
+}
+
+
+def run():
+    orig = open(SRC).read()
+    bad = []
+    try:
+        for name, (a, b) in MUTATIONS.items():
+            assert orig.count(a) == 1, f"mutation anchor not unique: {name}"
+            open(SRC, "w").write(orig.replace(a, b))
+            r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", os.path.join(ROOT, "tests", "test_oracle_pins.py")],
+                               cwd=ROOT, capture_output=True, text=True)
+            caught = r.returncode != 0
+            print(f"{'caught' if caught else 'MISSED'}: {name}")
+            if not caught:
+                bad.append(name)
+    finally:
+        open(SRC, "w").write(orig)
+        sys.path.insert(0, ROOT)
+        import oracle
+        oracle.build(force=True)
+    return bad
+
+
+if __name__ == "__main__":
+    sys.exit(1 if run() else 0)
