@@ -11,8 +11,10 @@ Krylov basis ~2.4 GB) exceeds the 126 MB L2, so no flush is needed.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
---impl reference times the plain CPU oracle (oracle/) on bounded samples of
-the same workload on the host cores.
+--gpus N > 1 without a torch.distributed environment re-launches itself under
+torch.distributed.run with N ranks (one process per GPU, NCCL); under torchrun
+WORLD_SIZE must equal N.  --impl reference times the plain CPU oracle (oracle/)
+on bounded samples of the same workload on the host cores.
 """
 from __future__ import annotations
 
@@ -34,6 +36,36 @@ from synth import problems as P  # noqa: E402
 
 METRIC = "FGMRES solve-phase ms/iteration (HBM GB/s fraction in roofline)"
 UNIT = "ms/iteration"
+
+
+def cpu_info():
+    """CPU model, sockets, physical cores (the oracle's timing context)."""
+    model, sockets = None, set()
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name") and model is None:
+                model = line.split(":", 1)[1].strip()
+            if line.startswith("physical id"):
+                sockets.add(line.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False) or os.cpu_count()
+        mem = round(psutil.virtual_memory().total / 2**30, 1)
+    except Exception:
+        phys, mem = os.cpu_count(), None
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except Exception:
+        avail = os.cpu_count()
+    return {"model": model, "sockets": len(sockets) or 1, "physical_cores": phys, "logical_cpus_available": avail,
+            "mem_gib": mem}
+
+
+def oracle_threads():
+    info = cpu_info()
+    return max(1, min(info["physical_cores"] or 1, info["logical_cpus_available"] or 1)), info
 
 
 def peaks():
@@ -171,7 +203,7 @@ def run_ours(args):
     s.solve(bd, rtol=1e-300, restart=restart, maxit=max(W, 1))
     torch.cuda.synchronize()
 
-    def timed(profile):
+    def timed(profile, maxit=None):
         if profile:
             s.profile(True, reset=True)
         if world > 1:
@@ -180,7 +212,7 @@ def run_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        out = s.solve(bd, rtol=1e-300, restart=restart, maxit=K)
+        out = s.solve(bd, rtol=1e-300, restart=restart, maxit=maxit or K)
         e1.record(stream)
         torch.cuda.synchronize()
         if profile:
@@ -198,6 +230,11 @@ def run_ours(args):
     its = out["its"]
     assert its == K, (its, K)
     ms_per = ms / its
+    # the cost of an iteration grows with its column in the restart cycle (CGS2 reads
+    # j + 1 basis vectors): one whole cycle of `restart` iterations, timed the same way
+    ms_cyc, _ = timed(False, maxit=restart)
+    cycle = {"iterations": restart, "ms_per_iteration": round(ms_cyc / restart, 4),
+             "note": "one full restart cycle (columns 1..m); value/ms_per_step cover the first K columns"}
     # per-kernel CUDA-event timing over a second identical timed region
     ms_prof, out2 = timed(True)
     stats = s.stats()
@@ -223,14 +260,20 @@ def run_ours(args):
         per_kernel[kname] = rec
     dom = max((k for k in per_kernel if k in gb), key=lambda k: per_kernel[k]["ms_total"])
     dd = per_kernel[dom]
-    traffic = None                                   # DRAM bytes per launch from the committed ncu launch list
+    traffic, traffic_src = None, None                # DRAM bytes per launch, ncu capture of this bench command
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            traffic = json.load(f).get(dom)
+        import glob
+        caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+        if caps:
+            with open(caps[-1]) as f:
+                tj = json.load(f)
+            traffic = tj.get(dom)
+            traffic_src = f"profiles/{os.path.basename(caps[-1])} ({tj.get('_capture', 'ncu --set full of this command')})"
     except Exception:
         traffic = None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": dd["GBps"], "peak": peak, "unit": "GB/s",
-                "frac": dd["frac"], "traffic": round(traffic) if traffic else None, "peak_source": peak_src,
+                "frac": dd["frac"], "traffic": round(traffic) if traffic else None, "traffic_source": traffic_src,
+                "peak_source": peak_src,
                 "bytes_per_launch": round(gb[dom] / dd["launches"]), "us_per_launch": dd["us_per_launch"]}
     # The triangular solves are bound by their level depth, not by HBM:
     # the latency account of the dominant class — level-barrier rounds per launch set
@@ -280,7 +323,10 @@ def run_ours(args):
                    "parallelism": "1 GPU" if world == 1 else f"subdomain row partition over {world} GPUs (NCCL send/recv halos, all-reduce)",
                    "l2": "working set (~2.4 GB) > 126 MB L2; no flush",
                    "setup_s": round(setup_s, 2), "timed_region": f"{K} FGMRES iterations (maxit=K, unreachable rtol)"},
-        "roofline": roofline, "kernels": per_kernel, "ms_per_step_profiled": round(ms_prof / out2["its"], 4),
+        "cycle": cycle, "roofline": roofline, "kernels": per_kernel,
+        "ms_per_step_profiled": round(ms_prof / out2["its"], 4),
+        "profiled_note": "per-kernel CUDA events around every launch of a second identical K-iteration solve "
+                         "(no graphs, done flag read every iteration: no no-op launches)",
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
     }
     if cpu is not None:
@@ -292,14 +338,17 @@ def run_ours(args):
 
 
 def cpu_baseline(prob, prm, s, b, iters):
-    """The oracle as it stands (single-threaded C++), bounded sample: `iters` FGMRES
-    iterations of the same workload on the same exported setup bundle."""
+    """The oracle as it stands (C++ with OpenMP over independent work and fixed-order
+    reductions), bounded sample: `iters` FGMRES iterations of the same workload on the
+    same exported setup bundle, with all physical cores and with one thread."""
     import oracle
     from tests.bundle_io import Bundle
+    nth, info = oracle_threads()
     with tempfile.TemporaryDirectory() as d:
         s.export(d)
         B = Bundle(d)
         st = B.structure()
+        oracle.set_threads(nth)
         t0 = time.perf_counter()
         kind = oracle.ILU0 if prm["ilu"] == "ilu0" else oracle.ILUT
         Pc = oracle.Precond(prob, st, ilu=(kind, prm["ilut_drop"], prm["ilut_fill"]))
@@ -308,12 +357,17 @@ def cpu_baseline(prob, prm, s, b, iters):
             if lr is not None:
                 Pc.set_lowrank(l, lr[0], lr[2])
         t_setup = time.perf_counter() - t0
-        t1 = time.perf_counter()
-        out = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=iters)
-        dt = time.perf_counter() - t1
-    return {"value": round(1e3 * dt / out["its"], 2), "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{out['its']} FGMRES iterations of the same {prob.n}-row workload (oracle factor setup "
-                      f"{t_setup:.1f}s excluded)", "threads": 1}
+        res = {}
+        for nt, its in ((nth, iters), (1, max(iters // 2, 2))):
+            oracle.set_threads(nt)
+            t1 = time.perf_counter()
+            out = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=its)
+            res[nt] = (1e3 * (time.perf_counter() - t1) / out["its"], out["its"])
+    return {"value": round(res[nth][0], 2), "unit": UNIT, "cores": nth, "kind": "oracle",
+            "sample": f"{res[nth][1]} FGMRES iterations of the same {prob.n}-row workload on the same setup bundle "
+                      f"(oracle factor setup {t_setup:.1f}s excluded)",
+            "threads": nth, "one_thread": {"value": round(res[1][0], 2), "iterations": res[1][1]},
+            "cpu": info}
 
 
 def run_reference(args):
@@ -323,6 +377,8 @@ def run_reference(args):
         return
     import oracle
     from oracle import dense as D
+    nth, info = oracle_threads()
+    oracle.set_threads(nth)
     name = args.config
     prob, b, xt, prm = P.make_config(name, gpus=1)
     t0 = time.perf_counter()
@@ -341,7 +397,7 @@ def run_reference(args):
             "warmup": W, "ms_per_step": round(val, 2), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded 7-pt Laplacian, b = A x_true)",
             "config": {"workload": f"{name} per-GPU problem {prob.dims}", "n": prob.n, "setup_s": round(setup, 1)},
-            "cpu_baseline": {"value": round(val, 2), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": round(val, 2), "unit": UNIT, "cores": nth, "kind": "oracle", "cpu": info,
                              "sample": f"{out['its']} FGMRES iterations, oracle's own RCB structure, ILU and "
                                        f"one-cycle Arnoldi low rank (setup {setup:.0f}s excluded)"},
             "e2e": {"value": round(val, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -362,6 +418,18 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        # one process per GPU: re-launch under torch.distributed.run (NCCL over NVLink)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if world is not None and int(world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (one rank per GPU)")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -21,9 +21,10 @@ _lib = None
 
 
 def build(force=False):
-    """Compile liboracle.so (g++ -O2 -ffp-contract=off; reading Q22)."""
+    """Compile liboracle.so (g++ -O2 -ffp-contract=off -fopenmp; reading Q22; thread-count
+    independent results, oracle.cpp header)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        cmd = ["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fPIC", "-shared",
+        cmd = ["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
                "-o", _SO + ".tmp", _SRC]
         subprocess.check_call(cmd)
         os.replace(_SO + ".tmp", _SO)
@@ -37,6 +38,8 @@ def lib():
         L = C.CDLL(_SO)
         vp, i64, i32p, i64p, dp = C.c_void_p, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_double)
         L.or_spmv.argtypes = [C.c_int, i64, vp, vp, vp, vp, vp]
+        L.or_set_threads.argtypes = [C.c_int]
+        L.or_get_threads.restype = C.c_int
         L.or_ilu_create.argtypes = [C.c_int, i64, vp, vp, vp, C.c_int, C.c_double, C.c_int, C.c_char_p, C.c_int]
         L.or_ilu_create.restype = vp
         L.or_ilu_nnz.argtypes = [vp, C.c_int]
@@ -61,6 +64,15 @@ def lib():
         L.or_fgmres.restype = C.c_int
         _lib = L
     return _lib
+
+
+def set_threads(n):
+    """OpenMP threads of the oracle (results are the same for any count)."""
+    lib().or_set_threads(int(n))
+
+
+def get_threads():
+    return int(lib().or_get_threads())
 
 
 def _p(a):

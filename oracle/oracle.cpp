@@ -22,6 +22,12 @@
 //
 // Pins: see tests/test_oracle_pins.py (closed forms, textbook special cases,
 // dense LU/Schur on tiny problems).  Nothing here is "parity unpinned".
+//
+// Threads: OpenMP only over independent work — rows of a
+// SpMV or a vector update, the subdomain blocks of one level (B_l is block
+// diagonal), the k columns of W^H z2.  The two reductions over vector entries
+// (dot, nrm2) sum fixed chunks of kChunk entries in ascending order and then the
+// chunk sums in ascending order, so every result is the same for any thread count.
 // ============================================================================
 #include <algorithm>
 #include <cmath>
@@ -32,6 +38,9 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 using zc = std::complex<double>;
 
@@ -56,6 +65,7 @@ struct Csr {
 // ---- c2: plain SpMV, natural order, j ascending ----------------
 template <typename T>
 void spmv(const Csr<T> &A, const T *x, T *y) {
+#pragma omp parallel for schedule(static) if (A.n > 4096)
   for (int64_t i = 0; i < A.n; ++i) {
     T s = T(0);
     for (int64_t p = A.ptr[i]; p < A.ptr[i + 1]; ++p) s += A.val[p] * x[A.col[p]];
@@ -66,6 +76,7 @@ void spmv(const Csr<T> &A, const T *x, T *y) {
 // y -= A x
 template <typename T>
 void spmv_sub(const Csr<T> &A, const T *x, T *y) {
+#pragma omp parallel for schedule(static) if (A.n > 4096)
   for (int64_t i = 0; i < A.n; ++i) {
     T s = T(0);
     for (int64_t p = A.ptr[i]; p < A.ptr[i + 1]; ++p) s += A.val[p] * x[A.col[p]];
@@ -263,16 +274,33 @@ Ilu<T> factor(const Csr<T> &B, int type, double tau, int lfil, std::string &err)
 // verified by tests/); everything else the oracle computes itself from its
 // own A: Â = Pᵀ A P, B_l, E_l, F_l (Q3), its own
 // ILU factors of every block.
+constexpr int64_t kChunk = 8192;           // fixed reduction chunk (thread-count independent)
 template <typename T>
 T dot(int64_t n, const T *x, const T *y) {  // Σ conj(x_i) y_i (reading Q30)
+  const int64_t nc = (n + kChunk - 1) / kChunk;
+  std::vector<T> part(nc, T(0));
+#pragma omp parallel for schedule(static) if (nc > 1)
+  for (int64_t c = 0; c < nc; ++c) {
+    T s = T(0);
+    for (int64_t i = c * kChunk; i < std::min(n, (c + 1) * kChunk); ++i) s += conjv(x[i]) * y[i];
+    part[c] = s;
+  }
   T s = T(0);
-  for (int64_t i = 0; i < n; ++i) s += conjv(x[i]) * y[i];
+  for (int64_t c = 0; c < nc; ++c) s += part[c];
   return s;
 }
 template <typename T>
 double nrm2(int64_t n, const T *x) {
+  const int64_t nc = (n + kChunk - 1) / kChunk;
+  std::vector<double> part(nc, 0.0);
+#pragma omp parallel for schedule(static) if (nc > 1)
+  for (int64_t c = 0; c < nc; ++c) {
+    double s = 0.0;
+    for (int64_t i = c * kChunk; i < std::min(n, (c + 1) * kChunk); ++i) s += abs2(x[i]);
+    part[c] = s;
+  }
   double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s += abs2(x[i]);
+  for (int64_t c = 0; c < nc; ++c) s += part[c];
   return std::sqrt(s);
 }
 
@@ -300,6 +328,7 @@ struct Precond {
     const int64_t sl = s(l);
     const int kl = k[l];
     std::vector<T> sv(kl, T(0)), tv(kl, T(0));
+#pragma omp parallel for schedule(static)
     for (int c = 0; c < kl; ++c) {                 // s = W^H z2
       T acc = T(0);
       for (int64_t i = 0; i < sl; ++i) acc += conjv(W[l][c * sl + i]) * rJ[i];
@@ -310,6 +339,7 @@ struct Precond {
       for (int c = 0; c < kl; ++c) acc += G[l][c * kl + a] * sv[c];
       tv[a] = acc;
     }
+#pragma omp parallel for schedule(static) if (sl > 4096)
     for (int64_t i = 0; i < sl; ++i) {             // z2 += W t
       T acc = T(0);
       for (int c = 0; c < kl; ++c) acc += W[l][c * sl + i] * tv[c];
@@ -319,14 +349,18 @@ struct Precond {
 
   // B_l^{-1} approximated blockwise: x[I_l] = U^-1 L^-1 b[I_l] per block
   void block_solve(int l, const T *b, T *x) const {
-    for (size_t q = 0; q + 1 < blk[l].size(); ++q) {
+    const int64_t nb = (int64_t)blk[l].size() - 1;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < nb; ++q) {
       const int64_t a = blk[l][q] - o[l];
       lusolve(fac[l][q], b + a, x + a);
     }
   }
   // C_{L-1}^{-1} by block-Jacobi ILU of the RCM-ordered last separator
   void last_solve(const T *b, T *x) const {
-    for (size_t q = 0; q + 1 < last.size(); ++q) {
+    const int64_t nb = (int64_t)last.size() - 1;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < nb; ++q) {
       const int64_t a = last[q] - o[L];
       lusolve(lastfac[q], b + a, x + a);
     }
@@ -352,6 +386,7 @@ struct Precond {
         const int64_t sl = s(l);
         const int kl = k[l];
         std::vector<T> sv(kl, T(0)), tv(kl, T(0));
+#pragma omp parallel for schedule(static)
         for (int c = 0; c < kl; ++c) {                 // s = W^H z2
           T acc = T(0);
           for (int64_t i = 0; i < sl; ++i) acc += conjv(W[l][c * sl + i]) * rJ[i];
@@ -362,6 +397,7 @@ struct Precond {
           for (int c = 0; c < kl; ++c) acc += G[l][c * kl + a] * sv[c];
           tv[a] = acc;
         }
+#pragma omp parallel for schedule(static) if (sl > 4096)
         for (int64_t i = 0; i < sl; ++i) {             // z2 += W t
           T acc = T(0);
           for (int c = 0; c < kl; ++c) acc += W[l][c * sl + i] * tv[c];
@@ -378,6 +414,7 @@ struct Precond {
       std::vector<T> t(nI, T(0)), w(nI, T(0));
       spmv(F[l], yJ, t.data());                        // F_l y2
       block_solve(l, t.data(), w.data());              // U^-1 L^-1 F_l y2
+#pragma omp parallel for schedule(static) if (nI > 4096)
       for (int64_t i = 0; i < nI; ++i) yI[i] = z[l][i] - w[i];   // y1 = z1 - ...
     }
     std::copy(y.begin(), y.end(), y_out);
@@ -526,12 +563,14 @@ FgmresOut<T> fgmres(const Csr<T> &A, precond_fn M, void *Muser, const T *b, T *x
   std::vector<T> sn(m);
   auto resid = [&]() {                                      // r = b - A x
     spmv(A, x, r.data());
+#pragma omp parallel for schedule(static) if (n > 4096)
     for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
     return nrm2(n, r.data());
   };
   double beta = resid();
   out.hist.push_back(beta / bnorm);
   while (beta > rtol * bnorm && out.its < maxit) {
+#pragma omp parallel for schedule(static) if (n > 4096)
     for (int64_t i = 0; i < n; ++i) V[i] = r[i] / beta;
     std::fill(g.begin(), g.end(), T(0));
     std::fill(H.begin(), H.end(), T(0));
@@ -546,15 +585,13 @@ FgmresOut<T> fgmres(const Csr<T> &A, precond_fn M, void *Muser, const T *b, T *x
       const double eta = nrm2(n, w.data());
       std::vector<T> h(j + 1), h2(j + 1);
       for (int i = 0; i <= j; ++i) h[i] = dot(n, V.data() + (size_t)i * n, w.data());   // pass 1
-      for (int i = 0; i <= j; ++i) {
-        const T *vi = V.data() + (size_t)i * n;
-        for (int64_t q = 0; q < n; ++q) w[q] -= vi[q] * h[i];
-      }
+#pragma omp parallel for schedule(static) if (n > 4096)
+      for (int64_t q = 0; q < n; ++q)                       // w -= V h (per entry, i ascending)
+        for (int i = 0; i <= j; ++i) w[q] -= V[(size_t)i * n + q] * h[i];
       for (int i = 0; i <= j; ++i) h2[i] = dot(n, V.data() + (size_t)i * n, w.data());  // pass 2
-      for (int i = 0; i <= j; ++i) {
-        const T *vi = V.data() + (size_t)i * n;
-        for (int64_t q = 0; q < n; ++q) w[q] -= vi[q] * h2[i];
-      }
+#pragma omp parallel for schedule(static) if (n > 4096)
+      for (int64_t q = 0; q < n; ++q)                       // w -= V h2
+        for (int i = 0; i <= j; ++i) w[q] -= V[(size_t)i * n + q] * h2[i];
       const double hnext = nrm2(n, w.data());
       for (int i = 0; i <= j; ++i) H[(size_t)j * (m + 1) + i] = h[i] + h2[i];
       H[(size_t)j * (m + 1) + j + 1] = hnext;
@@ -590,6 +627,7 @@ FgmresOut<T> fgmres(const Csr<T> &A, precond_fn M, void *Muser, const T *b, T *x
       jend = j + 1;
       if (absval(g[j + 1]) <= rtol * bnorm || hnext <= 1e-14 * eta || out.its >= maxit) break;
       T *vn = V.data() + (size_t)(j + 1) * n;
+#pragma omp parallel for schedule(static) if (n > 4096)
       for (int64_t q = 0; q < n; ++q) vn[q] = w[q] / hnext;
     }
     if (diag) {
@@ -625,10 +663,9 @@ FgmresOut<T> fgmres(const Csr<T> &A, precond_fn M, void *Muser, const T *b, T *x
       for (int c = i + 1; c < jend; ++c) s -= H[(size_t)c * (m + 1) + i] * y[c];
       y[i] = s / H[(size_t)i * (m + 1) + i];
     }
-    for (int c = 0; c < jend; ++c) {                         // x += Z y
-      const T *zc = Z.data() + (size_t)c * n;
-      for (int64_t q = 0; q < n; ++q) x[q] += zc[q] * y[c];
-    }
+#pragma omp parallel for schedule(static) if (n > 4096)
+    for (int64_t q = 0; q < n; ++q)                          // x += Z y (per entry, c ascending)
+      for (int c = 0; c < jend; ++c) x[q] += Z[(size_t)c * n + q] * y[c];
     const double est = out.hist.back();
     beta = resid();                                          // explicit residual
     out.max_est_gap = std::max(out.max_est_gap, std::fabs(est - beta / bnorm));
@@ -713,25 +750,32 @@ Precond<T> *build_precond(int64_t n, const int64_t *rowptr, const int32_t *col, 
     std::vector<int64_t> b(blk_off + pos, blk_off + pos + nblk[l] + 1);
     pos += nblk[l] + 1;
     P->blk.push_back(b);
-    std::vector<Ilu<T>> f;
+    std::vector<Ilu<T>> f(nblk[l]);                // blocks of B_l are independent
+    std::vector<std::string> errs(nblk[l]);
+#pragma omp parallel for schedule(dynamic, 1)
     for (int q = 0; q < nblk[l]; ++q) {
       Csr<T> B = submatrix(P->Ahat, b[q], b[q + 1], b[q], b[q + 1]);
       add_diag(B, sigma);
-      f.push_back(factor(B, ilu_type, tau, lfil, err));
-      if (!err.empty()) { err += " (level " + std::to_string(l) + ", block " + std::to_string(q) + ")"; delete P; return nullptr; }
+      f[q] = factor(B, ilu_type, tau, lfil, errs[q]);
     }
+    for (int q = 0; q < nblk[l]; ++q)
+      if (!errs[q].empty()) { err = errs[q] + " (level " + std::to_string(l) + ", block " + std::to_string(q) + ")"; delete P; return nullptr; }
     P->fac.push_back(std::move(f));
     if (l == 0) P->C0 = submatrix(P->Ahat, P->o[1], n, P->o[1], n);
     P->E.push_back(submatrix(P->Ahat, P->o[l + 1], n, P->o[l], P->o[l + 1]));
     P->F.push_back(submatrix(P->Ahat, P->o[l], P->o[l + 1], P->o[l + 1], n));
   }
   P->last.assign(last_off, last_off + nlast + 1);
+  P->lastfac.resize(nlast);
+  std::vector<std::string> errs(nlast);
+#pragma omp parallel for schedule(dynamic, 1)
   for (int q = 0; q < nlast; ++q) {
     Csr<T> C = submatrix(P->Ahat, P->last[q], P->last[q + 1], P->last[q], P->last[q + 1]);
     add_diag(C, sigma);
-    P->lastfac.push_back(factor(C, ilu_type, tau, lfil, err));
-    if (!err.empty()) { err += " (C_last block " + std::to_string(q) + ")"; delete P; return nullptr; }
+    P->lastfac[q] = factor(C, ilu_type, tau, lfil, errs[q]);
   }
+  for (int q = 0; q < nlast; ++q)
+    if (!errs[q].empty()) { err = errs[q] + " (C_last block " + std::to_string(q) + ")"; delete P; return nullptr; }
   return P;
 }
 
@@ -763,6 +807,22 @@ void copy_csr(const Csr<T> &A, int64_t *ptr, int64_t *col, void *val) {
 // extern "C" surface for tests/oracle_py.py (ctypes)
 // ============================================================================
 extern "C" {
+
+// OpenMP threads of the oracle (results do not depend on it; bench.py times 1 and all cores)
+void or_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n > 0 ? n : 1);
+#else
+  (void)n;
+#endif
+}
+int or_get_threads() {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
 
 void or_spmv(int cplx, int64_t n, const int64_t *rowptr, const int32_t *col, const void *val,
              const void *x, void *y) {
@@ -886,16 +946,20 @@ void or_precond_natural(void *hv, const void *in, void *out) {
   if (h->is_cplx) {
     const zc *x = static_cast<const zc *>(in);
     std::vector<zc> a(n), b(n);
+#pragma omp parallel for schedule(static) if (n > 4096)
     for (int64_t i = 0; i < n; ++i) a[i] = x[h->perm[i]];
     static_cast<Precond<zc> *>(h->p)->apply_from(0, a.data(), b.data());
     zc *y = static_cast<zc *>(out);
+#pragma omp parallel for schedule(static) if (n > 4096)
     for (int64_t i = 0; i < n; ++i) y[h->perm[i]] = b[i];
   } else {
     const double *x = static_cast<const double *>(in);
     std::vector<double> a(n), b(n);
+#pragma omp parallel for schedule(static) if (n > 4096)
     for (int64_t i = 0; i < n; ++i) a[i] = x[h->perm[i]];
     static_cast<Precond<double> *>(h->p)->apply_from(0, a.data(), b.data());
     double *y = static_cast<double *>(out);
+#pragma omp parallel for schedule(static) if (n > 4096)
     for (int64_t i = 0; i < n; ++i) y[h->perm[i]] = b[i];
   }
 }

@@ -1802,7 +1802,9 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
       // iterations queued (a synchronous copy would drain the stream; with a lag
       // of 2 a host hiccup of ~2 ms starved the GPU in some bench runs).  After
       // convergence at most kLag queued iterations run, every kernel exiting at once.
-      constexpr int kLag = 6;
+      // (profiling: lag 0, so no iteration is queued after the last one and every
+      // timed launch is a real one)
+      const int kLag = ctx->prof.on ? 0 : 6;
       CK(cudaMemcpyAsync(hflags + j, done, sizeof(int), cudaMemcpyDeviceToHost, s));
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

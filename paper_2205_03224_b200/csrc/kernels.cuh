@@ -695,6 +695,10 @@ template <typename T, int W, int NW, int NB>
 __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
                                                             const int *__restrict__ done) {
   pdl_launch();
+  // An iteration queued after convergence exits before its prologue.  (The flag only
+  // goes 0 -> 1 within a cycle, so reading it before griddepcontrol.wait is safe: a
+  // stale 0 falls through to the check after the wait.)
+  if (done && *(volatile const int *)done) return;
   if (blockIdx.y) {                                                // right-hand side column blockIdx.y (NEXT-4)
     x += (size_t)blockIdx.y * P.ldx;
     tmp += (size_t)blockIdx.y * P.ldx;

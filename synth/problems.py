@@ -133,6 +133,14 @@ def helmholtz_shifted(dims, omega2h2=0.1, damping=0.5, name=None):
                     name=name or f"helmholtz{nd}d_{'x'.join(map(str, dims))}")
 
 
+def laplacian_shifted(dims, sigma, name=None):
+    """The 7-pt / 5-pt Laplacian with diagonal 2d - sigma: indefinite for sigma above its
+    smallest eigenvalue (a real analogue of the Helmholtz operator; test input only)."""
+    nd = len(dims)
+    return _stencil(dims, 2.0 * nd - sigma, [-1.0] * nd, [-1.0] * nd,
+                    name=name or f"laplacian_shift{sigma}_{'x'.join(map(str, dims))}")
+
+
 def rhs_vector(n, is_complex, seed=0):
     """Q20: numpy.random.default_rng(seed); real uniform(-1,1); complex re then im."""
     rng = np.random.default_rng(seed)

@@ -319,20 +319,92 @@ def test_zero_rhs_and_maxit(tmp_path):
     assert len(out["hist"]) == 8
 
 
+def test_solve_twice_with_growing_maxit(tmp_path):
+    """The FGMRES iteration graphs are captured once per (restart, basis, history buffer):
+    a second solve with a larger maxit (a new history buffer) must re-capture them and
+    report the full history (stale graphs wrote past the old buffer)."""
+    prob, b, xt, prm = P.make_config("C5", dims=(24, 24, 20), subdomains=8, rank=4)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    bd = to_dev(s, b[st["perm"]])
+    first = s.solve(bd, rtol=1e-300, restart=10, maxit=5)
+    assert first["its"] == 5 and len(first["hist"]) == 6
+    for maxit in (37, 80):
+        out = s.solve(bd, rtol=1e-300, restart=10, maxit=maxit)
+        ref = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=10, maxit=maxit)
+        assert out["its"] == maxit and len(out["hist"]) == maxit + 1
+        h = np.asarray(ref["hist"])
+        keep = h > 1e-12                                      # above the rounding floor
+        assert np.allclose(out["hist"][keep], h[keep], rtol=1e-6, atol=0)
+        assert np.allclose(first["hist"], out["hist"][:6], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("rank", [47, 51])
+def test_rank_near_the_limit(tmp_path, rank):
+    """k_ewx with 6 / 8 accumulators per warp (k up to 52 after the conjugate-pair rule):
+    apply parity with the oracle; rank 52 is refused."""
+    prob, b, xt, prm = P.make_config("C5", dims=(28, 28, 24), subdomains=4, rank=rank, levels=2)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    ks = [x["k"] for x in s.stats()["stages"]]
+    assert ks[0] >= rank
+    for seed in (2, 3):
+        r = P.rhs_vector(prob.n, False, seed)
+        assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
+    with pytest.raises(gm.GemslrError):
+        gm.Solver(prob.rowptr, prob.colidx, prob.values, 2, 4, 52, coords=prob.coords, device=0)
+
+
+@pytest.mark.parametrize("cplx,restart", [(False, 50), (False, 100), (True, 64), (True, 100)])
+def test_gram_schmidt_every_column_count(tmp_path, cplx, restart):
+    """CGS2 (reading Q14) at 1..restart columns, i.e. every Gram-Schmidt kernel the solver
+    dispatches by column count: fp64 k_gs2<8..32> (<= 32), k_gs<4,6> / k_gs<2,6> /
+    k_gs2<48> (33-48), k_gs2h (49-64), k_gs<1,13> (65-100); complex k_gs2<8..32>,
+    k_gs<2,6> (33-48), k_gs2g<2,32> (49-64), k_gs2g<4,26> (65-104).  The problem is
+    indefinite (shifted Laplacian / weakly damped Helmholtz) so the residual stays well
+    above the rounding floor through the whole cycle and every column's Hessenberg
+    entries shape the history: histories equal the oracle's to 1e-7 relative over a full
+    cycle plus a restart, and the explicit residual at the end matches."""
+    if cplx:
+        prob = P.helmholtz_shifted((16, 16, 14), omega2h2=1.0, damping=0.01)
+    else:
+        prob = P.laplacian_shifted((20, 20, 20), 0.6)
+    prm = dict(levels=2, subdomains=8, rank=4, ilu="ilut")
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    b = P.rhs_vector(prob.n, cplx, 0)
+    maxit = restart + 10
+    out = s.solve(to_dev(s, b[st["perm"]]), rtol=1e-300, restart=restart, maxit=maxit)
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=restart, maxit=maxit)
+    assert out["its"] == ref["its"] == maxit
+    h = np.asarray(ref["hist"])
+    assert h[restart] > 1e-6, "the problem converged too fast to exercise the late columns"
+    assert np.allclose(out["hist"], h, rtol=1e-7, atol=0), np.abs(out["hist"] / h - 1).max()
+    xg = np.empty(prob.n, dtype=b.dtype)
+    xg[st["perm"]] = out["x"].cpu().numpy()
+    assert rel(xg, ref["x"]) <= 1e-7
+    assert out["final_relres"] == pytest.approx(ref["final_relres"], rel=1e-7)
+
+
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["C2", "C5"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
 def test_full_size_parity(tmp_path, name):
-    """BASELINE sizes (64^3 / 128^3), the configuration bench.py times: full-vector
-    SpMV and apply parity, and the first FGMRES iterations' residual estimates."""
+    """BASELINE sizes (64^3 / 128^3; C5 is the configuration bench.py times): full-vector
+    SpMV and apply parity, then the whole FGMRES solve on both sides — iterations within
+    ±1 of the oracle and the true residual <= rtol (the north_star gate)."""
     prob, b, xt, prm = P.make_config(name)
     s, B, st, Pc = make_pair(prob, prm, tmp_path)
     perm = st["perm"]
-    x = P.rhs_vector(prob.n, False, 13)
+    x = P.rhs_vector(prob.n, prob.is_complex, 13)
     y = s.spmv(to_dev(s, x[perm])).cpu().numpy()
     yo = oracle.spmv(prob, x)[perm]
     assert rel(y, yo) <= TOL
     yg = s.apply_precond(to_dev(s, x)).cpu().numpy()
     assert rel(yg, Pc.apply(x)) <= TOL
-    out = s.solve(to_dev(s, b[perm]), rtol=1e-300, restart=prm["restart"], maxit=8)
-    ref = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=8)
-    assert np.allclose(out["hist"], ref["hist"], rtol=1e-7, atol=0)
+    out = s.solve(to_dev(s, b[perm]), rtol=prm["rtol"], restart=prm["restart"], maxit=1000)
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"], maxit=1000)
+    assert out["status"] == 0 and ref["status"] == 0
+    assert abs(out["its"] - ref["its"]) <= 1, (out["its"], ref["its"])
+    xg = np.empty(prob.n, dtype=b.dtype)
+    xg[perm] = out["x"].cpu().numpy()
+    true_rel = np.linalg.norm(b - oracle.spmv(prob, xg)) / np.linalg.norm(b)
+    assert true_rel <= prm["rtol"], true_rel
+    h = min(len(out["hist"]), len(ref["hist"]))
+    assert np.allclose(out["hist"][:h], ref["hist"][:h], rtol=1e-6, atol=1e2 * prm["rtol"])

@@ -468,3 +468,24 @@ def test_fgmres_with_gemslr_oracle_converges_and_rank_helps():
         assert np.linalg.norm(A @ out["x"] - b) <= 1e-8 * np.linalg.norm(b)
         its.append(out["its"])
     assert its[1] <= its[0]                # S:L490 soft check
+
+
+def test_oracle_results_do_not_depend_on_thread_count():
+    """the OpenMP oracle sums in fixed chunks, so 1 and 4 threads give
+    bit-identical applies and FGMRES histories (vectors longer than one chunk)."""
+    prob = P.laplacian((24, 24, 24))
+    A = prob.scipy()
+    st = D.tiny_structure(A, prob.coords, 2, 8, nlast=4)
+    b = P.rhs_vector(prob.n, False, 3)
+    res = []
+    nt0 = oracle.get_threads()
+    try:
+        for nt in (1, 4):
+            oracle.set_threads(nt)
+            Pc = oracle.Precond(A, st, ilu=(oracle.ILUT, 1e-3, 10))
+            out = oracle.fgmres(prob, b, M=Pc, rtol=1e-10, restart=20)
+            res.append((Pc.apply(b), out["x"], out["hist"]))
+    finally:
+        oracle.set_threads(nt0)
+    for a, c in zip(res[0], res[1]):
+        assert np.array_equal(a, c)
