@@ -101,7 +101,10 @@ gemslr_status gemslr_create(gemslr_ctx **out, int cuda_device, void *nccl_comm, 
  * and C_last rows to the rank owning most of their earlier-level neighbours;
  * exterior values move by grouped ncclSend/ncclRecv, W^H products, Gram-Schmidt
  * dots and the last separator by ncclAllReduce; the last-separator solve is
- * replicated. */
+ * replicated.  nranks = 1 with a non-NULL nccl_id builds a one-rank
+ * NCCL communicator and runs the DISTRIBUTED code path on one GPU (every
+ * all-reduce an NCCL call, no halo peers): a check of the NCCL plumbing and of the
+ * distributed kernels without a second GPU. */
 gemslr_status gemslr_nccl_unique_id(const char *nccl_lib, void *id128);
 gemslr_status gemslr_create_dist(gemslr_ctx **out, int cuda_device, void *cuda_stream, int nranks, int rank,
                                  const void *nccl_id, const char *nccl_lib);
@@ -201,8 +204,12 @@ gemslr_status gemslr_to_natural(gemslr_ctx *ctx, const void *x_local_dev, void *
 
 /* Write the setup bundle (manifest.json + raw little-endian .bin arrays) to
  * directory `dir` (created if missing): permutation, level / block offsets,
- * every ILU factor (block-local CSR), W_l (s_l x k_l column-major), R_l, G_l.
- * This is what tests/ hand to the independent oracle verifier. */
+ * every ILU factor (block-local CSR), W_l (s_l x k_l column-major, rows in the
+ * global permuted order of J_l), R_l, G_l.  This is what tests/ hand to the
+ * independent oracle verifier.  Collective with several ranks: the rows of W_l are
+ * gathered (one all-reduce per level), rank 0 writes the bundle, and
+ * the factors are omitted (each rank holds only its own blocks; the oracle
+ * recomputes all of them from its own A). */
 gemslr_status gemslr_export_setup(const gemslr_ctx *ctx, const char *dir);
 
 /* JSON statistics: levels achieved, level offsets, block counts, nnz of the

@@ -156,7 +156,10 @@ class Solver:
         torch.distributed world (one process per GPU; the NCCL id is broadcast
         with torch.distributed).  device = -1 with explicit nranks/my_rank builds
         the host-only plan of that rank (no GPU, no NCCL).  comm = "host" uses the
-        host-staged backend over torch.distributed (gloo) instead of NCCL."""
+        host-staged backend over torch.distributed (gloo) instead of NCCL.
+        comm = "nccl1" on one GPU runs the distributed code path over a one-rank NCCL
+        communicator (every all-reduce is an NCCL call; tests and the bench's
+        distributed-path line)."""
         L = lib()
         self.rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
         self.colidx = np.ascontiguousarray(colidx, dtype=np.int32)
@@ -174,7 +177,13 @@ class Solver:
                 nranks, my_rank = dist.get_world_size(), dist.get_rank()
         self.nranks = nranks or 1
         self.my_rank = my_rank or 0
-        if self.nranks == 1:
+        if self.nranks == 1 and comm == "nccl1" and device >= 0:
+            libp = nccl_lib_path()
+            idb = C.create_string_buffer(128)
+            self._check(L.gemslr_nccl_unique_id(libp.encode() if libp else None, idb), "nccl_unique_id")
+            self._check(L.gemslr_create_dist(C.byref(self.h), int(device), C.c_void_p(stream or 0), 1, 0, idb,
+                                             libp.encode() if libp else None), "create_dist")
+        elif self.nranks == 1:
             self._check(L.gemslr_create(C.byref(self.h), int(device), None, C.c_void_p(stream or 0)), "create")
         elif comm == "host" and device >= 0:
             self._cbs = _torch_host_callbacks()

@@ -175,6 +175,7 @@ struct Comm {
   void *comm = nullptr;
   bool owned = false;
   int nranks = 1, rank = 0;
+  bool force = false;          // one-rank NCCL communicator driving the distributed path (tests, bench)
   typedef int (*fn_uid)(void *);
   typedef int (*fn_init)(void **, int, const void *, int);   // id passed by value: see init()
   typedef int (*fn_destroy)(void *);
@@ -258,7 +259,7 @@ struct Comm {
   bool hostmode() const { return h_allreduce != nullptr; }
   // sum over ranks in place; count in doubles (complex = 2 doubles each)
   void allreduce(void *buf, size_t ndouble, cudaStream_t s) {
-    if (nranks == 1 || ndouble == 0) return;
+    if ((nranks == 1 && !force) || ndouble == 0) return;
     if (hostmode()) {
       double *h = host(ndouble);
       if (cudaMemcpyAsync(h, buf, ndouble * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
@@ -360,6 +361,7 @@ struct Engine {
   std::vector<LevelDev<D>> lev;
   StageDev<D> last;
   const int64_t *perm_d = nullptr;   // natural (original) row of every local row
+  bool dist = false;                 // distributed path: several ranks, or a forced one-rank NCCL communicator
   HaloDev<D> hA;
   std::vector<HaloDev<D>> hE, hF;
   D *rl_full = nullptr, *yl_full = nullptr;   // replicated last separator (nranks > 1)
@@ -642,7 +644,7 @@ void Engine<T>::upload(cudaStream_t s) {
         d.st.frow = P.upload<int>(frow, s);
         d.st.nf = (int64_t)fpos.size();
       }
-      if (plan.nranks == 1 && d.st.xU && d.st.nf >= 0) {        // the UP then reads z1 from xU (k_pack_f path)
+      if (!dist && d.st.xU && d.st.nf >= 0) {        // the UP then reads z1 from xU (k_pack_f path)
         const auto &Eh = plan.E[l];
         std::vector<int32_t> upos(S.reg.lpos.size(), -1);
         for (size_t q = 0; q < S.Up.slice_row.size(); ++q) {
@@ -664,7 +666,7 @@ void Engine<T>::upload(cudaStream_t s) {
   }
   hA = upload_halo<D>(P, s, plan.hA);
   last = upload_stage<D>(P, s, plan.last_stage, ctx->params.cluster_ctas, ctx->params.tri_kernel);
-  if (plan.nranks == 1) {                                          // packed next-stage right-hand sides from k_ewx
+  if (!dist) {                                                     // packed next-stage right-hand sides from k_ewx
     for (int l = 0; l < L; ++l) {
       LevelDev<D> &d = lev[l];
       const Stage<T> &NS = (l + 1 < L) ? plan.stage[l + 1] : plan.last_stage;
@@ -686,7 +688,7 @@ void Engine<T>::upload(cudaStream_t s) {
       CK(cudaMemsetAsync(const_cast<D *>(nd.Rg.rhsL), 0, std::max<int64_t>(nd.lslices * 32, 1) * sizeof(D), s));
     }
   }
-  if (plan.nranks > 1) {
+  if (dist) {
     rl_full = P.get<D>(plan.slast + 1);
     yl_full = P.get<D>(plan.slast + 1);
     last_idx_d = P.upload<int>(plan.last_idx, s);
@@ -1012,7 +1014,6 @@ template <typename T>
 void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
   const int L = (int)lev.size();
   cudaStream_t s = ctx->stream;
-  const bool dist = plan.nranks > 1;
   if (l0 == 0 && root_its > 0 && L > 0 && !dist) {                // Alg. 2 with GMRES at the root (NEXT-1)
     LevelDev<D> &d = lev[0];
     launch_trisolve(ctx, d.st, TRI_DOWN, in, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, 0);   // z1
@@ -1108,7 +1109,7 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
 // SpMV reads A once for all columns; the E/W coupling runs per column.
 template <typename T>
 bool Engine<T>::multi_ok() const {
-  if (plan.nranks != 1) return false;
+  if (dist) return false;
   for (const auto &d : lev)
     if (!(d.st.nblk == 0 || d.st.rows == 0 || (d.st.reg && d.st.nf >= 0))) return false;
   return last.nblk == 0 || last.rows == 0 || last.reg;
@@ -1665,8 +1666,11 @@ void Engine<T>::ensure_krylov(int m, int maxit) {
     kry_m = m;
   }
   if (hist_cap < maxit + 1) {
-    hist = P.get<double>(maxit + 2);
-    hist_cap = maxit + 1;
+    // the captured iteration graphs hold this pointer (graph_hist): allocate with
+    // room to spare so a later solve with a larger maxit rarely forces a re-capture
+    const int cap = std::max(maxit + 1, std::max(4095, 2 * hist_cap));
+    hist = P.get<double>(cap + 1);
+    hist_cap = cap;
   }
 }
 
@@ -1742,7 +1746,9 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
       }
     };
     static const bool no_graph = getenv("GEMSLR_NO_GRAPH") != nullptr;
-    const bool use_graph = !no_graph && plan.nranks == 1 && !ctx->prof.on;
+    // graphs on one GPU and over NCCL (its calls are captured with the kernels); the
+    // host-staged backend synchronises inside its collectives and cannot be captured
+    const bool use_graph = !no_graph && !ctx->comm.hostmode() && !ctx->prof.on;
     if (use_graph && (graph_m != m || graph_V != V || graph_hist != hist)) {
       for (auto &ge : graphs) if (ge) cudaGraphExecDestroy(ge);
       graphs.assign(m, nullptr);
@@ -1862,8 +1868,38 @@ static void write_bin(const std::string &path, const void *p, size_t bytes) {
   std::fclose(f);
 }
 
+// Collective on every rank (several ranks: the W_l rows of all ranks are summed
+// into the global J_l order by one all-reduce per level; rank 0 writes the bundle).
+// The structure and R_l, G_l are replicated; the ILU factors are written by a
+// single-rank context only (each rank holds its own blocks; the oracle recomputes
+// every factor from its own A anyway, c3).
 template <typename T>
 void Engine<T>::export_bundle(const std::string &dir) const {
+  using S = typename std::conditional<std::is_same<T, double>::value, double, zc>::type;
+  const bool dist = plan.nranks > 1;
+  std::vector<std::vector<S>> Wg(lev.size());
+  for (int l = 0; l < (int)lev.size(); ++l) {
+    const auto &d = lev[l];
+    if (d.k == 0) continue;
+    if (!dist) { Wg[l] = d.Wh; continue; }
+    const int64_t og = plan.st.o[l + 1], sg = nglob - og;
+    std::vector<S> full((size_t)sg * d.k, S(0));
+    for (int c = 0; c < d.k; ++c)
+      for (int64_t i = 0; i < d.s; ++i) full[(size_t)c * sg + (plan.gpos[d.o1 + i] - og)] = d.Wh[(size_t)c * d.s + i];
+    D *buf = static_cast<D *>(ctx->alloc.alloc(std::max<size_t>(full.size(), 1) * sizeof(D)));
+    try {
+      CK(cudaMemcpyAsync(buf, full.data(), full.size() * sizeof(D), cudaMemcpyHostToDevice, ctx->stream));
+      const_cast<Engine<T> *>(this)->allreduce(buf, full.size());
+      CK(cudaMemcpyAsync(full.data(), buf, full.size() * sizeof(D), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      ctx->alloc.release(buf);
+      throw;
+    }
+    ctx->alloc.release(buf);
+    Wg[l].swap(full);
+  }
+  if (plan.rank != 0) return;
   mkdir(dir.c_str(), 0755);
   std::string man = "{\n";
   const char *vt = std::is_same<T, double>::value ? "float64" : "complex128";
@@ -1898,14 +1934,16 @@ void Engine<T>::export_bundle(const std::string &dir) const {
       add(b + "_nnzoff", "int64", nnzoff.data(), nnzoff.size(), 8, {(int64_t)nnzoff.size()});
     }
   };
-  for (int l = 0; l < st.L; ++l) facs("fac" + std::to_string(l), plan.fac[l]);
-  facs("faclast", plan.lastfac);
+  if (!dist) {
+    for (int l = 0; l < st.L; ++l) facs("fac" + std::to_string(l), plan.fac[l]);
+    facs("faclast", plan.lastfac);
+  }
   std::string ranks = "[";
   for (int l = 0; l < (int)lev.size(); ++l) {
     const auto &d = lev[l];
     ranks += (l ? ", " : "") + std::to_string(d.k);
     if (d.k > 0) {
-      add("W_" + std::to_string(l), vt, d.Wh.data(), d.Wh.size(), sizeof(T), {(int64_t)d.k, d.s});
+      add("W_" + std::to_string(l), vt, Wg[l].data(), Wg[l].size(), sizeof(T), {(int64_t)d.k, nglob - st.o[l + 1]});
       add("R_" + std::to_string(l), vt, d.Rh.data(), d.Rh.size(), sizeof(T), {(int64_t)d.k, (int64_t)d.k});
       add("G_" + std::to_string(l), vt, d.Gh.data(), d.Gh.size(), sizeof(T), {(int64_t)d.k, (int64_t)d.k});
     }
@@ -1914,7 +1952,8 @@ void Engine<T>::export_bundle(const std::string &dir) const {
   const gemslr_params &p = ctx->params;
   man += "  \"meta\": {\"n\": " + std::to_string(n) + ", \"levels\": " + std::to_string(st.L) + ", \"dtype\": \"" + vt +
          "\", \"ilu\": " + std::to_string(p.ilu) + ", \"ilut_drop\": " + std::to_string(p.ilut_drop) +
-         ", \"ilut_fill\": " + std::to_string(p.ilut_fill) + ", \"ranks\": " + ranks + "}\n}\n";
+         ", \"ilut_fill\": " + std::to_string(p.ilut_fill) + ", \"ranks\": " + ranks +
+         ", \"nranks\": " + std::to_string(plan.nranks) + "}\n}\n";
   write_bin(dir + "/manifest.json", man.data(), man.size());
 }
 
@@ -2063,10 +2102,11 @@ gemslr_status gemslr_create_dist(gemslr_ctx **out, int cuda_device, void *cuda_s
   if (st) return st;
   c->comm.nranks = nranks;
   c->comm.rank = rank;
-  if (!c->host_only && nranks > 1) {
+  if (!c->host_only && (nranks > 1 || nccl_id)) {
     if (!nccl_id) { delete c; return GEMSLR_ERR_INVALID_ARG; }
     try {
       c->comm.init(nccl_lib, nranks, rank, nccl_id);
+      c->comm.force = nranks == 1;                                 // one rank: the distributed path over NCCL
     } catch (const Error &e) {
       delete c;
       return (gemslr_status)e.code;
@@ -2141,6 +2181,7 @@ static gemslr_status do_setup(gemslr_ctx *c, std::unique_ptr<Engine<T>> &E, int6
   auto t1 = std::chrono::steady_clock::now();
   E->setup_host_s = std::chrono::duration<double>(t1 - t0).count();
   E->n = n;
+  E->dist = E->plan.nranks > 1 || c->comm.force;
   if (c->host_only) return GEMSLR_OK;
   E->upload(c->stream);
   CK(cudaStreamSynchronize(c->stream));
@@ -2166,7 +2207,7 @@ gemslr_status gemslr_setup(gemslr_ctx *c, gemslr_dtype dtype, int64_t n, const i
     return fail(c, GEMSLR_ERR_INVALID_ARG, "levels < 1, subdomains < 1, rank < 0 or bad dtype/ilu");
   if (2 * prm->rank + 2 > GS_MAXC) return fail(c, GEMSLR_ERR_INVALID_ARG, "rank > 51 not supported (Arnoldi cycle 2k + 1 <= 103 columns)");
   if (prm->root_inner_its < 0 || prm->root_inner_its + 2 > GS_MAXC ||
-      (prm->root_inner_its > 0 && c->comm.nranks > 1))
+      (prm->root_inner_its > 0 && (c->comm.nranks > 1 || c->comm.force)))
     return fail(c, GEMSLR_ERR_INVALID_ARG, "root_inner_its < 0, too large, or with several ranks (one GPU only)");
   if (prm->ilu_shift != 0.0 && (dtype != GEMSLR_C128 || !(prm->ilu_shift == prm->ilu_shift)))
     return fail(c, GEMSLR_ERR_INVALID_ARG, "ilu_shift needs complex arithmetic (GEMSLR_C128)");
@@ -2366,7 +2407,6 @@ gemslr_status gemslr_to_natural(gemslr_ctx *c, const void *xl, void *xn) { retur
 gemslr_status gemslr_export_setup(const gemslr_ctx *c, const char *dir) {
   if (!c || !dir) return GEMSLR_ERR_INVALID_ARG;
   if (!c->ready) return fail(c, GEMSLR_ERR_STATE, "export before setup");
-  if (c->comm.nranks > 1) return fail(c, GEMSLR_ERR_STATE, "export_setup is single-rank only");
   return guarded(const_cast<gemslr_ctx *>(c), [&]() -> gemslr_status {
     if (c->dtype == GEMSLR_F64) c->ed->export_bundle(dir); else c->ez->export_bundle(dir);
     return GEMSLR_OK;
