@@ -76,6 +76,12 @@ typedef struct {
   double ilu_shift;         /* complex diagonal shift of the block ILUs: sigma = i*ilu_shift*sum|a_ii|/n added
                                to every B_l and C_last block before factoring (the paper uses
                                0.05); 0 = off; GEMSLR_C128 only (INVALID_ARG for GEMSLR_F64)               */
+  int tri_split;            /* CTAs (one thread-block cluster) per subdomain block in the register-prefetched
+                               triangular solves: the block's rows cut into that many contiguous chunks on as
+                               many SMs, values crossing chunks moved through distributed shared memory; 0 =
+                               automatic (the deep level-0 blocks: 4 or 2 when blocks x Q fit the SMs), 1 = off,
+                               2 or 4 = forced on every level stage.  The solves compute the same Alg. 2
+                               substitutions in the same order inside every row.          */
 } gemslr_params;
 
 typedef struct gemslr_ctx gemslr_ctx;

@@ -45,7 +45,7 @@ class Params(C.Structure):
                 ("ilut_drop", C.c_double), ("ilut_fill", C.c_int), ("last_blocks", C.c_int),
                 ("arnoldi_tol", C.c_double), ("arnoldi_max_cycles", C.c_int), ("seed", C.c_ulonglong),
                 ("cluster_ctas", C.c_int), ("tri_kernel", C.c_int), ("root_inner_its", C.c_int),
-                ("ilu_shift", C.c_double)]
+                ("ilu_shift", C.c_double), ("tri_split", C.c_int)]
 
 
 def lib():
@@ -151,7 +151,8 @@ class Solver:
 
     def __init__(self, rowptr, colidx, values, levels, subdomains, rank, ilu="ilut", ilut_drop=1e-3,
                  ilut_fill=10, last_blocks=0, coords=None, device=0, stream=None, seed=0, arnoldi_tol=1e-2,
-                 arnoldi_max_cycles=10, cluster_ctas=0, tri_kernel=0, ilu_shift=0.0, root_inner_its=0, nranks=None, my_rank=None, comm="nccl"):
+                 arnoldi_max_cycles=10, cluster_ctas=0, tri_kernel=0, ilu_shift=0.0, root_inner_its=0, nranks=None, my_rank=None, comm="nccl",
+                 tri_split=0):
         """nranks/my_rank: None = single GPU, or taken from an initialised
         torch.distributed world (one process per GPU; the NCCL id is broadcast
         with torch.distributed).  device = -1 with explicit nranks/my_rank builds
@@ -208,7 +209,7 @@ class Solver:
             self._check(L.gemslr_set_coordinates(self.h, self.coords.shape[1], _ptr(self.coords)), "coordinates")
         p = Params(levels, subdomains, rank, 0 if ilu == "ilu0" else 1, ilut_drop, ilut_fill, last_blocks,
                    arnoldi_tol, arnoldi_max_cycles, seed, cluster_ctas, tri_kernel, root_inner_its,
-                   ilu_shift)
+                   ilu_shift, tri_split)
         self.params = p
         self._check(L.gemslr_setup(self.h, 1 if self.is_complex else 0, self.n, _ptr(self.rowptr), _ptr(self.colidx),
                                    _ptr(self.values), C.byref(p)), "setup")

@@ -19,6 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # GEMSLR_TRACE=1: compile the clock64 trace of k_tri_reg in (tools/trace_reg.py)
 TRACE = ["-DGEMSLR_TRACE"] if os.environ.get("GEMSLR_TRACE") == "1" else []
+# experiments: GEMSLR_NVCC_DEFS="-DNAME=VALUE ..." extra defines (e.g. SPLIT_BACKOFF_NS)
+TRACE += os.environ.get("GEMSLR_NVCC_DEFS", "").split()
 
 CPP = ["partition.cpp", "ilu.cpp", "schedule.cpp", "hostplan.cpp", "schur.cpp"]
 CU = ["context.cu"]

@@ -291,6 +291,7 @@ struct StageDev {
   bool reg = false;        // register-prefetched kernel (k_tri_reg), preferred when available
   int reg_w = 0;           // record width W (4, 8, 10, 12 or 16)
   int reg_nw = 0;          // consumer warps of k_tri_reg (reg_nw_for)
+  int reg_q = 1;           // split form: CTAs (a cluster) per block
   RegDev<D> Rg{};
   int64_t reg_bytes = 0;   // record bytes of both sweeps
   const int *lrow = nullptr;       // per packed L position: the row (-1 padding), DOWN gather
@@ -465,7 +466,8 @@ static int reg_nw_for(const RegPack<T> &R) {
   const double K = lv > 0 ? (double)sl / (double)lv : 1.0;
   if (sizeof(D) == 8) {
     if (env == 15 || env == 23) return env;
-    return K >= 3.0 ? 23 : 15;
+    // split chunks (C5 level 0 at Q = 4: K = 2.8): 23 warps measured 4 % faster than 15
+    return K >= (R.Q > 1 ? 2.5 : 3.0) ? 23 : 15;
   }
   if (env == 7 || env == 15) return env;
   return 15;                                                       // complex: 15 warps, one buffer (C4: every level)
@@ -510,7 +512,8 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     d.nearc = S.pipe.near;
   }
   if (S.reg.ok && cps_override <= 0 && tri_kernel == 0 && d.nblk > 0 &&
-      reg_smem_bytes<D>(S.reg.ring, S.reg.max_block_slices) <= 232448 - 1024) {
+      reg_smem_bytes<D>(S.reg.ring, S.reg.max_block_slices, S.reg.imp_L + S.reg.imp_U, S.reg.plev_L + S.reg.plev_U,
+                        S.reg.Q > 1) <= 232448 - 1024) {
     static_assert(REG_BINFO == REG_BINFO_INTS, "binfo layout");
     d.reg = true;
     d.reg_w = S.reg.W;
@@ -531,9 +534,19 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     d.urow = P.upload<int>(S.Up.slice_row, s);
     d.xU = P.get<D>(std::max<int64_t>(S.reg.uslices * 32, 1));
     d.Rg.ring = S.reg.ring;
+    d.reg_q = S.reg.Q;
+    d.Rg.Q = S.reg.Q;
+    d.Rg.imp_L = S.reg.imp_L;
+    d.Rg.imp_U = S.reg.imp_U;
+    d.Rg.plev_L = S.reg.plev_L;
+    d.Rg.plev_U = S.reg.plev_U;
+    d.Rg.sneed = S.reg.Q > 1 ? P.upload<unsigned short>(S.reg.sneed, s) : nullptr;
+    d.Rg.xexp = S.reg.Q > 1 ? P.upload<unsigned short>(S.reg.xexp, s) : nullptr;
     d.reg_bytes = (int64_t)S.reg.data.size();
     if (!d.pipe) d.P.lpos = P.upload<int>(S.reg.lpos, s);
   }
+  if (S.reg.Q > 1 && !d.reg)                                       // chunks are not independent blocks
+    throw Error{GEMSLR_ERR_INVALID_ARG, "split triangular solves need the register-prefetched kernel"};
   d.nnz = S.Lp.nnz_real + S.Up.nnz_real + (int64_t)d.rows;
   d.padded = (int64_t)S.Lp.val.size() + (int64_t)S.Up.val.size() + (int64_t)S.Up.diag.size();
   // CTAs per block: enough to cover the average rows of one level with 8-warp CTAs,
@@ -775,6 +788,29 @@ static void launch_pdl(void (*kern)(KA...), dim3 grid, dim3 block, size_t smem, 
   CK(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
 }
 
+// The same with a thread-block cluster of `csize` CTAs along x (the split form of
+// k_tri_reg: one cluster per subdomain block).
+template <typename... KA, typename... A>
+static void launch_pdl_cluster(void (*kern)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int csize,
+                               A &&...args) {
+  static const bool on = getenv("GEMSLR_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 2 : 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
+}
+
 static int grid_for(int64_t units, int per_sm) {
   int64_t g = std::min<int64_t>(units, (int64_t)num_sm() * per_sm);
   return (int)std::max<int64_t>(g, 1);
@@ -813,6 +849,15 @@ static void launch_ewx(cudaStream_t st, int64_t s, int64_t rowbase, const int64_
                        const D *Eval, const D *z, const D *zh, int64_t nloc, const D *src, D *dst, const D *W,
                        int64_t ldw, int k, const D *G, D *partial, unsigned *ticket, D *sout, int *flag,
                        const int *done, int64_t npk, const int *pkpos, D *pk) {
+  static const int small_max = getenv("GEMSLR_EWC_MAX") ? atoi(getenv("GEMSLR_EWC_MAX")) : 16384;
+  if (s <= small_max) {                                            // small interface: one cluster (k_ewc)
+    const int C = (int)std::max<int64_t>(1, std::min<int64_t>(8, (s + 255) / 256));
+    with_nacc(k, [&](auto nc) {
+      launch_pdl_cluster(k_ewc<D, decltype(nc)::value>, dim3(C), dim3(256), 0, st, C, s, rowbase, Eptr, Ecol, Eval, z, zh,
+                         nloc, src, dst, W, ldw, k, G, done, npk, pkpos, pk);
+    });
+    return;
+  }
   with_nacc(k, [&](auto nc) {
     auto kern = k_ewx<D, decltype(nc)::value>;
     static int max_ctas[64] = {0};                                  // per device
@@ -857,7 +902,8 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
   const D *Fv = F ? F->val : nullptr;
   const int pgrid = grid_for((S.rows + 255) / 256, 4);
   if (S.reg) {
-    const size_t smem = reg_smem_bytes<D>(S.Rg.ring, S.Rg.max_slices);
+    const size_t smem = reg_smem_bytes<D>(S.Rg.ring, S.Rg.max_slices, S.Rg.imp_L + S.Rg.imp_U,
+                                          S.Rg.plev_L + S.Rg.plev_U, S.reg_q > 1);
     RegDev<D> Rg = S.Rg;
     Rg.ldx = Rg.rsL = Rg.rsU = 0;
     D *rL = const_cast<D *>(S.Rg.rhsL), *rUp = S.rhs_up;
@@ -906,10 +952,22 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
       static std::set<const void *> attr;                          // once per instance
       if (attr.insert((const void *)kern).second)
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024));   // room for the static block info
-      launch_pdl(kern, dim3(S.nblk, nr), dim3(32 * nw), smem, ctx->stream, Rg, mode, x, tmp, doneflag);
+      if (S.reg_q > 1) launch_pdl_cluster(kern, dim3(S.nblk * S.reg_q, nr), dim3(32 * (nw + 1)), smem, ctx->stream, S.reg_q,
+                                          Rg, mode, x, tmp, doneflag);      // + the import warp
+      else launch_pdl(kern, dim3(S.nblk, nr), dim3(32 * nw), smem, ctx->stream, Rg, mode, x, tmp, doneflag);
     };
     auto by_w = [&](auto nwc, auto nbc) {
       constexpr int NW = decltype(nwc)::value, NB = decltype(nbc)::value;
+      if (S.reg_q > 1) {                                           // split form: a cluster per block
+        switch (S.reg_w) {
+          case 4: go(k_tri_reg<D, 4, NW, NB, true>, NW); break;
+          case 8: go(k_tri_reg<D, 8, NW, NB, true>, NW); break;
+          case 10: go(k_tri_reg<D, 10, NW, NB, true>, NW); break;
+          case 12: go(k_tri_reg<D, 12, NW, NB, true>, NW); break;
+          default: go(k_tri_reg<D, 16, NW, NB, true>, NW); break;
+        }
+        return;
+      }
       switch (S.reg_w) {
         case 4: go(k_tri_reg<D, 4, NW, NB>, NW); break;
         case 8: go(k_tri_reg<D, 8, NW, NB>, NW); break;
@@ -1976,6 +2034,7 @@ std::string Engine<T>::stats_json() const {
            ", \"pipe\": " + (S.pipe ? "true" : "false") + ", \"chunks\": " + std::to_string(S.nchunks) +
            ", \"far\": " + std::to_string(S.far) + ", \"near\": " + std::to_string(S.nearc) +
            ", \"kernel\": \"" + (S.reg ? "reg" : S.pipe ? "pipe" : "level") + "\", \"reg_w\": " + std::to_string(S.reg_w) +
+           ", \"split\": " + std::to_string(S.reg ? S.reg_q : 1) + ", \"reg_nw\": " + std::to_string(S.reg_nw) +
            ", \"reg_bytes\": " + std::to_string(S.reg_bytes) + "}";
   };
   j += ", \"stages\": [";
@@ -1986,6 +2045,17 @@ std::string Engine<T>::stats_json() const {
          ", \"nnzF\": " + std::to_string(d.F.nnz) + "}";
   }
   j += "], \"last\": " + stage(last);
+  j += ", \"packs\": [";                                          // host packing of every level stage
+  for (size_t l = 0; l < plan.stage.size(); ++l) {
+    const auto &R = plan.stage[l].reg;
+    j += (l ? ", " : "") + std::string("{\"ok\": ") + (R.ok ? "true" : "false") + ", \"Q\": " + std::to_string(R.Q) +
+         ", \"ring\": " + std::to_string(R.ring) + ", \"W\": " + std::to_string(R.W) + ", \"imp_L\": " +
+         std::to_string(R.imp_L) + ", \"imp_U\": " + std::to_string(R.imp_U) + ", \"plev_L\": " +
+         std::to_string(R.plev_L) + ", \"plev_U\": " + std::to_string(R.plev_U) + ", \"exports\": " +
+         std::to_string(R.exports) + ", \"records\": " + std::to_string(R.nrec) + ", \"max_levels\": " +
+         std::to_string(R.max_levels) + "}";
+  }
+  j += "]";
   j += ", \"setup_host_s\": " + std::to_string(setup_host_s) + ", \"setup_device_s\": " + std::to_string(setup_dev_s) +
        ", \"arnoldi_s\": " + std::to_string(arnoldi_s);
   j += ", \"device_bytes\": " + std::to_string(ctx->pool.bytes);
@@ -2167,6 +2237,11 @@ static gemslr_status do_setup(gemslr_ctx *c, std::unique_ptr<Engine<T>> &E, int6
   opt.shift = prm->ilu_shift;
   opt.nranks = c->comm.nranks;
   opt.rank = c->comm.rank;
+  // split form of the level-0 triangular solves (plan.hpp): only with the register
+  // kernel (tri_kernel 0, no cluster override); GEMSLR_SPLIT=1/2/4 forces it
+  opt.split = (prm->tri_kernel != 0 || prm->cluster_ctas > 0) ? 1 : prm->tri_split;
+  if (getenv("GEMSLR_SPLIT")) opt.split = atoi(getenv("GEMSLR_SPLIT"));
+  if (!c->host_only) opt.sms = num_sm();
   if (c->coord_dim > 0 && c->coords_src) {
     c->coords.assign(c->coords_src, c->coords_src + (size_t)n * c->coord_dim);
     opt.coord_dim = c->coord_dim;
@@ -2209,6 +2284,8 @@ gemslr_status gemslr_setup(gemslr_ctx *c, gemslr_dtype dtype, int64_t n, const i
   if (prm->root_inner_its < 0 || prm->root_inner_its + 2 > GS_MAXC ||
       (prm->root_inner_its > 0 && (c->comm.nranks > 1 || c->comm.force)))
     return fail(c, GEMSLR_ERR_INVALID_ARG, "root_inner_its < 0, too large, or with several ranks (one GPU only)");
+  if (prm->tri_split < 0 || prm->tri_split == 3 || prm->tri_split > 4)
+    return fail(c, GEMSLR_ERR_INVALID_ARG, "tri_split must be 0, 1, 2 or 4");
   if (prm->ilu_shift != 0.0 && (dtype != GEMSLR_C128 || !(prm->ilu_shift == prm->ilu_shift)))
     return fail(c, GEMSLR_ERR_INVALID_ARG, "ilu_shift needs complex arithmetic (GEMSLR_C128)");
   c->params = *prm;

@@ -4,7 +4,9 @@
 // (P:L458-464), factor every block in parallel and
 // build the level-scheduled sweeps.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "plan.hpp"
 
@@ -99,8 +101,32 @@ bool factor_blocks(const Csr<T> &Ahat, const std::vector<int64_t> &bl, const Set
 }
 
 // drop empty blocks for the device stage
+// Clusters per block of a stage's triangular solves (plan.hpp, split form): the
+// subdomains of level 0 are few (p / nranks) and deep, so each is cut into Q
+// chunks on Q SMs; stages with small blocks keep one CTA per block.
+static int split_for(const std::vector<int64_t> &bl, const SetupOptions &opt, bool is_complex) {
+  if (opt.split == 1) return 1;
+  int nb = 0;
+  int64_t rows = 0;
+  for (size_t q = 0; q + 1 < bl.size(); ++q)
+    if (bl[q + 1] > bl[q]) { nb++; rows += bl[q + 1] - bl[q]; }
+  if (nb == 0) return 1;
+  if (opt.split >= 2) return opt.split;
+  // complex (C4, 64 blocks: Q = 2): measured 278 / 290 us per level-0 sweep pair vs
+  // 268 / 284 unsplit (15 warps either way) — the split only pays in fp64
+  if (is_complex) return 1;
+  const int64_t avg = rows / nb;
+  static const int qmax = getenv("GEMSLR_SPLIT_MAX") ? atoi(getenv("GEMSLR_SPLIT_MAX")) : 4;   // experiments
+  for (int Q = 4; Q >= 2; Q /= 2) {
+    if (Q > qmax) continue;
+    const int fit = Q == 4 ? opt.sms - 16 : opt.sms;                // clusters of 4 leave a few SMs of each GPC idle
+    if ((int64_t)nb * Q <= fit && avg / Q >= 4096) return Q;
+  }
+  return 1;
+}
+
 template <typename T>
-void make_stage(const std::vector<int64_t> &bl, const std::vector<Factor<T>> &fac, Stage<T> &S) {
+void make_stage(const std::vector<int64_t> &bl, const std::vector<Factor<T>> &fac, Stage<T> &S, int Q = 1) {
   std::vector<int64_t> bounds;
   std::vector<Factor<T>> facs;
   for (size_t q = 0; q + 1 < bl.size(); ++q) {
@@ -110,7 +136,7 @@ void make_stage(const std::vector<int64_t> &bl, const std::vector<Factor<T>> &fa
     facs.push_back(fac[q]);
   }
   if (bounds.empty()) bounds.push_back(bl.empty() ? 0 : bl[0]);
-  pack_stage(bounds, facs, S);
+  pack_stage(bounds, facs, S, Q);
 }
 
 }  // namespace
@@ -315,7 +341,7 @@ bool build_host_plan(int64_t n, const int64_t *rowptr, const int32_t *colidx, co
     // local stage: owned blocks are contiguous in the local layout
     std::vector<int64_t> lb{plan.lo[l]};
     for (size_t t = 0; t < own_q.size(); ++t) lb.push_back(lb.back() + (bl[own_q[t] + 1] - bl[own_q[t]]));
-    make_stage(lb, own_fac, plan.stage[l]);
+    make_stage(lb, own_fac, plan.stage[l], split_for(lb, opt, !std::is_same<T, double>::value));
     plan.E[l] = local_rows(plan.lo[l + 1], nloc, st.o[l], st.o[l + 1], plan.hE[l], false);
     plan.F[l] = local_rows(plan.lo[l], plan.lo[l + 1], st.o[l + 1], n, plan.hF[l], G > 1);
   }

@@ -633,16 +633,47 @@ struct RegDev {
   // several right-hand sides (NEXT-4): column blockIdx.y works on x/tmp + col*ldx
   // and rhsL/mid + col*rs (0 for one column); the factor records are shared
   long long ldx, rsL, rsU;
+  // split form (plan.hpp RegPack, Q > 1): a Q-CTA cluster per block
+  int Q;
+  int imp_L, imp_U;            // import areas after the ring (entries)
+  int plev_L, plev_U;          // counter / expectation table sizes
+  const unsigned short *sneed; // per record: producer level needed + 1 (0 none)
+  const unsigned short *xexp;  // expected exporting slices per producer level
 };
 #ifdef GEMSLR_TRACE
 constexpr bool kRegTrace = true;         // clock64 trace of block 0 (tools/trace_reg.py; build with GEMSLR_TRACE=1)
 #else
 constexpr bool kRegTrace = false;
 #endif
-template <typename T> __host__ __device__ inline size_t reg_smem_bytes(int ring, int max_slices) {
-  return (size_t)ring * sizeof(T) + 16 + (((size_t)max_slices * 2 + 15) & ~(size_t)15);
+__host__ __device__ constexpr size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
+// [ring | imports] T, 16 bytes, [mbarriers u64 | expectations u16] (split), level
+// table u16, [need table u16] (split)
+template <typename T> __host__ __device__ inline size_t reg_smem_bytes(int ring, int max_slices, int imp = 0, int plev = 0,
+                                                                       bool split = false) {
+  return (size_t)(ring + imp) * sizeof(T) + 16 + (split ? al16((size_t)plev * 8) + al16((size_t)plev * 2) : 0) +
+         al16((size_t)max_slices * 2) * (split ? 2 : 1);
 }
-constexpr int REG_BINFO = 12;            // ints per block in RegDev::binfo (= REG_BINFO_INTS)
+constexpr int REG_BINFO = 16;            // ints per block in RegDev::binfo (= REG_BINFO_INTS)
+
+// DSMEM hand-off of the split form: every exported value is an asynchronous
+// remote store (st.async) that completes its bytes on the consumer's mbarrier of
+// the producer's level; the consumer set each barrier's expected bytes at start and
+// waits on it (local try_wait) only when a slice reads that level's values.  No
+// fence on either side: the producer never stalls on its stores.
+__device__ inline unsigned mapa_shared(unsigned addr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ inline void st_async_cluster(unsigned addr, double v, unsigned mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(addr), "d"(v), "r"(mbar)
+               : "memory");
+}
+__device__ inline void st_async_cluster(unsigned addr, cd v, unsigned mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "d"(v.x), "d"(v.y), "r"(mbar)
+               : "memory");
+}
 
 // Level v of a sweep ends at named barrier 1 + v % 15 (15 ids in rotation).
 // A warp that computes in level v + 1 SYNCS there (arrive + wait); every other
@@ -682,6 +713,7 @@ struct RegBuf {
   uint4 c[W8];
   T rhs, dg, xo;
   int out;
+  int exp;                                       // split: import index at the consumer (-1 none)
   __device__ T val(int e) const { return vec_get<T>(v[e / VE], e % VE); }
   __device__ unsigned slot(int e) const {
     const uint4 &q = c[e / 8];
@@ -691,14 +723,18 @@ struct RegBuf {
   }
 };
 
-template <typename T, int W, int NW, int NB>
-__global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
+#ifndef SPLIT_EXPORT_FIRST
+#define SPLIT_EXPORT_FIRST 0
+#endif
+template <typename T, int W, int NW, int NB, bool SPLIT = false>
+__global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
                                                             const int *__restrict__ done) {
   pdl_launch();
   // An iteration queued after convergence exits before its prologue.  (The flag only
   // goes 0 -> 1 within a cycle, so reading it before griddepcontrol.wait is safe: a
-  // stale 0 falls through to the check after the wait.)
-  if (done && *(volatile const int *)done) return;
+  // stale 0 falls through to the check after the wait.)  Not in the split form: the
+  // CTAs of a cluster must take the same decision (they meet at cluster barriers).
+  if (!SPLIT && done && *(volatile const int *)done) return;
   if (blockIdx.y) {                                                // right-hand side column blockIdx.y (NEXT-4)
     x += (size_t)blockIdx.y * P.ldx;
     tmp += (size_t)blockIdx.y * P.ldx;
@@ -707,8 +743,15 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
   }
   extern __shared__ __align__(128) unsigned char smem[];
   T *ring = reinterpret_cast<T *>(smem);
-  unsigned short *lvt = reinterpret_cast<unsigned short *>(smem + (size_t)P.ring * sizeof(T) + 16);
   const int R = P.ring;
+  const int IL = SPLIT ? P.imp_L : 0, PL = SPLIT ? P.plev_L : 0, PLU = SPLIT ? P.plev_L + P.plev_U : 0;
+  unsigned char *tail = smem + (size_t)(R + (SPLIT ? P.imp_L + P.imp_U : 0)) * sizeof(T) + 16;
+  // split: the import warp's progress, per sweep: producer levels whose values landed
+  volatile int *ready = reinterpret_cast<volatile int *>(tail - 16);
+  unsigned long long *mb = reinterpret_cast<unsigned long long *>(tail);       // split: one mbarrier per producer level
+  unsigned short *xex = reinterpret_cast<unsigned short *>(tail + al16((size_t)PLU * 8));
+  unsigned short *lvt = reinterpret_cast<unsigned short *>(SPLIT ? tail + al16((size_t)PLU * 8) + al16((size_t)PLU * 2) : tail);
+  unsigned short *ndt = lvt + al16((size_t)P.max_slices * 2) / 2;             // split: producer level needed + 1
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // The block's info goes through shared memory: a register loaded from global
   // memory shares a scoreboard slot with the prefetch loads issued later, and
@@ -730,11 +773,61 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
       for (int u = 0; u < U; ++u) lvt[i + u * nt] = v[u];
     }
     for (; i < nl; i += nt) lvt[i] = P.slev[f + i];
+    if constexpr (SPLIT) {
+      for (int j = tid; j < nl; j += nt) ndt[j] = P.sneed[f + j];
+      for (int j = tid; j < PLU; j += nt) {                        // producer level j: expected values
+        const int in_l = j < PL;
+        const int u = in_l ? j : j - PL;
+        const unsigned e = in_l ? (u < bi[13] ? P.xexp[bi[12] + u] : 0u) : (u < bi[15] ? P.xexp[bi[14] + u] : 0u);
+        xex[j] = (unsigned short)e;
+        mbar_init(&mb[j], 1);
+      }
+    }
   }
   for (int i = tid; i < R; i += blockDim.x) ring[i] = dzero<T>();
   __syncthreads();
+  // split: the neighbours' import areas and barriers (L exports go to q + 1, U to q - 1)
+  unsigned rimp[2] = {0, 0}, rmb[2] = {0, 0};
+  if constexpr (SPLIT) {
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    for (int j = tid; j < PLU; j += blockDim.x) {                 // arm: the phase completes when the bytes land
+      const unsigned bytes = (unsigned)xex[j] * (unsigned)sizeof(T);
+      if (bytes) mbar_expect_tx(&mb[j], bytes);
+      else mbar_arrive(&mb[j]);
+    }
+    const unsigned q = cluster_ctarank();
+    const unsigned rs = smem_u32(ring), ms = smem_u32(mb);
+    if (q + 1 < (unsigned)P.Q) { rimp[0] = mapa_shared(rs + (unsigned)(R * sizeof(T)), q + 1); rmb[0] = mapa_shared(ms, q + 1); }
+    if (q > 0) {
+      rimp[1] = mapa_shared(rs + (unsigned)((R + IL) * sizeof(T)), q - 1);
+      rmb[1] = mapa_shared(ms + (unsigned)(PL * 8), q - 1);
+    }
+    if (tid < 2) ready[tid] = -1;
+    cluster_sync_all();                                            // barriers armed before any export
+  }
   pdl_wait();                                                      // the prologue above reads setup data only
   if (done && *done) return;
+  if (SPLIT && warp == NW) {
+    // the import warp: follows the producer levels' barriers in order (L, then U)
+    // and publishes how far the imports have landed; the compute warps only read
+    // that word (a barrier check costs ~150 cycles; walking them on the critical
+    // path made every consumer level 2-3x slower)
+    if constexpr (SPLIT) {
+      for (int sw2 = 0; sw2 < 2; ++sw2) {
+        const int np = sw2 ? bi[15] : bi[13], off = sw2 ? PL : 0;
+        for (int u = 0; u < np; ++u) {
+          if (xex[off + u])
+            while (!mbar_test(&mb[off + u], 0)) __nanosleep(20);
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence_block();
+            ready[sw2] = u;
+          }
+        }
+      }
+    }
+  } else {
   const bool inplace = mode == TRI_UP && P.xU != nullptr;
   const size_t RB = (size_t)P.rec_bytes;
   using Buf = RegBuf<T, W>;
@@ -757,6 +850,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
 #pragma unroll
       for (int j = 0; j < W8; ++j) B.c[j] = ld_na(cp + 32 * j);
       B.out = __ldg(op + lane);
+      if constexpr (SPLIT) B.exp = __ldg(reinterpret_cast<const int *>(op + 32 + 32 * (int)(sizeof(T) / 4)) + lane);
       const size_t ri = (size_t)(gbase + s) * 32 + lane;
       if (upper) {
         B.dg = ld_nc(reinterpret_cast<const T *>(op + 32) + lane);
@@ -797,7 +891,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
     };
     // x_i = (rhs_i - sum_j a_ij x_j) [/ u_ii]: W ring gathers, four partial sums
     auto solve = [&](const Buf &B, int s) {
-      const bool tr = kRegTrace && P.dbg && blockIdx.x == 0 && lane == 0 && s < 2048;
+      const bool tr = !SPLIT && kRegTrace && P.dbg && blockIdx.x == 0 && lane == 0 && s < 2048;
       long long *tp = tr ? P.dbg + 8 * (sw * 2048 + s) : nullptr;
       if (tr) { tp[2] = clock64(); tp[6] = lvt[lvbase + s]; tp[7] = warp; tp[0] = tp[2]; }
       if (tr) {
@@ -833,6 +927,28 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
       }
     };
     auto level_of = [&](int t) { return t < ns ? (int)lvt[lvbase + t] : nlev; };
+    // split: wait until the neighbour's exports this slice reads have landed (the
+    // producer levels up to need - 1, monotone per warp); one acquire fence when any
+    int rdy = -1;
+    const unsigned rimp_sw = upper ? rimp[1] : rimp[0], rmb_sw = upper ? rmb[1] : rmb[0];
+    // (test_wait polling: a try_wait suspends the warp and a remote st.async
+    // completion did not wake it before the suspend limit — microseconds per wait)
+    auto wait_imports = [&](int s_) {
+      if constexpr (SPLIT) {
+        const int needu = (int)ndt[lvbase + s_] - 1;
+        if (rdy >= needu) return;
+        while ((rdy = ready[sw]) < needu) {}
+        __threadfence_block();                                     // acquire the landed values
+      }
+    };
+    // split: this slice's exported values to the neighbour's import area, each
+    // completing its bytes on the neighbour's barrier of this slice's level
+    auto export_ = [&](const Buf &B, int s_, const T &acc) {
+      if constexpr (SPLIT) {
+        if (B.exp >= 0)
+          st_async_cluster(rimp_sw + (unsigned)(B.exp * (int)sizeof(T)), acc, rmb_sw + (unsigned)lvt[lvbase + s_] * 8u);
+      }
+    };
     // The global stores are read only after the sweep-transition barrier.
     auto store = [&](const Buf &B, const T &acc, int s) {
       if (upper && P.xP) {                                         // coalesced: U-packed position of the row
@@ -854,6 +970,17 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
     // with the next slice (the NW = 23 variant, 80 registers).  NB = 2: two
     // buffers alternating, refilled two slices ahead (NW = 15; measured best
     // for stages with 1-2 slices per level).
+    // split trace (GEMSLR_TRACE=1, tools/trace_split.py): CTAs 0..Q-1 of block 0, lane 0
+    // of every slice: clock64 before the level wait, after the import wait, after the
+    // solve, and the slice's level; per CTA one (clock64, globaltimer) pair at start
+    const bool str = SPLIT && kRegTrace && P.dbg && blockIdx.x < (unsigned)P.Q && lane == 0;
+    long long *sbase = str ? P.dbg + 16 + (size_t)blockIdx.x * (2 * 2048 * 4) + (size_t)sw * 2048 * 4 : nullptr;
+    if (str && sw == 0 && warp == 0) {
+      long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      P.dbg[2 * blockIdx.x] = clock64();
+      P.dbg[2 * blockIdx.x + 1] = g;
+    }
     Buf A, B;
     int s = warp;
     load(A, s);
@@ -861,20 +988,40 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
 #pragma unroll 1
     while (s < ns) {
       int nxt = level_of(s + NW);                                  // read before the barrier: off the critical path
+      const long long tq0 = (str && s < 2048) ? clock64() : 0;
       wait_level(lvt[lvbase + s]);
+      wait_imports(s);
+      const long long tq1 = (str && s < 2048) ? clock64() : 0;
       const T a0 = solve(A, s);
       publish(A, s, a0);
+      if (str && s < 2048) {
+        const double pr = dabs2(a0);
+        long long *q4 = sbase + 4 * s;
+        q4[0] = tq0; q4[1] = tq1; q4[2] = clock64() + (pr != pr ? 1 : 0); q4[3] = lvt[lvbase + s] | ((long long)ndt[lvbase + s] << 32);
+      }
+      if (SPLIT_EXPORT_FIRST) export_(A, s, a0);
       depart(nxt);
+      if (!SPLIT_EXPORT_FIRST) export_(A, s, a0);
       store(A, a0, s);
       load(A, s + NB * NW);
       s += NW;
       if (NB == 2) {
         if (s >= ns) break;
         nxt = level_of(s + NW);
+        const long long tr0 = (str && s < 2048) ? clock64() : 0;
         wait_level(lvt[lvbase + s]);
+        wait_imports(s);
+        const long long tr1 = (str && s < 2048) ? clock64() : 0;
         const T a1 = solve(B, s);
         publish(B, s, a1);
+        if (str && s < 2048) {
+          const double pr = dabs2(a1);
+          long long *q4 = sbase + 4 * s;
+          q4[0] = tr0; q4[1] = tr1; q4[2] = clock64() + (pr != pr ? 1 : 0); q4[3] = lvt[lvbase + s] | ((long long)ndt[lvbase + s] << 32);
+        }
+        if (SPLIT_EXPORT_FIRST) export_(B, s, a1);
         depart(nxt);
+        if (!SPLIT_EXPORT_FIRST) export_(B, s, a1);
         store(B, a1, s);
         load(B, s + 2 * NW);
         s += NW;
@@ -900,6 +1047,8 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tri_reg(RegDev<T> P, int mode, T
     }
     for (; i < i1; i += 32 * NW) x[i] = x[i] - ld_cg(tmp + i);
   }
+  }                                                                // (compute warps)
+  if constexpr (SPLIT) cluster_sync_all();                         // no CTA leaves while a neighbour may still write
 }
 
 // sum_p val[p] * g(col[p]) over p in [p0, p1) in p order (the plain loop's rounding);
@@ -1202,6 +1351,101 @@ __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const i
       if (i < npk) pk[pkpos[i]] = v;                               // the next stage's packed right-hand side
     }
   }
+}
+
+// ----------------------------------------------------------------- K6+K7+K8 on one cluster (small s_l)
+// The same as k_ewx for the small interfaces of the deeper levels (C5: s_1 = 4.6k,
+// s_2 = 667 rows), where a grid-wide hand-off costs more than the work: ONE
+// cluster of C CTAs, CTA c owns the rows [c s / C, (c+1) s / C).  Each CTA sums
+// its W^H r_J partials over its warps (fixed order) into shared memory; after a
+// cluster barrier every CTA reads the C partial vectors through DSMEM in rank
+// order (the same s in all CTAs), forms t = G s and adds W t to its rows; a second
+// cluster barrier keeps the partials alive until every CTA has read them.
+__device__ inline double ld_dsmem(unsigned addr, double) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ inline cd ld_dsmem(unsigned addr, cd) {
+  cd v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+template <typename T, int NACC>
+__global__ void __launch_bounds__(256) k_ewc(int64_t s, int64_t rowbase, const int64_t *__restrict__ Eptr,
+                                             const int32_t *__restrict__ Ecol, const T *__restrict__ Eval,
+                                             const T *__restrict__ z, const T *__restrict__ zh, int64_t nloc,
+                                             const T *src, T *dst, const T *__restrict__ W, int64_t ldw, int k,
+                                             const T *__restrict__ G, const int *__restrict__ done, int64_t npk = 0,
+                                             const int *__restrict__ pkpos = nullptr, T *__restrict__ pk = nullptr) {
+  pdl_launch();
+  pdl_wait();
+  if (done && *done) return;                                       // uniform over the cluster (predecessor complete)
+  __shared__ T sv[256];
+  __shared__ T wpart[8][8 * NACC];
+  __shared__ T cpart[8 * NACC];
+  __shared__ T st[8 * NACC];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned C = gridDim.x, c = blockIdx.x;
+  const int64_t r0 = s * c / C, r1 = s * (c + 1) / C;
+  T acc[NACC];
+#pragma unroll
+  for (int a = 0; a < NACC; ++a) acc[a] = dzero<T>();
+  for (int64_t t0 = r0; t0 < r1; t0 += 256) {
+    const int64_t i = t0 + tid;
+    T v = dzero<T>();
+    if (i < r1) {
+      const T e = csr_dot(Eptr[i], Eptr[i + 1], Ecol, Eval, [&](int64_t cc) { return cc < nloc ? z[cc] : zh[cc - nloc]; });
+      v = (src ? src[rowbase + i] : dzero<T>()) - e;
+      dst[rowbase + i] = v;
+    }
+    sv[tid] = v;
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < NACC; ++a) {
+      const int cc = warp + 8 * a;
+      if (cc < k) {
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          const int64_t ii = t0 + rr * 32 + lane;
+          if (ii < r1) acc[a] += dconj(W[cc * ldw + ii]) * sv[rr * 32 + lane];
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < NACC; ++a) {
+    const T r = warp_sum(acc[a]);
+    if (lane == 0) wpart[warp][a] = r;                               // column warp + 8 a
+  }
+  __syncthreads();
+  if (tid < k) {                                                   // this CTA's partial of column tid
+    const T r = wpart[tid % 8][tid / 8];
+    cpart[tid] = r;
+  }
+  cluster_sync_all();
+  if (tid < k) {                                                   // s over the cluster, rank order
+    T sc = dzero<T>();
+    const unsigned a0 = smem_u32(&cpart[tid]);
+    for (unsigned q = 0; q < C; ++q) sc += ld_dsmem(mapa_shared(a0, q), dzero<T>());
+    sv[tid] = sc;
+  }
+  __syncthreads();
+  if (tid < k) {                                                   // t = G s
+    T t = dzero<T>();
+    for (int a = 0; a < k; ++a) t += G[(int64_t)a * k + tid] * sv[a];
+    st[tid] = t;
+  }
+  __syncthreads();
+  for (int64_t i = r0 + tid; i < r1; i += 256) {                  // r_J += W t
+    T a = dzero<T>();
+    for (int cc = 0; cc < k; ++cc) a += ld_nc(W + cc * ldw + i) * st[cc];
+    const T v = dst[rowbase + i] + a;
+    dst[rowbase + i] = v;
+    if (i < npk) pk[pkpos[i]] = v;                                 // the next stage's packed right-hand side
+  }
+  cluster_sync_all();                                              // partials read by every CTA before any exits
 }
 
 // ----------------------------------------------------------------- K8

@@ -137,12 +137,30 @@ struct PipePack {
 // row, stage-global packed L slice of the block's first L slice (right-hand
 // sides rhsL[(base + s) * 32 + lane]), same for U (mid).
 // lev_off: per block and sweep, the first record of every level and the end.
+//
+// Split form (Q > 1, the level-0 subdomains when Q x blocks fit the SMs): block b
+// is cut into Q contiguous row ranges ("chunks", rows [n q / Q, n (q+1) / Q) of the
+// block order), chunk q of block b is "block" b Q + q of the pack and runs on CTA
+// q of a Q-CTA cluster.  Levels are those of the whole block's DAG; a chunk keeps
+// the levels in which it has rows (its local levels).  Because L is lower and U
+// upper triangular in the block order, chunk q's L rows depend only on chunks
+// <= q and its U rows only on chunks >= q: with chunks at least one dependency
+// bandwidth thick, only on q - 1 (L) and q + 1 (U).  Those values ("imports")
+// arrive by asynchronous DSMEM stores (st.async) from the producing CTA into an
+// import area after the ring (slots R + i: L imports, R + IL + i: U imports), each
+// completing its bytes on the consumer's mbarrier of the producer's local level;
+// the consumer's slice waits on the barriers of the producer levels it needs
+// (sneed).  The producer never waits for the consumer, so the CTAs of a block
+// run pipelined one hand-off apart instead of paying it per level.
+// Record extension: int32 exp[32] after rdiag (import index in the consumer's
+// area of this sweep, -1 none).
 constexpr int REG_RING_BYTES = 128 * 1024;     // solution window: 16384 doubles / 8192 complex
-constexpr int REG_BINFO_INTS = 12;
+constexpr int REG_BINFO_INTS = 16;             // + split: producer-L xexp offset, producer-L levels, same for U
 inline int reg_width(int w) { return w <= 4 ? 4 : w <= 8 ? 8 : w <= 10 ? 10 : w <= 12 ? 12 : w <= 16 ? 16 : 0; }
 template <typename T>
-inline size_t reg_record_bytes(int W) {
-  const size_t b = (size_t)W * 32 * sizeof(T) + (size_t)((W + 7) / 8) * 32 * 16 + 32 * 4 + 32 * sizeof(T);
+inline size_t reg_record_bytes(int W, bool split = false) {
+  const size_t b = (size_t)W * 32 * sizeof(T) + (size_t)((W + 7) / 8) * 32 * 16 + 32 * 4 + 32 * sizeof(T) +
+                   (split ? 32 * 4 : 0);
   return (b + 127) / 128 * 128;
 }
 template <typename T>
@@ -161,6 +179,14 @@ struct RegPack {
   int64_t lslices = 0, uslices = 0, nrec = 0;
   int64_t near = 0, far = 0;
   int max_levels = 0;
+  // split form (Q > 1): import areas (entries, max over chunks), producer level
+  // tables, per-record prefix-max of the producer level needed (+1, 0 = none)
+  int Q = 1;
+  int imp_L = 0, imp_U = 0;                     // IL, IU
+  int plev_L = 0, plev_U = 0;                   // max producer local levels (counter / xexp table sizes)
+  std::vector<uint16_t> sneed;                  // per record
+  std::vector<uint16_t> xexp;                   // per chunk and sweep: values exported per local level
+  int64_t exports = 0;
 };
 
 template <typename T>
@@ -221,6 +247,8 @@ struct SetupOptions {
   double shift = 0.0;                           // complex ILU shift factor, complex only
   int coord_dim = 0;
   const double *coords = nullptr;               // n x coord_dim (optional)
+  int split = 0;                                // triangular-solve clusters per block: 0 auto, 1 off, 2/4 forced
+  int sms = 148;                                // SMs of the device (auto split: blocks x Q must fit)
 };
 
 // partition.cpp
@@ -232,7 +260,8 @@ template <typename T> bool ilu0(const Csr<T> &B, Factor<T> &F, std::string &err)
 template <typename T> bool ilut(const Csr<T> &B, double tau, int lfil, Factor<T> &F, std::string &err);
 
 // schedule.cpp
-template <typename T> void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, Stage<T> &S);
+template <typename T> void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, Stage<T> &S,
+                                      int Q = 1);
 
 // hostplan.cpp
 template <typename T>

@@ -9,6 +9,7 @@
 // level they are sorted ascending and packed 32 per slice (one row per lane),
 // entries column-major inside the slice so a warp's loads are coalesced.
 #include <algorithm>
+#include <unordered_map>
 
 #include "plan.hpp"
 
@@ -16,8 +17,12 @@ namespace gemslr {
 
 namespace {
 
+// Q > 1 (split form, plan.hpp RegPack): block b is packed as Q chunks of
+// contiguous rows, each with the levels of the whole block's DAG in which it has
+// rows; "block" b Q + q of the pack is chunk q of block b.
 template <typename T>
-void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, bool upper, TriPack<T> &P) {
+void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, bool upper, TriPack<T> &P,
+                int Q = 1) {
   P = TriPack<T>();
   P.blk_lev.push_back(0);
   P.lev_slice.push_back(0);
@@ -46,27 +51,32 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
     }
     if (n == 0) nlev = 0;
     P.max_depth = std::max(P.max_depth, (int)nlev);
+    std::vector<int32_t> ll;                                      // L levels (U packing order inside a level)
+    if (upper) {
+      const Csr<T> &Lm = fac[b].L;
+      ll.assign(n, 0);
+      for (int64_t i = 0; i < n; ++i) {
+        int32_t v = 0;
+        for (int64_t p = Lm.ptr[i]; p < Lm.ptr[i + 1]; ++p) v = std::max(v, ll[Lm.col[p]] + 1);
+        ll[i] = v;
+      }
+    }
+   for (int q = 0; q < Q; ++q) {
+    const int64_t c0 = n * q / Q, c1 = n * (q + 1) / Q;            // this chunk's rows
     // bucket rows by level (ascending row inside a level)
     std::vector<int64_t> cnt(nlev + 1, 0);
-    for (int64_t i = 0; i < n; ++i) cnt[lev[i] + 1]++;
+    for (int64_t i = c0; i < c1; ++i) cnt[lev[i] + 1]++;
     for (int32_t v = 0; v < nlev; ++v) cnt[v + 1] += cnt[v];
-    std::vector<int64_t> rows(n);
+    std::vector<int64_t> rows(c1 - c0);
     {
       std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
-      for (int64_t i = 0; i < n; ++i) rows[pos[lev[i]]++] = i;
+      for (int64_t i = c0; i < c1; ++i) rows[pos[lev[i]]++] = i;
     }
     if (upper) {
       // Inside a U level, order the rows by their L level (ascending row within
       // it), the order of the L packing: the rows of one L slice that share a U
       // level become adjacent in the U packing, so the L sweep's stores of its
       // results at their U positions coalesce.  Any order inside a level is valid.
-      const Csr<T> &Lm = fac[b].L;
-      std::vector<int32_t> ll(n, 0);
-      for (int64_t i = 0; i < n; ++i) {
-        int32_t v = 0;
-        for (int64_t p = Lm.ptr[i]; p < Lm.ptr[i + 1]; ++p) v = std::max(v, ll[Lm.col[p]] + 1);
-        ll[i] = v;
-      }
       for (int32_t v = 0; v < nlev; ++v)
         std::stable_sort(rows.begin() + cnt[v], rows.begin() + cnt[v + 1],
                          [&](int64_t a, int64_t c) { return ll[a] < ll[c]; });
@@ -74,6 +84,7 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
     auto len = [&](int64_t i) { return M.ptr[i + 1] - M.ptr[i]; };
     (void)len;
     for (int32_t v = 0; v < nlev; ++v) {
+      if (Q > 1 && cnt[v + 1] == cnt[v]) continue;                 // a level without rows of this chunk
       for (int64_t s0 = cnt[v]; s0 < cnt[v + 1]; s0 += 32) {
         const int64_t s1 = std::min<int64_t>(s0 + 32, cnt[v + 1]);
         int64_t width = 0;
@@ -107,6 +118,7 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
       P.lev_slice.push_back((int32_t)(P.slice_off.size() - 1));
     }
     P.blk_lev.push_back((int32_t)(P.lev_slice.size() - 1));
+   }
   }
 }
 
@@ -304,11 +316,15 @@ static std::pair<int, int> refine_record(uint8_t *base, int W) {
   return {before, after};
 }
 
-// Register-prefetched records of the two sweeps (RegPack, k_tri_reg).
+// Register-prefetched records of the two sweeps (RegPack, k_tri_reg).  Q > 1:
+// the split form (plan.hpp), with the chunks of pack_sweep(Q) as its "blocks".
 template <typename T>
-void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPack<T> &Up, RegPack<T> &P) {
+void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPack<T> &Up, RegPack<T> &P, int Q = 1) {
   P = RegPack<T>();
-  const size_t nb = blk.size() - 1;
+  P.Q = Q;
+  const bool split = Q > 1;
+  const size_t nblk = blk.size() - 1;
+  const size_t nb = nblk * (size_t)Q;                              // pack "blocks" (chunks)
   const int64_t R0 = blk.front(), NR = blk.back() - blk.front();
   P.lslices = (int64_t)Lp.slice_row.size() / 32;
   P.uslices = (int64_t)Up.slice_row.size() / 32;
@@ -318,7 +334,7 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
   P.W = reg_width(std::max(P.wmax, 1));
   if (P.W == 0) return;
   const int W = P.W, W8 = (W + 7) / 8, VE = 16 / (int)sizeof(T);
-  P.rec_bytes = reg_record_bytes<T>(W);
+  P.rec_bytes = reg_record_bytes<T>(W, split);
   P.nrec = P.lslices + P.uslices;
   P.data.assign((size_t)P.nrec * P.rec_bytes, 0);
   std::vector<int32_t> upos(NR, -1);
@@ -333,9 +349,29 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
       const int32_t row = Up.slice_row[s * 32 + lane];
       if (row >= 0) upos[row - R0] = (int32_t)(s * 32 + lane);
     }
-  // solution window: the smallest power of two covering every dependency
-  // distance (level end - dependency position), so the ring leaves shared
-  // memory to the record stages of k_tri_seq
+  // chunk of every stage row (the chunk's rows: pack_sweep's n q / Q split)
+  std::vector<int32_t> chunk(NR, 0);
+  for (size_t b = 0; b < nblk; ++b) {
+    const int64_t n = blk[b + 1] - blk[b];
+    for (int q = 0; q < Q; ++q)
+      for (int64_t i = n * q / Q; i < n * (q + 1) / Q; ++i) chunk[blk[b] - R0 + i] = (int32_t)(b * Q + q);
+  }
+  // slice -> (chunk, local level) of each sweep, for the producer side of imports
+  std::vector<int32_t> sl_chunk[2], sl_lev[2];
+  for (int sweep = 0; sweep < 2; ++sweep) {
+    const TriPack<T> &S = sweep ? Up : Lp;
+    const int64_t ns = (int64_t)S.slice_row.size() / 32;
+    sl_chunk[sweep].assign(ns, 0);
+    sl_lev[sweep].assign(ns, 0);
+    for (size_t c = 0; c < nb; ++c)
+      for (int32_t v = S.blk_lev[c]; v < S.blk_lev[c + 1]; ++v)
+        for (int32_t sl = S.lev_slice[v]; sl < S.lev_slice[v + 1]; ++sl) {
+          sl_chunk[sweep][sl] = (int32_t)c;
+          sl_lev[sweep][sl] = v - S.blk_lev[c];
+        }
+  }
+  // solution window: the smallest power of two covering every (in-chunk)
+  // dependency distance (level end - dependency position)
   int64_t need = 1;
   for (size_t b = 0; b < nb; ++b)
     for (int sweep = 0; sweep < 2; ++sweep) {
@@ -346,7 +382,7 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
         const int64_t send = S.lev_slice[v + 1] - sb0;
         for (int64_t g = S.slice_off[S.lev_slice[v]]; g < S.slice_off[S.lev_slice[v + 1]]; ++g) {
           const int32_t dep = S.col[g];
-          if (dep < 0) continue;
+          if (dep < 0 || chunk[dep - R0] != (int32_t)b) continue;
           const int32_t q = (sweep ? upos[dep - R0] : P.lpos[dep - R0]) - sb0 * 32;
           need = std::max(need, send * 32 - q);
         }
@@ -355,11 +391,53 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
   P.ring = 1024;
   while (P.ring < need && P.ring < REG_RING_BYTES / (int)sizeof(T)) P.ring *= 2;
   const int R = P.ring;
+  // split: imports of every chunk and sweep (dependency rows in another chunk),
+  // numbered in the order the consumer's records first need them
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> imp[2];   // per chunk: (stage row, producer slice)
+  if (split) {
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      const TriPack<T> &S = sweep ? Up : Lp;
+      imp[sweep].assign(nb, {});
+      std::vector<int32_t> seen(NR, -1);
+      for (size_t b = 0; b < nb; ++b)
+        for (int64_t g = S.slice_off[S.lev_slice[S.blk_lev[b]]]; g < S.slice_off[S.lev_slice[S.blk_lev[b + 1]]]; ++g) {
+          const int32_t dep = S.col[g];
+          if (dep < 0) continue;
+          const int32_t pc = chunk[dep - R0];
+          if (pc == (int32_t)b) continue;
+          // one-directional chains only: L from chunk q - 1, U from q + 1 of the same block
+          if (pc / Q != (int32_t)b / Q || pc != (int32_t)b + (sweep ? 1 : -1)) return;
+          if (seen[dep - R0] == (int32_t)b) continue;
+          seen[dep - R0] = (int32_t)b;
+          const int32_t pslice = (sweep ? upos[dep - R0] : P.lpos[dep - R0]) / 32;
+          imp[sweep][b].push_back({dep - (int32_t)R0, pslice});
+        }
+    }
+    for (size_t b = 0; b < nb; ++b) {
+      P.imp_L = std::max(P.imp_L, (int)imp[0][b].size());
+      P.imp_U = std::max(P.imp_U, (int)imp[1][b].size());
+    }
+    if ((int64_t)R + P.imp_L + P.imp_U > 65535) return;
+  }
+  // per chunk and sweep: stage row -> import index (only rows imported by that chunk)
+  std::vector<std::unordered_map<int32_t, int32_t>> impmap[2];
+  if (split)
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      impmap[sweep].resize(nb);
+      for (size_t b = 0; b < nb; ++b)
+        for (size_t i = 0; i < imp[sweep][b].size(); ++i) impmap[sweep][b][imp[sweep][b][i].first] = (int32_t)i;
+    }
+  std::vector<int64_t> rec_of[2];                                  // stage slice -> record
+  rec_of[0].assign(P.lslices, -1);
+  rec_of[1].assign(P.uslices, -1);
   int64_t rec = 0;
   for (size_t b = 0; b < nb; ++b) {
-    int32_t info[REG_BINFO_INTS];
-    info[8] = (int32_t)blk[b];
-    info[9] = (int32_t)blk[b + 1];
+    int32_t info[REG_BINFO_INTS] = {0};
+    const size_t bk = b / (size_t)Q;                               // original block
+    const int64_t nbk = blk[bk + 1] - blk[bk];
+    const int qq = (int)(b % (size_t)Q);
+    info[8] = (int32_t)(blk[bk] + nbk * qq / Q);                   // this chunk's rows
+    info[9] = (int32_t)(blk[bk] + nbk * (qq + 1) / Q);
     for (int sweep = 0; sweep < 2; ++sweep) {
       const TriPack<T> &S = sweep ? Up : Lp;
       const bool upper = sweep == 1;
@@ -371,6 +449,7 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
       info[6 + sweep] = (int32_t)P.lev_off.size();
       info[10 + sweep] = sb0;
       P.max_levels = std::max(P.max_levels, lv1 - lv0);
+      int need_pref = -1;                                          // split: producer level needed so far
       for (int32_t v = lv0; v < lv1; ++v) {
         P.lev_off.push_back((int32_t)rec);
         const int32_t send = S.lev_slice[v + 1] - sb0;     // level end (block-relative slice)
@@ -381,6 +460,11 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
           uint16_t *col = reinterpret_cast<uint16_t *>(base + (size_t)W * 32 * sizeof(T));
           int32_t *out = reinterpret_cast<int32_t *>(col + (size_t)W8 * 32 * 8);
           T *rdiag = reinterpret_cast<T *>(out + 32);
+          if (split) {
+            int32_t *exp = reinterpret_cast<int32_t *>(rdiag + 32);
+            for (int lane = 0; lane < 32; ++lane) exp[lane] = -1;
+          }
+          rec_of[sweep][s] = rec;
           if (v - lv0 > 65535) return;
           P.slev.push_back((uint16_t)(v - lv0));
           // entries of every lane with their ring slots
@@ -394,12 +478,21 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
               const int64_t g = S.slice_off[s] + 32 * e + lane;
               const int32_t dep = S.col[g];
               if (dep < 0) continue;
+              if (split && chunk[dep - R0] != (int32_t)b) {         // an import (DSMEM from the neighbour chunk)
+                const int32_t ii = impmap[sweep][b].at(dep - (int32_t)R0);
+                const int32_t pslice = imp[sweep][b][ii].second;
+                need_pref = std::max(need_pref, sl_lev[sweep][pslice]);
+                ent[lane].push_back(Ent{S.val[g], (uint16_t)(R + (upper ? P.imp_L : 0) + ii)});
+                P.near++;
+                continue;
+              }
               const int32_t pd = upper ? upos[dep - R0] : P.lpos[dep - R0];
               const int32_t q = pd - sb0 * 32;                  // block-relative position
               if ((int64_t)send * 32 - 1 - q < R) { ent[lane].push_back(Ent{S.val[g], (uint16_t)(q & (R - 1))}); P.near++; }
               else { P.far++; }
             }
           }
+          if (split) P.sneed.push_back((uint16_t)(need_pref + 1));
           // Column e of the slice is one shared-memory gather of 32 lanes (8 or 16
           // bytes each); order each lane's entries (any order gives the same sum up
           // to rounding) so that every column spreads its distinct slots over the
@@ -446,6 +539,45 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
     P.binfo.insert(P.binfo.end(), info, info + REG_BINFO_INTS);
     P.max_block_slices = std::max(P.max_block_slices, info[1] + info[4]);
   }
+  if (split) {
+    // exports: the producer lane of every import, and per producer chunk and sweep
+    // the number of values exported at each local level (the bytes the consumer's
+    // barrier of that level awaits); binfo[12..15] of the CONSUMER point at its
+    // producers' tables
+    std::vector<int32_t> xoff[2];
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      const TriPack<T> &S = sweep ? Up : Lp;
+      xoff[sweep].assign(nb, 0);
+      std::vector<std::vector<uint16_t>> tab(nb);
+      for (size_t c = 0; c < nb; ++c) tab[c].assign(S.blk_lev[c + 1] - S.blk_lev[c], 0);
+      for (size_t b = 0; b < nb; ++b)
+        for (size_t i = 0; i < imp[sweep][b].size(); ++i) {
+          const int32_t row = imp[sweep][b][i].first, ps = imp[sweep][b][i].second;
+          const int32_t pd = sweep ? upos[row] : P.lpos[row];
+          const int64_t r = rec_of[sweep][ps];
+          uint8_t *base = P.data.data() + (size_t)r * P.rec_bytes;
+          int32_t *exp = reinterpret_cast<int32_t *>(base + (size_t)W * 32 * sizeof(T) + (size_t)W8 * 512 + 32 * 4 +
+                                                     32 * sizeof(T));
+          if (exp[pd % 32] >= 0) return;                           // exported to two chunks: not supported
+          exp[pd % 32] = (int32_t)i;
+          P.exports++;
+          uint16_t &t = tab[sl_chunk[sweep][ps]][sl_lev[sweep][ps]];   // values the consumer's barrier awaits
+          if (t == 65535) return;
+          t++;
+        }
+      for (size_t c = 0; c < nb; ++c) {
+        xoff[sweep][c] = (int32_t)P.xexp.size();
+        P.xexp.insert(P.xexp.end(), tab[c].begin(), tab[c].end());
+        (sweep ? P.plev_U : P.plev_L) = std::max(sweep ? P.plev_U : P.plev_L, (int)tab[c].size());
+      }
+    }
+    for (size_t b = 0; b < nb; ++b) {
+      int32_t *info = &P.binfo[b * REG_BINFO_INTS];
+      const int qq = (int)(b % (size_t)Q);
+      if (qq > 0) { info[12] = xoff[0][b - 1]; info[13] = Lp.blk_lev[b] - Lp.blk_lev[b - 1]; }
+      if (qq + 1 < Q) { info[14] = xoff[1][b + 1]; info[15] = Up.blk_lev[b + 2] - Up.blk_lev[b + 1]; }
+    }
+  }
   {
     long long cb = 0, ca = 0;
 #pragma omp parallel for schedule(dynamic, 256) reduction(+ : cb, ca)
@@ -464,16 +596,29 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
 
 }  // namespace
 
+// Q > 1: the split form (every block's sweeps over a Q-CTA cluster); when it
+// cannot be built (a dependency two chunks away, too many imports) the stage
+// falls back to Q / 2, down to the one-CTA form.  The split form has no TMA /
+// level-kernel variant (their blocks must be independent).
 template <typename T>
-void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, Stage<T> &S) {
+void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, Stage<T> &S, int Q) {
   S.blk = blk;
+  for (; Q > 1; Q /= 2) {
+    pack_sweep(blk, fac, false, S.Lp, Q);
+    pack_sweep(blk, fac, true, S.Up, Q);
+    pack_reg(blk, S.Lp, S.Up, S.reg, Q);
+    if (S.reg.ok) {
+      S.pipe = PipePack<T>();
+      return;
+    }
+  }
   pack_sweep(blk, fac, false, S.Lp);
   pack_sweep(blk, fac, true, S.Up);
   pack_pipe(blk, S.Lp, S.Up, S.pipe);
   pack_reg(blk, S.Lp, S.Up, S.reg);
 }
 
-template void pack_stage<double>(const std::vector<int64_t> &, const std::vector<Factor<double>> &, Stage<double> &);
-template void pack_stage<zc>(const std::vector<int64_t> &, const std::vector<Factor<zc>> &, Stage<zc> &);
+template void pack_stage<double>(const std::vector<int64_t> &, const std::vector<Factor<double>> &, Stage<double> &, int);
+template void pack_stage<zc>(const std::vector<int64_t> &, const std::vector<Factor<zc>> &, Stage<zc> &, int);
 
 }  // namespace gemslr
