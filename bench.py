@@ -309,6 +309,30 @@ def run_ours(args):
         e2e_ms = float(t.item())
     e2e = {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": round(bh.nbytes / K),
            "d2h_bytes_per_step": round(xh.nbytes / K), "h2d_bytes_total": bh.nbytes, "d2h_bytes_total": xh.nbytes}
+    # the distributed code path at N = 1 (one-rank NCCL communicator: every all-reduce an
+    # NCCL call, overlapped SpMV form, FGMRES graphs with their NCCL calls, no peers):
+    # what the multi-GPU path costs per GPU before any communication volume
+    dist_path = None
+    if world == 1 and not args.no_dist_path:
+        try:
+            s2 = gm.Solver(prob.rowptr, prob.colidx, prob.values, prm["levels"], prm["subdomains"], prm["rank"],
+                           ilu=prm["ilu"], ilut_drop=prm["ilut_drop"], ilut_fill=prm["ilut_fill"], coords=prob.coords,
+                           device=local, comm="nccl1")
+            s2.solve(bd, rtol=1e-300, restart=restart, maxit=max(W, 1))
+            torch.cuda.synchronize()
+            a0 = s2.stats()["allreduces"]
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            o2 = s2.solve(bd, rtol=1e-300, restart=restart, maxit=K)
+            f1.record(stream)
+            torch.cuda.synchronize()
+            dist_path = {"ms_per_iteration": round(f0.elapsed_time(f1) / o2["its"], 4), "iterations": o2["its"],
+                         "nccl_allreduces_per_iteration": round((s2.stats()["allreduces"] - a0) / o2["its"], 2),
+                         "note": "distributed code path on this GPU over a one-rank NCCL communicator (no peers)"}
+            s2.close()
+        except Exception as e:                                     # report, keep the main line
+            dist_path = {"error": str(e)[:200]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(prob, prm, s, b, args.cpu_iters)
@@ -329,6 +353,8 @@ def run_ours(args):
                          "(no graphs, done flag read every iteration: no no-op launches)",
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
     }
+    if dist_path is not None:
+        line["dist_path_n1"] = dist_path
     if cpu is not None:
         line["cpu_baseline"] = cpu
     if rank == 0:
@@ -415,6 +441,7 @@ def main():
     ap.add_argument("--cluster-ctas", type=int, default=0)
     ap.add_argument("--cpu-iters", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dist-path", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -33,6 +33,11 @@ namespace gemslr {
 
 // SMs of the current device (cudaDevAttrMultiProcessorCount; sizes the grids and
 // the cooperative k_ewx launch, so a partitioned GPU — MIG, MPS limits — still works)
+// E_l's columns: local (or U-packed) positions below kHaloE, halo entries at
+// kHaloE + index (the E kernels take nloc = kHaloE); packed positions may exceed
+// the local length, so the split point cannot be n.
+static constexpr int32_t kHaloE = 1 << 30;
+
 static int num_sm() {
   static int cache[64] = {0};
   int dev = 0;
@@ -325,6 +330,7 @@ struct LevelDev {
   // one GPU, register trisolve: E_l's columns as U-packed positions of the level's
   // stage, so E_l z1 reads z1 from the U-packed copy the DOWN trisolve writes (xpm)
   const int32_t *Ecol_p = nullptr;
+  const int32_t *esidx_p = nullptr;  // several ranks: hE's send indices as U-packed positions
   // one GPU: k_ewx also writes the first npk rows of r_J (the next stage's rows)
   // at their packed L positions pkpos in that stage's right-hand-side buffer
   int64_t npk = 0;
@@ -356,12 +362,23 @@ struct Engine {
   int64_t n = 0, nnzA = 0;
   // SpMV (SELL-32 of Â)
   int64_t nslices = 0, sell_padded = 0, sell_wmax = 0;
+  // long / uneven rows: warp-per-row CSR SpMV (k_spmv_wpr) instead of SELL-32
+  bool use_wpr = false;
+  const int64_t *csr_ptr = nullptr;
+  const int32_t *csr_col = nullptr;
+  const D *csr_val = nullptr;
   const int64_t *sell_off = nullptr;
   const int32_t *sell_col = nullptr;
   const D *sell_val = nullptr;
   std::vector<LevelDev<D>> lev;
   StageDev<D> last;
   const int64_t *perm_d = nullptr;   // natural (original) row of every local row
+  // distributed SpMV: the SELL slices without / with halo columns, so the halo
+  // exchange (on comm_stream) overlaps the interior slices (north_star; Note N P:L58-63)
+  const int *sl_in = nullptr, *sl_bd = nullptr;
+  int64_t n_in = 0, n_bd = -1;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool dist = false;                 // distributed path: several ranks, or a forced one-rank NCCL communicator
   HaloDev<D> hA;
   std::vector<HaloDev<D>> hE, hF;
@@ -390,6 +407,9 @@ struct Engine {
   const double *graph_hist = nullptr;  // captured k_fgmres_scale nodes write hist: a new buffer needs new graphs
   cudaStream_t cap_stream = nullptr;
   ~Engine() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     if (hflags) cudaFreeHost(hflags);
     for (auto &ge : graphs) if (ge) cudaGraphExecDestroy(ge);
     if (cap_stream) cudaStreamDestroy(cap_stream);
@@ -397,7 +417,8 @@ struct Engine {
   double setup_host_s = 0, setup_dev_s = 0, arnoldi_s = 0;
 
   void upload(cudaStream_t s);
-  void exchange(HaloDev<D> &h, const D *src, const int *doneflag);
+  void exchange(HaloDev<D> &h, const D *src, const int *doneflag, cudaStream_t comm_st = nullptr,
+                const int *sidx = nullptr);
   void allreduce(D *buf, size_t count);
   void apply_from(int l0, const D *in, D *out, const int *doneflag);
   // several right-hand sides (NEXT-4, one GPU): column-major n x nr blocks, leading dimension ld
@@ -622,6 +643,31 @@ void Engine<T>::upload(cudaStream_t s) {
   sell_off = P.upload<int64_t>(off, s);
   sell_col = P.upload<int32_t>(col, s);
   sell_val = P.upload<D>(val, s);
+  {
+    // SELL pads every lane of a slice to the slice's longest row: rows of 32+
+    // entries on average, or more than half the stored entries padding, go to the
+    // warp-per-row kernel (GEMSLR_SPMV=sell / wpr forces one)
+    const double avg = n > 0 ? (double)nnzA / (double)n : 0.0;
+    use_wpr = avg >= 32.0 || (double)sell_padded > 2.0 * (double)std::max<int64_t>(nnzA, 1);
+    if (const char *e = getenv("GEMSLR_SPMV")) use_wpr = std::string(e) == "wpr";
+    if (use_wpr) {
+      csr_ptr = P.upload<int64_t>(A.ptr, s);
+      csr_col = P.upload<int32_t>(A.col, s);
+      csr_val = P.upload<D>(A.val, s);
+    }
+  }
+  if (dist) {
+    std::vector<int32_t> in, bd;
+    for (int64_t sl = 0; sl < nslices; ++sl) {
+      bool halo = false;
+      for (int64_t e = off[sl]; e < off[sl + 1] && !halo; ++e) halo = col[e] >= n;
+      (halo ? bd : in).push_back((int32_t)sl);
+    }
+    sl_in = P.upload<int32_t>(in, s);
+    sl_bd = P.upload<int32_t>(bd, s);
+    n_in = (int64_t)in.size();
+    n_bd = (int64_t)bd.size();
+  }
   std::vector<int64_t> nat(n);
   for (int64_t i = 0; i < n; ++i) nat[i] = plan.st.perm[plan.gpos[i]];
   perm_d = P.upload<int64_t>(nat, s);
@@ -636,6 +682,12 @@ void Engine<T>::upload(cudaStream_t s) {
     d.s = n - d.o1;
     d.st = upload_stage<D>(P, s, plan.stage[l], ctx->params.cluster_ctas, ctx->params.tri_kernel);
     d.E = upload_csr<D>(P, s, plan.E[l]);
+    {                                                              // E's halo columns at kHaloE + index
+      std::vector<int32_t> ec(plan.E[l].col);
+      for (auto &c : ec)
+        if (c >= n) c = kHaloE + (int32_t)(c - n);
+      d.E.col = P.upload<int32_t>(ec, s);
+    }
     d.F = upload_csr<D>(P, s, plan.F[l]);
     if (d.st.reg) {                                                // sparse UP pack: the rows with F_l entries
       const auto &Fh = plan.F[l];
@@ -657,21 +709,35 @@ void Engine<T>::upload(cudaStream_t s) {
         d.st.frow = P.upload<int>(frow, s);
         d.st.nf = (int64_t)fpos.size();
       }
-      if (!dist && d.st.xU && d.st.nf >= 0) {        // the UP then reads z1 from xU (k_pack_f path)
+      if (d.st.xU && d.st.nf >= 0) {                 // the UP then reads z1 from xU (k_pack_f path)
         const auto &Eh = plan.E[l];
         std::vector<int32_t> upos(S.reg.lpos.size(), -1);
         for (size_t q = 0; q < S.Up.slice_row.size(); ++q) {
           const int64_t row = (int64_t)S.Up.slice_row[q] - R0;
           if (S.Up.slice_row[q] >= 0 && row >= 0 && row < (int64_t)upos.size()) upos[row] = (int32_t)q;
         }
+        auto packed = [&](int64_t lrow_) -> int32_t {               // local row -> U-packed position, -1 if none
+          const int64_t row = lrow_ - R0;
+          return (row < 0 || row >= (int64_t)upos.size()) ? -1 : upos[row];
+        };
         std::vector<int32_t> ecp(Eh.col.size());
         bool eok = true;
         for (size_t q = 0; q < Eh.col.size() && eok; ++q) {
-          const int64_t row = (int64_t)Eh.col[q] - R0;
-          if (row < 0 || row >= (int64_t)upos.size() || upos[row] < 0) eok = false;
-          else ecp[q] = upos[row];
+          if (Eh.col[q] >= n) { ecp[q] = kHaloE + (int32_t)(Eh.col[q] - n); continue; }   // halo: as in E.col
+          ecp[q] = packed(Eh.col[q]);
+          eok = ecp[q] >= 0;
         }
-        if (eok && !ecp.empty()) d.Ecol_p = P.upload<int32_t>(ecp, s);
+        // several ranks: the z1 values this rank sends for the others' E_l are read
+        // from the same U-packed copy
+        std::vector<int32_t> sp(plan.hE[l].sidx.size());
+        for (size_t q = 0; q < sp.size() && eok; ++q) {
+          sp[q] = packed(plan.hE[l].sidx[q]);
+          eok = sp[q] >= 0;
+        }
+        if (eok && !ecp.empty()) {
+          d.Ecol_p = P.upload<int32_t>(ecp, s);
+          d.esidx_p = P.upload<int32_t>(sp, s);
+        }
       }
     }
     hE[l] = upload_halo<D>(P, s, plan.hE[l]);
@@ -679,8 +745,9 @@ void Engine<T>::upload(cudaStream_t s) {
   }
   hA = upload_halo<D>(P, s, plan.hA);
   last = upload_stage<D>(P, s, plan.last_stage, ctx->params.cluster_ctas, ctx->params.tri_kernel);
-  if (!dist) {                                                     // packed next-stage right-hand sides from k_ewx
+  {                                                                // packed next-stage right-hand sides from k_ewx / k_waxpy
     for (int l = 0; l < L; ++l) {
+      if (dist && l + 1 == L) continue;                            // several ranks: C_last is gathered and replicated
       LevelDev<D> &d = lev[l];
       const Stage<T> &NS = (l + 1 < L) ? plan.stage[l + 1] : plan.last_stage;
       StageDev<D> &nd = (l + 1 < L) ? lev[l + 1].st : last;
@@ -723,14 +790,20 @@ void Engine<T>::upload(cudaStream_t s) {
 // Neighbour exchange: pack src[sidx] and send/receive with every
 // peer in one NCCL group on the solver stream.  No-op on one GPU.
 template <typename T>
-void Engine<T>::exchange(HaloDev<D> &h, const D *src, const int *doneflag) {
+void Engine<T>::exchange(HaloDev<D> &h, const D *src, const int *doneflag, cudaStream_t comm_st, const int *sidx) {
   if (h.peer.empty()) return;
   Comm &C = ctx->comm;
   const int w = (int)(sizeof(D) / sizeof(double));
   if (h.nsend > 0) {
     const int grid = (int)std::min<int64_t>((h.nsend + 255) / 256, 4 * num_sm());
-    k_gather_idx<D><<<grid, 256, 0, ctx->stream>>>(h.nsend, h.sidx, src, h.sbuf, doneflag);
+    k_gather_idx<D><<<grid, 256, 0, ctx->stream>>>(h.nsend, sidx ? sidx : h.sidx, src, h.sbuf, doneflag);
     CK(cudaGetLastError());
+  }
+  if (comm_st) {                                                   // the caller forked comm_st after the pack
+    CK(cudaEventRecord(ev_fork, ctx->stream));
+    CK(cudaStreamWaitEvent(comm_st, ev_fork, 0));
+  } else {
+    comm_st = ctx->stream;
   }
   if (C.hostmode()) {
     const size_t ns = (size_t)h.nsend * w, nr = (size_t)h.nrecv * w;
@@ -755,8 +828,8 @@ void Engine<T>::exchange(HaloDev<D> &h, const D *src, const int *doneflag) {
     C.check(C.gstart_(), "GroupStart");
     for (size_t i = 0; i < h.peer.size(); ++i) {
       const int64_t ns = h.soff[i + 1] - h.soff[i], nr = h.roff[i + 1] - h.roff[i];
-      if (ns > 0) C.check(C.send_(h.sbuf + h.soff[i], (size_t)ns * w, 8, h.peer[i], C.comm, ctx->stream), "Send");
-      if (nr > 0) C.check(C.recv_(h.rbuf + h.roff[i], (size_t)nr * w, 8, h.peer[i], C.comm, ctx->stream), "Recv");
+      if (ns > 0) C.check(C.send_(h.sbuf + h.soff[i], (size_t)ns * w, 8, h.peer[i], C.comm, comm_st), "Send");
+      if (nr > 0) C.check(C.recv_(h.rbuf + h.roff[i], (size_t)nr * w, 8, h.peer[i], C.comm, comm_st), "Recv");
     }
     C.check(C.gend_(), "GroupEnd");
   }
@@ -1042,17 +1115,54 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
 
 template <typename T>
 void Engine<T>::spmv(const D *x, D *y, int mode, const D *b, const int *doneflag) {
+  if (dist && n_bd >= 0 && sell_wmax <= 8 && !ctx->comm.hostmode()) {
+    // Overlapped form (NCCL): pack the send values, fork the grouped send/recv onto
+    // comm_stream, the interior slices meanwhile, join, then the slices with halo
+    // columns.  Captured into the FGMRES graphs like the rest (fork / join events).
+    if (!comm_stream) {
+      CK(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    const bool peers = !hA.peer.empty();
+    if (peers) exchange(hA, x, doneflag, comm_stream);             // exterior columns (Note N P:L59-61)
+    if (peers) CK(cudaEventRecord(ev_join, comm_stream));
+    Timed t(ctx->prof, ctx->stream, KC_SPMV);
+    constexpr int SPW = 2;
+    auto part = [&](auto kern, const int *lst, int64_t cnt) {
+      if (cnt <= 0) return;
+      const int g2 = (int)std::max<int64_t>((cnt + 8 * SPW - 1) / (8 * SPW), 1);
+      launch_pdl(kern, dim3(g2), dim3(256), 0, ctx->stream, n, cnt, sell_off, sell_col, sell_val, x, hA.rbuf, y, mode, b,
+                 doneflag, lst);
+    };
+    part(k_spmv_sell2<D, false, SPW, 8>, sl_in, n_in);
+    if (peers) CK(cudaStreamWaitEvent(ctx->stream, ev_join, 0));
+    part(k_spmv_sell2<D, true, SPW, 8>, sl_bd, n_bd);
+    CK(cudaGetLastError());
+    return;
+  }
   exchange(hA, x, doneflag);                                     // exterior columns (Note N P:L59-61)
   Timed t(ctx->prof, ctx->stream, KC_SPMV);
+  if (use_wpr) {                                                  // long / uneven rows: a warp per row
+    const int grid = grid_for((n + 7) / 8, 8);
+    if (hA.nrecv > 0)
+      launch_pdl(k_spmv_wpr<D, true>, dim3(grid), dim3(256), 0, ctx->stream, n, csr_ptr, csr_col, csr_val, x, hA.rbuf, y,
+                 mode, b, doneflag);
+    else
+      launch_pdl(k_spmv_wpr<D, false>, dim3(grid), dim3(256), 0, ctx->stream, n, csr_ptr, csr_col, csr_val, x, hA.rbuf, y,
+                 mode, b, doneflag);
+    CK(cudaGetLastError());
+    return;
+  }
   if (sell_wmax <= 8) {                                           // 7-point / 5-point stencils and similar
     constexpr int SPW = 2;
     const int g2 = (int)std::max<int64_t>((nslices + 8 * SPW - 1) / (8 * SPW), 1);
     if (hA.nrecv > 0)
       launch_pdl(k_spmv_sell2<D, true, SPW, 8>, dim3(g2), dim3(256), 0, ctx->stream, n, nslices, sell_off, sell_col,
-                 sell_val, x, hA.rbuf, y, mode, b, doneflag);
+                 sell_val, x, hA.rbuf, y, mode, b, doneflag, (const int *)nullptr);
     else
       launch_pdl(k_spmv_sell2<D, false, SPW, 8>, dim3(g2), dim3(256), 0, ctx->stream, n, nslices, sell_off, sell_col,
-                 sell_val, x, hA.rbuf, y, mode, b, doneflag);
+                 sell_val, x, hA.rbuf, y, mode, b, doneflag, (const int *)nullptr);
     CK(cudaGetLastError());
     return;
   }
@@ -1077,7 +1187,7 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     launch_trisolve(ctx, d.st, TRI_DOWN, in, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, 0);   // z1
     {
       Timed t(ctx->prof, s, KC_EW);                              // z2 = b2 - E_0 z1 -> r[J_0]
-      launch_ew<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, out, hE[0].rbuf, n, in, r, d.W, d.ldw, 0, partial,
+      launch_ew<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, out, hE[0].rbuf, (int64_t)kHaloE, in, r, d.W, d.ldw, 0, partial,
                    tickets + 0, tvec, doneflag);
     }
     root_gmres(r + d.o1, out + d.o1, doneflag);                   // y2 ≈ Ŝ_0^-1 z2
@@ -1095,14 +1205,15 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     LevelDev<D> &d = lev[l];
     const D *src = (l == l0) ? in : r;
     // z1 = U_l^-1 L_l^-1 b1  -> out[I_l] (xpm: U-packed in d.st.xU, read by E_l and the UP)
-    const bool xpm = !dist && d.Ecol_p != nullptr;
+    const bool xpm = d.Ecol_p != nullptr;
     launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, l, 1, 0, xpm, packed);
     packed = false;
     const D *zsrc = xpm ? (const D *)d.st.xU : (const D *)out;
     const int32_t *ecol = xpm ? d.Ecol_p : d.E.col;
-    const int64_t znloc = xpm ? INT64_MAX : n;                     // packed positions may exceed n: no halo part
+    const int64_t znloc = kHaloE;                                  // E's halo columns start there (U-packed ones may exceed n)
     if (d.s > 0 || dist) {
-      exchange(hE[l], out, doneflag);                              // z1 entries of E_l's exterior columns
+      if (xpm) exchange(hE[l], d.st.xU, doneflag, nullptr, d.esidx_p);   // z1 entries of E_l's exterior columns
+      else exchange(hE[l], out, doneflag);
       if (!dist && d.k > 0) {                                      // one cooperative launch: K6 + K7 + K8
         Timed t(ctx->prof, s, KC_EW);
         StageDev<D> &nst = (l + 1 < L) ? lev[l + 1].st : last;
@@ -1124,7 +1235,10 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
         }
         Timed t(ctx->prof, s, KC_WAXPY);
         const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 8);
-        k_waxpy<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.W, d.ldw, d.k, d.G, tvec, r, doneflag);
+        StageDev<D> &nst = (l + 1 < L) ? lev[l + 1].st : last;
+        k_waxpy<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.W, d.ldw, d.k, d.G, tvec, r, doneflag, d.npk, d.pkpos,
+                                        const_cast<D *>(nst.Rg.rhsL));
+        packed = d.npk > 0;
         CK(cudaGetLastError());
       }
     }
@@ -1156,7 +1270,7 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     fa.nh = hF[l].nrecv;
     fa.yl = yl_full;
     launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP, l, 1, 0,
-                    !dist && d.Ecol_p != nullptr);
+                    d.Ecol_p != nullptr);
   }
 }
 
@@ -1200,11 +1314,11 @@ void Engine<T>::ew_column(LevelDev<D> &d, int l, const D *src, const D *z, D *ds
   cudaStream_t s = ctx->stream;
   Timed t(ctx->prof, s, KC_EW);
   if (d.k > 0) {
-    launch_ewx<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, z, hE[l].rbuf, n, src, dst, d.W, d.ldw, d.k, d.G, partial,
+    launch_ewx<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, z, hE[l].rbuf, (int64_t)kHaloE, src, dst, d.W, d.ldw, d.k, d.G, partial,
                   tickets + 0, tvec, ewflag, doneflag, 0, nullptr, nullptr);   // no next-stage packing here
     return;
   }
-  launch_ew<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, z, hE[l].rbuf, n, src, dst, d.W, d.ldw, 0, partial, tickets + 0,
+  launch_ew<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, z, hE[l].rbuf, (int64_t)kHaloE, src, dst, d.W, d.ldw, 0, partial, tickets + 0,
                tvec, doneflag);
 }
 
@@ -1335,7 +1449,7 @@ void Engine<T>::ghat(int l, D *bufA, D *bufB) {
   launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, bufB, tmp, fa, nullptr, KC_TRI_UP);
   // bufB[J_l] = 0 - E_l (-u) = E_l u   (K6+K7 with k = 0, src = 0)
   exchange(hE[l], bufB, nullptr);
-  launch_ew<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, bufB, hE[l].rbuf, n, (const D *)nullptr, bufB,
+  launch_ew<D>(s, d.s, d.o1, d.E.ptr, d.E.col, d.E.val, bufB, hE[l].rbuf, (int64_t)kHaloE, (const D *)nullptr, bufB,
                (const D *)nullptr, 0, 0, partial, tickets + 1, tvec, nullptr);
 }
 
@@ -2027,6 +2141,7 @@ std::string Engine<T>::stats_json() const {
   j += "], \"fill\": " + std::to_string((double)plan.fac_nnz / std::max<int64_t>(1, plan.Ahat.nnz()));
   j += ", \"fac_nnz\": " + std::to_string(plan.fac_nnz);
   j += ", \"sell_padded\": " + std::to_string(sell_padded);
+  j += std::string(", \"spmv_kernel\": \"") + (use_wpr ? "wpr" : (sell_wmax <= 8 ? "sell2" : "sell")) + "\"";
   auto stage = [&](const StageDev<D> &S) {
     return "{\"blocks\": " + std::to_string(S.nblk) + ", \"rows\": " + std::to_string(S.rows) + ", \"cps\": " +
            std::to_string(S.cps) + ", \"depth_L\": " + std::to_string(S.depthL) + ", \"depth_U\": " +

@@ -132,11 +132,15 @@ __global__ void __launch_bounds__(256) k_spmv_sell(int64_t n, int64_t nslices, c
 // of width <= WM, issues all their column and value loads, then all x gathers
 // (the gathers depend on the columns, so batching both levels is what hides
 // the latency; one slice per warp left the kernel at 57 % of HBM).
+// slist != nullptr: the warp's slices are slist[s0 + q] of a list of nslices
+// entries (the interior / boundary slices of a distributed SpMV, whose halo
+// exchange overlaps the interior part).
 template <typename T, bool HALO, int SPW, int WM>
 __global__ void __launch_bounds__(256) k_spmv_sell2(int64_t n, int64_t nslices, const int64_t *__restrict__ off,
                                                     const int32_t *__restrict__ col, const T *__restrict__ val,
                                                     const T *__restrict__ x, const T *__restrict__ xh, T *__restrict__ y,
-                                                    int mode, const T *__restrict__ b, const int *__restrict__ done) {
+                                                    int mode, const T *__restrict__ b, const int *__restrict__ done,
+                                                    const int *__restrict__ slist = nullptr) {
   pdl_launch();
   pdl_wait();
   if (done && *done) return;
@@ -145,11 +149,14 @@ __global__ void __launch_bounds__(256) k_spmv_sell2(int64_t n, int64_t nslices, 
   const int lane = threadIdx.x & 31;
   int c[SPW][WM];
   T v[SPW][WM];
+  int64_t sid[SPW];
+#pragma unroll
+  for (int q = 0; q < SPW; ++q) sid[q] = s0 + q < nslices ? (slist ? (int64_t)slist[s0 + q] : s0 + q) : -1;
 #pragma unroll
   for (int q = 0; q < SPW; ++q) {
-    const int64_t s = s0 + q;
-    const int64_t o = s < nslices ? off[s] : 0;
-    const int w = s < nslices ? (int)((off[s + 1] - o) >> 5) : 0;
+    const int64_t s = sid[q];
+    const int64_t o = s >= 0 ? off[s] : 0;
+    const int w = s >= 0 ? (int)((off[s + 1] - o) >> 5) : 0;
 #pragma unroll
     for (int e = 0; e < WM; ++e) {
       c[q][e] = e < w ? __ldg(col + o + 32 * e + lane) : -1;
@@ -169,8 +176,34 @@ __global__ void __launch_bounds__(256) k_spmv_sell2(int64_t n, int64_t nslices, 
     T acc = dzero<T>();
 #pragma unroll
     for (int e = 0; e < WM; ++e) acc += v[q][e] * xv[q][e];
-    const int64_t row = (s0 + q) * 32 + lane;
-    if (row < n) y[row] = mode ? b[row] - acc : acc;
+    const int64_t row = sid[q] * 32 + lane;
+    if (sid[q] >= 0 && row < n) y[row] = mode ? b[row] - acc : acc;
+  }
+}
+
+// Warp per row (CSR) for matrices whose rows are long or very uneven (north_star:
+// "warp-per-row or row-block variants picked by nnz/row"): lanes stride over a
+// row's entries (coalesced column / value loads), a warp sum gives y_i.  SELL-32
+// (one row per lane) would pad every lane of a slice to its longest row.
+template <typename T, bool HALO>
+__global__ void __launch_bounds__(256) k_spmv_wpr(int64_t n, const int64_t *__restrict__ ptr, const int32_t *__restrict__ col,
+                                                  const T *__restrict__ val, const T *__restrict__ x,
+                                                  const T *__restrict__ xh, T *__restrict__ y, int mode,
+                                                  const T *__restrict__ b, const int *__restrict__ done) {
+  pdl_launch();
+  pdl_wait();
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n; row += nw) {
+    T acc = dzero<T>();
+    const int64_t p1 = ptr[row + 1];
+    for (int64_t p = ptr[row] + lane; p < p1; p += 32) {
+      const int32_t c = __ldg(col + p);
+      acc += ld_nc(val + p) * ((!HALO || c < n) ? ld_nc(x + c) : ld_nc(xh + (c - n)));
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) y[row] = mode ? b[row] - acc : acc;
   }
 }
 
@@ -596,6 +629,31 @@ __global__ void __launch_bounds__(32 * (PIPE_NW_DEV + 1), 1) k_tri_pipe(PipeDev<
   }
   if (mode == TRI_UP)
     for (int64_t i = r0 + tid; i < r1; i += NCONS) x[i] = x[i] - tmp[i];   // y1 = z1 - U^-1 L^-1 F y2
+}
+
+// sum_p val[p] * g(col[p]) over p in [p0, p1) in p order (the plain loop's rounding);
+// the column/value loads of 8 entries, then their 8 gathers, are issued together, so
+// a short row costs two dependent round trips instead of two per entry.
+template <typename T, typename Gather>
+__device__ inline T csr_dot(int64_t p0, int64_t p1, const int32_t *__restrict__ col, const T *__restrict__ val,
+                            Gather g) {
+  T acc = dzero<T>();
+  for (int64_t q = p0; q < p1; q += 8) {
+    int64_t c[8];
+    T v[8], x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool ok = q + u < p1;
+      c[u] = ok ? (int64_t)col[q + u] : -1;
+      v[u] = ok ? val[q + u] : dzero<T>();
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = c[u] >= 0 ? g(c[u]) : dzero<T>();
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (q + u < p1) acc += v[u] * x[u];
+  }
+  return acc;
 }
 
 // ----------------------------------------------------------------- K4/K5/K9 register-prefetched
@@ -1051,31 +1109,6 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
   if constexpr (SPLIT) cluster_sync_all();                         // no CTA leaves while a neighbour may still write
 }
 
-// sum_p val[p] * g(col[p]) over p in [p0, p1) in p order (the plain loop's rounding);
-// the column/value loads of 8 entries, then their 8 gathers, are issued together, so
-// a short row costs two dependent round trips instead of two per entry.
-template <typename T, typename Gather>
-__device__ inline T csr_dot(int64_t p0, int64_t p1, const int32_t *__restrict__ col, const T *__restrict__ val,
-                            Gather g) {
-  T acc = dzero<T>();
-  for (int64_t q = p0; q < p1; q += 8) {
-    int64_t c[8];
-    T v[8], x[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const bool ok = q + u < p1;
-      c[u] = ok ? (int64_t)col[q + u] : -1;
-      v[u] = ok ? val[q + u] : dzero<T>();
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = c[u] >= 0 ? g(c[u]) : dzero<T>();
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (q + u < p1) acc += v[u] * x[u];
-  }
-  return acc;
-}
-
 // Right-hand sides of k_tri_reg's L sweep in packed order (index = slice·32 + lane).
 // DOWN: gather form dst[p] = src[lrow[p]] — coalesced writes, the reads hit L2
 // (the input vector was just written).  UP: only the rows with F_l entries,
@@ -1255,6 +1288,9 @@ __global__ void __launch_bounds__(256) k_ew(int64_t s, int64_t rowbase, const in
 // The flag is a generation counter in device memory: every CTA reads it before
 // taking its ticket, the last CTA (which takes the final ticket, so after every
 // read) advances it — no host-side epoch, so the launch can live in a CUDA graph.
+#ifndef EW_UNROLL_WT
+#define EW_UNROLL_WT 0
+#endif
 template <typename T, int NACC>
 __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const int64_t *__restrict__ Eptr,
                                              const int32_t *__restrict__ Ecol, const T *__restrict__ Eval,
@@ -1321,7 +1357,9 @@ __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const i
     __syncthreads();
     if (tid < k) {                                                 // t = G s
       T t = dzero<T>();
-      for (int a = 0; a < k; ++a) t += G[(int64_t)a * k + tid] * ld_cg(sout + a);
+#pragma unroll
+      for (int a = 0; a < 8 * NACC; ++a)                           // all loads in flight (a loop over k was
+        if (a < k) t += G[(int64_t)a * k + tid] * ld_cg(sout + a); // k dependent L2 round trips)
       sout[64 + tid] = t;
     }
     __threadfence();
@@ -1345,7 +1383,13 @@ __global__ void __launch_bounds__(256) k_ewx(int64_t s, int64_t rowbase, const i
     const int64_t i = tile * 256 + tid;
     if (i < s) {
       T a = dzero<T>();
+#if EW_UNROLL_WT
+#pragma unroll
+      for (int c = 0; c < 8 * NACC; ++c)
+        if (c < k) a += ld_nc(W + c * ldw + i) * st[c];
+#else
       for (int c = 0; c < k; ++c) a += ld_nc(W + c * ldw + i) * st[c];
+#endif
       const T v = ld_cg(dst + rowbase + i) + a;
       dst[rowbase + i] = v;
       if (i < npk) pk[pkpos[i]] = v;                               // the next stage's packed right-hand side
@@ -1434,13 +1478,17 @@ __global__ void __launch_bounds__(256) k_ewc(int64_t s, int64_t rowbase, const i
   __syncthreads();
   if (tid < k) {                                                   // t = G s
     T t = dzero<T>();
-    for (int a = 0; a < k; ++a) t += G[(int64_t)a * k + tid] * sv[a];
+#pragma unroll
+    for (int a = 0; a < 8 * NACC; ++a)                             // all loads in flight
+      if (a < k) t += G[(int64_t)a * k + tid] * sv[a];
     st[tid] = t;
   }
   __syncthreads();
   for (int64_t i = r0 + tid; i < r1; i += 256) {                  // r_J += W t
     T a = dzero<T>();
-    for (int cc = 0; cc < k; ++cc) a += ld_nc(W + cc * ldw + i) * st[cc];
+#pragma unroll
+    for (int cc = 0; cc < 8 * NACC; ++cc)
+      if (cc < k) a += ld_nc(W + cc * ldw + i) * st[cc];
     const T v = dst[rowbase + i] + a;
     dst[rowbase + i] = v;
     if (i < npk) pk[pkpos[i]] = v;                                 // the next stage's packed right-hand side
@@ -1454,21 +1502,26 @@ __global__ void __launch_bounds__(256) k_ewc(int64_t s, int64_t rowbase, const i
 template <typename T>
 __global__ void __launch_bounds__(256) k_waxpy(int64_t s, int64_t rowbase, const T *__restrict__ W, int64_t ldw, int k,
                                                const T *__restrict__ G, const T *__restrict__ sv, T *dst,
-                                               const int *__restrict__ done) {
+                                               const int *__restrict__ done, int64_t npk = 0,
+                                               const int *__restrict__ pkpos = nullptr, T *__restrict__ pk = nullptr) {
   if (done && *done) return;
   __shared__ T ss[64], st[64];
   if (threadIdx.x < k) ss[threadIdx.x] = sv[threadIdx.x];
   __syncthreads();
   if (threadIdx.x < k) {
     T t = dzero<T>();
+#pragma unroll 8
     for (int a = 0; a < k; ++a) t += G[(int64_t)a * k + threadIdx.x] * ss[a];
     st[threadIdx.x] = t;
   }
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
     T acc = dzero<T>();
+#pragma unroll 8
     for (int c = 0; c < k; ++c) acc += ld_nc(W + c * ldw + i) * st[c];
-    dst[rowbase + i] += acc;
+    const T v = dst[rowbase + i] + acc;
+    dst[rowbase + i] = v;
+    if (i < npk) pk[pkpos[i]] = v;                                 // the next stage's packed right-hand side
   }
 }
 
@@ -1995,7 +2048,28 @@ __global__ void __launch_bounds__(256) k_fgmres_scale(FgmDev<T> f, int m, int j,
   if constexpr (sizeof(T) == sizeof(double)) hn2 = res3[0]; else hn2 = res3[0].x;
   const double hnext = sqrt(hn2 > 0 ? hn2 : 0.0);
   const double sc = hnext > 0 ? 1.0 / hnext : 0.0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) fgmres_col_body(f, m, j, res1, res2, res3);
+  if (blockIdx.x == 0) {
+    // The Givens column on one thread, its inputs staged by the first warp (one
+    // round trip for all; a thread walking them read them one L2 latency at a time)
+    __shared__ T r1[GS_MAXC + 2], r2[GS_MAXC + 2], hcol[GS_MAXC + 2], sns[GS_MAXC];
+    __shared__ double css[GS_MAXC];
+    if (threadIdx.x < 32) {
+      for (int i = threadIdx.x; i <= j + 1; i += 32) { r1[i] = res1[i]; r2[i] = res2[i]; }
+      for (int i = threadIdx.x; i < j; i += 32) { css[i] = f.cs[i]; sns[i] = f.sn[i]; }
+      __syncwarp();
+      if (threadIdx.x == 0) {
+        FgmDev<T> fs = f;
+        fs.cs = css;
+        fs.sn = sns;
+        fs.H = hcol - (int64_t)j * (m + 1);                         // column j lands in hcol
+        fgmres_col_body(fs, m, j, r1, r2, res3);
+      }
+      __syncwarp();
+      T *Hj = f.H + (int64_t)j * (m + 1);
+      for (int i = threadIdx.x; i <= j + 1; i += 32) Hj[i] = hcol[i];
+      if (threadIdx.x == 0) { f.cs[j] = css[j]; f.sn[j] = sns[j]; }
+    }
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     vnext[i] = dscale(w[i], sc);
 }

@@ -435,3 +435,35 @@ def test_split_trisolve(tmp_path, name, dims, over, split):
     Y = s.apply_precond_multi(X).cpu().numpy()
     for c in range(3):
         assert rel(Y[c], Pc.apply(cols[c])) <= TOL
+
+
+@pytest.mark.parametrize("kind", ["long_rows", "forced_stencil"])
+def test_warp_per_row_spmv(tmp_path, kind, monkeypatch):
+    """Warp-per-row CSR SpMV (k_spmv_wpr), chosen for long rows (>= 32 entries on average)
+    or heavy SELL padding: SpMV and apply parity with the oracle, and an FGMRES solve."""
+    import scipy.sparse as sp
+    if kind == "long_rows":
+        n = 3000
+        M = sp.random(n, n, density=48.0 / n, random_state=7, format="csr")
+        M = sp.csr_matrix(M + M.T + sp.identity(n) * 60.0)
+        M.sort_indices()
+        prob = P.Problem("long", (n,), M.indptr.astype(np.int64), M.indices.astype(np.int32), M.data, np.zeros((n, 3)))
+        prm = dict(levels=2, subdomains=4, rank=4, ilu="ilut", ilut_drop=1e-3, ilut_fill=10)
+        coords = False
+    else:                                                          # the stencil with the kernel forced
+        monkeypatch.setenv("GEMSLR_SPMV", "wpr")
+        prob, b0, xt, prm = P.make_config("C3", dims=(20, 18, 16), subdomains=8, rank=6)
+        coords = True
+    s, B, st, Pc = make_pair(prob, prm, tmp_path, coords=coords)
+    assert s.stats()["spmv_kernel"] == "wpr"
+    perm = st["perm"]
+    x = P.rhs_vector(prob.n, prob.is_complex, 4)
+    y = s.spmv(to_dev(s, x[perm])).cpu().numpy()
+    yn = np.empty_like(y)
+    yn[perm] = y
+    assert rel(yn, oracle.spmv(prob, x)) <= TOL
+    assert rel(s.apply_precond(to_dev(s, x)).cpu().numpy(), Pc.apply(x)) <= TOL
+    b = P.rhs_vector(prob.n, prob.is_complex, 9)
+    out = s.solve(to_dev(s, b[perm]), rtol=1e-8, restart=30, maxit=500)
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=1e-8, restart=30, maxit=500)
+    assert out["status"] == ref["status"] == 0 and abs(out["its"] - ref["its"]) <= 1
