@@ -758,7 +758,8 @@ void Engine<T>::upload(cudaStream_t s) {
       std::vector<int32_t> pos(npk);
       bool ok = true;
       for (int64_t i = 0; i < npk && ok; ++i) {
-        const int64_t row = d.o1 + i - R0n;
+        // (the last stage numbers its rows from o_L: make_stage's relative bounds)
+        const int64_t row = d.o1 + i - (l + 1 < L ? R0n : plan.lo[L] + R0n);
         if (row < 0 || row >= (int64_t)NS.reg.lpos.size() || NS.reg.lpos[row] < 0) ok = false;
         else pos[i] = NS.reg.lpos[row];
       }
@@ -922,12 +923,15 @@ static void launch_ewx(cudaStream_t st, int64_t s, int64_t rowbase, const int64_
                        const D *Eval, const D *z, const D *zh, int64_t nloc, const D *src, D *dst, const D *W,
                        int64_t ldw, int k, const D *G, D *partial, unsigned *ticket, D *sout, int *flag,
                        const int *done, int64_t npk, const int *pkpos, D *pk) {
-  static const int small_max = getenv("GEMSLR_EWC_MAX") ? atoi(getenv("GEMSLR_EWC_MAX")) : 16384;
-  if (s <= small_max) {                                            // small interface: one cluster (k_ewc)
-    const int C = (int)std::max<int64_t>(1, std::min<int64_t>(8, (s + 255) / 256));
+  // small interface (<= 8 CTAs of one row per thread, k <= 32): one cluster (k_ewc)
+  static const int small_max = getenv("GEMSLR_EWC_MAX") ? atoi(getenv("GEMSLR_EWC_MAX")) : 2048;
+  if (s <= std::min(small_max, 8 * 256) && k <= 32) {
+    const int C = (int)std::max<int64_t>(1, (s + 255) / 256);
     with_nacc(k, [&](auto nc) {
-      launch_pdl_cluster(k_ewc<D, decltype(nc)::value>, dim3(C), dim3(256), 0, st, C, s, rowbase, Eptr, Ecol, Eval, z, zh,
-                         nloc, src, dst, W, ldw, k, G, done, npk, pkpos, pk);
+      constexpr int NA = decltype(nc)::value;
+      if constexpr (NA <= 4)
+        launch_pdl_cluster(k_ewc<D, NA>, dim3(C), dim3(256), 0, st, C, s, rowbase, Eptr, Ecol, Eval, z, zh, nloc, src, dst,
+                           W, ldw, k, G, done, npk, pkpos, pk);
     });
     return;
   }

@@ -1118,14 +1118,27 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_pack_gather(int64_t np, const int *__restrict__ lrow, const T *__restrict__ src,
                                                      T *__restrict__ dst, const int *__restrict__ done,
                                                      int64_t lds = 0, int64_t ldd = 0) {
+  // the packing map (setup data) is loaded before griddepcontrol.wait, while the
+  // predecessor runs; after it only the gathers (PG positions per thread in flight)
+  constexpr int PG = 16;
   pdl_launch();
-  pdl_wait();
-  if (done && *done) return;
   src += (size_t)blockIdx.y * lds;                                 // column blockIdx.y (several right-hand sides)
   dst += (size_t)blockIdx.y * ldd;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x) {
-    const int r = lrow[p];
-    dst[p] = r >= 0 ? src[r] : dzero<T>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int r[PG];
+#pragma unroll
+  for (int u = 0; u < PG; ++u) r[u] = p0 + u * stride < np ? lrow[p0 + u * stride] : -1;
+  pdl_wait();
+  if (done && *done) return;
+  T v[PG];
+#pragma unroll
+  for (int u = 0; u < PG; ++u) v[u] = r[u] >= 0 ? src[r[u]] : dzero<T>();
+#pragma unroll
+  for (int u = 0; u < PG; ++u)
+    if (p0 + u * stride < np) dst[p0 + u * stride] = v[u];
+  for (int64_t p = p0 + PG * stride; p < np; p += stride) {        // (more than PG per thread)
+    const int rr = lrow[p];
+    dst[p] = rr >= 0 ? src[rr] : dzero<T>();
   }
 }
 template <typename T>
@@ -1136,23 +1149,45 @@ __global__ void __launch_bounds__(256) k_pack_f(int64_t nf, const int *__restric
                                                 T *__restrict__ dst, const int *__restrict__ done, int64_t ldy = 0,
                                                 int64_t ldd = 0, int64_t npu = 0, const int *__restrict__ urow = nullptr,
                                                 T *__restrict__ xu = nullptr) {
+  // F_l's structure for this thread's first row (setup data) is loaded before
+  // griddepcontrol.wait; after it only the y gathers
+  constexpr int EM = 8;
   pdl_launch();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool have = i0 < nf;
+  const int pos0 = have ? fpos[i0] : 0, li0 = have ? frow[i0] : 0;
+  const int64_t q0 = have ? Fptr[li0] : 0, q1 = have ? Fptr[li0 + 1] : 0;
+  int32_t fc[EM];
+  T fv[EM];
+#pragma unroll
+  for (int u = 0; u < EM; ++u) {
+    fc[u] = q0 + u < q1 ? Fcol[q0 + u] : 0;
+    fv[u] = q0 + u < q1 ? Fval[q0 + u] : dzero<T>();
+  }
   pdl_wait();
   if (done && *done) return;
   y += (size_t)blockIdx.y * ldy;                                   // column blockIdx.y (one GPU: no halo / yl)
   dst += (size_t)blockIdx.y * ldd;
   // the level's current values x[rows] in U-packed order (k_tri_reg UP writes
   // x[row] = xu - U^-1 L^-1 F y in place; one column)
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npu; p += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t p = i0; p < npu; p += stride) {
     const int r = urow[p];
     xu[p] = r >= 0 ? y[r] : dzero<T>();
   }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += (int64_t)gridDim.x * blockDim.x) {
+  auto g = [&](int64_t c) { return c < nloc ? y[c] : (c < nloc + nh ? yh[c - nloc] : yl[c - nloc - nh]); };
+  if (have) {                                                      // the same p order as csr_dot
+    T xg[EM], v = dzero<T>();
+#pragma unroll
+    for (int u = 0; u < EM; ++u) xg[u] = q0 + u < q1 ? g(fc[u]) : dzero<T>();
+#pragma unroll
+    for (int u = 0; u < EM; ++u)
+      if (q0 + u < q1) v += fv[u] * xg[u];
+    if (q1 - q0 > EM) v += csr_dot(q0 + EM, q1, Fcol, Fval, g);  // (long rows: the rest, in order)
+    dst[pos0] = v;
+  }
+  for (int64_t i = i0 + stride; i < nf; i += stride) {
     const int li = frow[i];
-    const T v = csr_dot(Fptr[li], Fptr[li + 1], Fcol, Fval, [&](int64_t c) {
-      return c < nloc ? y[c] : (c < nloc + nh ? yh[c - nloc] : yl[c - nloc - nh]);
-    });
-    dst[fpos[i]] = v;
+    dst[fpos[i]] = csr_dot(Fptr[li], Fptr[li + 1], Fcol, Fval, g);
   }
 }
 
@@ -1422,50 +1457,60 @@ __global__ void __launch_bounds__(256) k_ewc(int64_t s, int64_t rowbase, const i
                                              const T *src, T *dst, const T *__restrict__ W, int64_t ldw, int k,
                                              const T *__restrict__ G, const int *__restrict__ done, int64_t npk = 0,
                                              const int *__restrict__ pkpos = nullptr, T *__restrict__ pk = nullptr) {
+  // One row per thread (s <= 256 C).  Everything that is setup data — the row's E
+  // entries, its W row, G, its packed position — is loaded BEFORE griddepcontrol.wait,
+  // while the predecessor still runs; after it only the z gathers and src remain,
+  // then two cluster barriers.  (A tile loop with the loads after the wait made this
+  // a chain of ~10 dependent memory round trips: 15-28 us for 667 / 4.6k rows.)
+  constexpr int KM = 8 * NACC, EM = 8;
   pdl_launch();
-  pdl_wait();
-  if (done && *done) return;                                       // uniform over the cluster (predecessor complete)
-  __shared__ T sv[256];
-  __shared__ T wpart[8][8 * NACC];
-  __shared__ T cpart[8 * NACC];
-  __shared__ T st[8 * NACC];
+  __shared__ T Gs[KM * KM];
+  __shared__ T wpart[8][KM];
+  __shared__ T cpart[KM];
+  __shared__ T sv[KM], st[KM];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned C = gridDim.x, c = blockIdx.x;
   const int64_t r0 = s * c / C, r1 = s * (c + 1) / C;
-  T acc[NACC];
+  const int64_t i = r0 + tid;
+  const bool own = i < r1;
+  const int64_t p0 = own ? Eptr[i] : 0, p1 = own ? Eptr[i + 1] : 0;
+  int32_t ec[EM];
+  T ev[EM], wr[KM];
 #pragma unroll
-  for (int a = 0; a < NACC; ++a) acc[a] = dzero<T>();
-  for (int64_t t0 = r0; t0 < r1; t0 += 256) {
-    const int64_t i = t0 + tid;
-    T v = dzero<T>();
-    if (i < r1) {
-      const T e = csr_dot(Eptr[i], Eptr[i + 1], Ecol, Eval, [&](int64_t cc) { return cc < nloc ? z[cc] : zh[cc - nloc]; });
-      v = (src ? src[rowbase + i] : dzero<T>()) - e;
-      dst[rowbase + i] = v;
-    }
-    sv[tid] = v;
-    __syncthreads();
-#pragma unroll
-    for (int a = 0; a < NACC; ++a) {
-      const int cc = warp + 8 * a;
-      if (cc < k) {
-#pragma unroll
-        for (int rr = 0; rr < 8; ++rr) {
-          const int64_t ii = t0 + rr * 32 + lane;
-          if (ii < r1) acc[a] += dconj(W[cc * ldw + ii]) * sv[rr * 32 + lane];
-        }
-      }
-    }
-    __syncthreads();
+  for (int u = 0; u < EM; ++u) {
+    ec[u] = p0 + u < p1 ? Ecol[p0 + u] : 0;
+    ev[u] = p0 + u < p1 ? Eval[p0 + u] : dzero<T>();
   }
 #pragma unroll
-  for (int a = 0; a < NACC; ++a) {
-    const T r = warp_sum(acc[a]);
-    if (lane == 0) wpart[warp][a] = r;                               // column warp + 8 a
+  for (int cc = 0; cc < KM; ++cc) wr[cc] = (own && cc < k) ? ld_nc(W + cc * ldw + i) : dzero<T>();
+  for (int q = tid; q < k * k; q += blockDim.x) Gs[q] = G[q];
+  const int ppk = (own && i < npk) ? pkpos[i] : -1;
+  pdl_wait();
+  if (done && *done) return;                                       // uniform over the cluster (predecessor complete)
+  T v = dzero<T>();
+  if (own) {
+    auto g = [&](int64_t cc) { return cc < nloc ? z[cc] : zh[cc - nloc]; };
+    T e = dzero<T>(), xg[EM];
+#pragma unroll
+    for (int u = 0; u < EM; ++u) xg[u] = p0 + u < p1 ? g(ec[u]) : dzero<T>();
+#pragma unroll
+    for (int u = 0; u < EM; ++u)
+      if (p0 + u < p1) e += ev[u] * xg[u];
+    for (int64_t p = p0 + EM; p < p1; ++p) e += Eval[p] * g(Ecol[p]);   // rows with more entries (rare)
+    v = (src ? src[rowbase + i] : dzero<T>()) - e;
+  }
+#pragma unroll
+  for (int cc = 0; cc < KM; ++cc) {                                // this CTA's part of W^H r_J
+    if (cc < k) {
+      const T r = warp_sum(dconj(wr[cc]) * v);
+      if (lane == 0) wpart[warp][cc] = r;
+    }
   }
   __syncthreads();
-  if (tid < k) {                                                   // this CTA's partial of column tid
-    const T r = wpart[tid % 8][tid / 8];
+  if (tid < k) {
+    T r = dzero<T>();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r += wpart[q][tid];
     cpart[tid] = r;
   }
   cluster_sync_all();
@@ -1478,20 +1523,18 @@ __global__ void __launch_bounds__(256) k_ewc(int64_t s, int64_t rowbase, const i
   __syncthreads();
   if (tid < k) {                                                   // t = G s
     T t = dzero<T>();
-#pragma unroll
-    for (int a = 0; a < 8 * NACC; ++a)                             // all loads in flight
-      if (a < k) t += G[(int64_t)a * k + tid] * sv[a];
+    for (int a = 0; a < k; ++a) t += Gs[a * k + tid] * sv[a];
     st[tid] = t;
   }
   __syncthreads();
-  for (int64_t i = r0 + tid; i < r1; i += 256) {                  // r_J += W t
+  if (own) {                                                       // r_J += W t
     T a = dzero<T>();
 #pragma unroll
-    for (int cc = 0; cc < 8 * NACC; ++cc)
-      if (cc < k) a += ld_nc(W + cc * ldw + i) * st[cc];
-    const T v = dst[rowbase + i] + a;
-    dst[rowbase + i] = v;
-    if (i < npk) pk[pkpos[i]] = v;                                 // the next stage's packed right-hand side
+    for (int cc = 0; cc < KM; ++cc)
+      if (cc < k) a += wr[cc] * st[cc];
+    const T v2 = v + a;
+    dst[rowbase + i] = v2;
+    if (ppk >= 0) pk[ppk] = v2;                                    // the next stage's packed right-hand side
   }
   cluster_sync_all();                                              // partials read by every CTA before any exits
 }
