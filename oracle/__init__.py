@@ -144,9 +144,12 @@ class Ilu:
         return x
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().or_ilu_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().or_ilu_destroy(self.h)
+                self.h = None
+        except Exception:                                          # interpreter shutdown
+            pass
 
 
 class Precond:
@@ -237,9 +240,12 @@ class Precond:
         return C.cast(lib().or_precond_natural, C.c_void_p), C.c_void_p(self.h)
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().or_precond_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().or_precond_destroy(self.h)
+                self.h = None
+        except Exception:                                          # interpreter shutdown
+            pass
 
 
 _PRECOND_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)

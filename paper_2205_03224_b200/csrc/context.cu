@@ -389,6 +389,7 @@ struct Engine {
   D *r = nullptr, *tmp = nullptr, *tvec = nullptr, *partial = nullptr, *res = nullptr;
   unsigned *tickets = nullptr;
   int *ewflag = nullptr;             // k_ewx generation counter (device-side)
+  unsigned *gtickets = nullptr;      // k_ewg grid-barrier ticket counters, one per level (apply_from)
   size_t partial_cap = 0;
   // Krylov workspace (lazy)
   int kry_m = -1;
@@ -783,6 +784,8 @@ void Engine<T>::upload(cudaStream_t s) {
   tickets = P.get<unsigned>(16);
   ewflag = P.get<int>(1);
   CK(cudaMemsetAsync(ewflag, 0, sizeof(int), s));
+  gtickets = P.get<unsigned>(std::max(L, 1));
+  CK(cudaMemsetAsync(gtickets, 0, std::max(L, 1) * sizeof(unsigned), s));
   CK(cudaMemsetAsync(tickets, 0, 16 * sizeof(unsigned), s));
   CK(cudaMemsetAsync(r, 0, (n + 1) * sizeof(D), s));
   CK(cudaMemsetAsync(tmp, 0, (n + 1) * sizeof(D), s));
@@ -922,7 +925,7 @@ template <typename D>
 static void launch_ewx(cudaStream_t st, int64_t s, int64_t rowbase, const int64_t *Eptr, const int32_t *Ecol,
                        const D *Eval, const D *z, const D *zh, int64_t nloc, const D *src, D *dst, const D *W,
                        int64_t ldw, int k, const D *G, D *partial, unsigned *ticket, D *sout, int *flag,
-                       const int *done, int64_t npk, const int *pkpos, D *pk) {
+                       const int *done, int64_t npk, const int *pkpos, D *pk, unsigned *gticket = nullptr) {
   // small interface (<= 8 CTAs of one row per thread, k <= 32): one cluster (k_ewc)
   static const int small_max = getenv("GEMSLR_EWC_MAX") ? atoi(getenv("GEMSLR_EWC_MAX")) : 2048;
   if (s <= std::min(small_max, 8 * 256) && k <= 32) {
@@ -934,6 +937,33 @@ static void launch_ewx(cudaStream_t st, int64_t s, int64_t rowbase, const int64_
                            W, ldw, k, G, done, npk, pkpos, pk);
     });
     return;
+  }
+  // large interface with a grid that fits the SMs: the PDL / grid-barrier form (k_ewg)
+  static const bool no_ewg = getenv("GEMSLR_NO_EWG") != nullptr;
+  if (gticket && k <= 32 && !no_ewg) {
+    bool launched = false;
+    with_nacc(k, [&](auto nc) {
+      constexpr int NA = decltype(nc)::value;
+      if constexpr (NA <= 4) {
+        auto kern = k_ewg<D, NA>;
+        static int cap[64] = {0};                                  // co-resident CTAs per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        dev = (dev >= 0 && dev < 64) ? dev : 0;
+        if (cap[dev] == 0) {
+          int per = 0;
+          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, 0));
+          cap[dev] = std::max(1, per) * num_sm();
+        }
+        const int64_t grid = (std::max<int64_t>(s, 1) + 255) / 256;
+        if (grid <= cap[dev]) {
+          launch_pdl(kern, dim3((unsigned)grid), dim3(256), 0, st, s, rowbase, Eptr, Ecol, Eval, z, zh, nloc, src, dst, W,
+                     ldw, k, G, partial, gticket, done, npk, pkpos, pk);
+          launched = true;
+        }
+      }
+    });
+    if (launched) return;
   }
   with_nacc(k, [&](auto nc) {
     auto kern = k_ewx<D, decltype(nc)::value>;
@@ -1222,7 +1252,8 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
         Timed t(ctx->prof, s, KC_EW);
         StageDev<D> &nst = (l + 1 < L) ? lev[l + 1].st : last;
         launch_ewx<D>(s, d.s, d.o1, d.E.ptr, ecol, d.E.val, zsrc, hE[l].rbuf, znloc, src, r, d.W, d.ldw, d.k, d.G,
-                      partial, tickets + 0, tvec, ewflag, doneflag, d.npk, d.pkpos, const_cast<D *>(nst.Rg.rhsL));
+                      partial, tickets + 0, tvec, ewflag, doneflag, d.npk, d.pkpos, const_cast<D *>(nst.Rg.rhsL),
+                      gtickets + l);
         packed = d.npk > 0;
         continue;
       }

@@ -1120,6 +1120,21 @@ __global__ void __launch_bounds__(256) k_pack_gather(int64_t np, const int *__re
                                                      int64_t lds = 0, int64_t ldd = 0) {
   // the packing map (setup data) is loaded before griddepcontrol.wait, while the
   // predecessor runs; after it only the gathers (PG positions per thread in flight)
+#ifndef PACK_GATHER_PREFETCH
+#define PACK_GATHER_PREFETCH 0   // measured: the prefetch form 0.965 vs 0.958 ms per C5 iteration
+#endif
+#if !PACK_GATHER_PREFETCH
+  pdl_launch();
+  pdl_wait();
+  if (done && *done) return;
+  src += (size_t)blockIdx.y * lds;
+  dst += (size_t)blockIdx.y * ldd;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x) {
+    const int r = lrow[p];
+    dst[p] = r >= 0 ? src[r] : dzero<T>();
+  }
+  return;
+#endif
   constexpr int PG = 16;
   pdl_launch();
   src += (size_t)blockIdx.y * lds;                                 // column blockIdx.y (several right-hand sides)
@@ -1537,6 +1552,122 @@ __global__ void __launch_bounds__(256) k_ewc(int64_t s, int64_t rowbase, const i
     if (ppk >= 0) pk[ppk] = v2;                                    // the next stage's packed right-hand side
   }
   cluster_sync_all();                                              // partials read by every CTA before any exits
+}
+
+// ----------------------------------------------------------------- K6+K7+K8 for large s_l (PDL, grid barrier)
+// The same one-row-per-thread form as k_ewc for the large interfaces (C5 s_0 = 113k,
+// s_1 = 4.6k), launched with programmatic dependent launch instead of as a
+// cooperative kernel: the setup data of every row (its E entries, its W row, G,
+// its packed position) is loaded while the predecessor trisolve still runs; after
+// griddepcontrol.wait: the z gathers, this CTA's partial of W^H r_J, a grid barrier
+// (a per-call-site ticket counter: this launch's CTAs wait for the round of
+// gridDim.x tickets to complete), every CTA sums all partials in CTA order (the same
+// s everywhere, deterministic), t = G s, r_J += W t.  griddepcontrol.launch_dependents
+// is issued only after the barrier, so no successor CTA can take an SM while a CTA
+// of this grid still waits to become resident (the host checks that the grid fits
+// the SMs at the occupancy of this kernel, else it uses k_ewx).
+template <typename T, int NACC>
+__global__ void __launch_bounds__(256, 3) k_ewg(int64_t s, int64_t rowbase, const int64_t *__restrict__ Eptr,
+                                                const int32_t *__restrict__ Ecol, const T *__restrict__ Eval,
+                                                const T *__restrict__ z, const T *__restrict__ zh, int64_t nloc,
+                                                const T *src, T *dst, const T *__restrict__ W, int64_t ldw, int k,
+                                                const T *__restrict__ G, T *__restrict__ partial,
+                                                unsigned *__restrict__ ticket, const int *__restrict__ done,
+                                                int64_t npk = 0, const int *__restrict__ pkpos = nullptr,
+                                                T *__restrict__ pk = nullptr) {
+  constexpr int KM = 8 * NACC, EM = 4;
+  __shared__ T Gs[KM * KM];
+  __shared__ T wpart[8][KM];
+  __shared__ T sv[KM], st[KM];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 256 + tid;
+  const bool own = i < s;
+  const int64_t p0 = own ? Eptr[i] : 0, p1 = own ? Eptr[i + 1] : 0;
+  int32_t ec[EM];
+  T ev[EM], wr[KM];
+#pragma unroll
+  for (int u = 0; u < EM; ++u) {
+    ec[u] = p0 + u < p1 ? Ecol[p0 + u] : 0;
+    ev[u] = p0 + u < p1 ? Eval[p0 + u] : dzero<T>();
+  }
+#pragma unroll
+  for (int cc = 0; cc < KM; ++cc) wr[cc] = (own && cc < k) ? ld_nc(W + cc * ldw + i) : dzero<T>();
+  for (int q = tid; q < k * k; q += blockDim.x) Gs[q] = G[q];
+  const int ppk = (own && i < npk) ? pkpos[i] : -1;
+  pdl_wait();
+  if (done && *done) return;                                       // uniform over the grid (predecessor complete)
+  T v = dzero<T>();
+  if (own) {
+    auto g = [&](int64_t cc) { return cc < nloc ? z[cc] : zh[cc - nloc]; };
+    T e = dzero<T>(), xg[EM];
+#pragma unroll
+    for (int u = 0; u < EM; ++u) xg[u] = p0 + u < p1 ? g(ec[u]) : dzero<T>();
+#pragma unroll
+    for (int u = 0; u < EM; ++u)
+      if (p0 + u < p1) e += ev[u] * xg[u];
+    for (int64_t p = p0 + EM; p < p1; ++p) e += Eval[p] * g(Ecol[p]);   // rows with more entries
+    v = (src ? src[rowbase + i] : dzero<T>()) - e;
+  }
+#pragma unroll
+  for (int cc = 0; cc < KM; ++cc) {
+    if (cc < k) {
+      const T r = warp_sum(dconj(wr[cc]) * v);
+      if (lane == 0) wpart[warp][cc] = r;
+    }
+  }
+  __syncthreads();
+  const unsigned Gn = gridDim.x;
+  if (tid < k) {
+    T r = dzero<T>();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r += wpart[q][tid];
+    partial[(int64_t)tid * Gn + blockIdx.x] = r;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {                                                  // grid barrier: this launch's round of tickets
+    const unsigned t = atomicAdd(ticket, 1u);
+    const unsigned end = (t / Gn + 1) * Gn;
+    unsigned c;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ticket) : "memory");
+    } while ((int)(c - end) < 0);
+  }
+  __syncthreads();
+  pdl_launch();
+  // s = sum over the CTAs of the partials, in CTA order (the same in every CTA)
+  for (int cc = warp; cc < k; cc += 8) {
+    const T *pp = partial + (int64_t)cc * Gn;
+    T a = dzero<T>();
+    for (unsigned q0 = 0; q0 < Gn; q0 += 256) {
+      T vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const unsigned q = q0 + lane + 32 * u;
+        vv[u] = q < Gn ? ld_cg(pp + q) : dzero<T>();
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += vv[u];
+    }
+    a = warp_sum(a);
+    if (lane == 0) sv[cc] = a;
+  }
+  __syncthreads();
+  if (tid < k) {                                                   // t = G s
+    T t = dzero<T>();
+    for (int a = 0; a < k; ++a) t += Gs[a * k + tid] * sv[a];
+    st[tid] = t;
+  }
+  __syncthreads();
+  if (own) {                                                       // r_J += W t
+    T a = dzero<T>();
+#pragma unroll
+    for (int cc = 0; cc < KM; ++cc)
+      if (cc < k) a += wr[cc] * st[cc];
+    const T v2 = v + a;
+    dst[rowbase + i] = v2;
+    if (ppk >= 0) pk[ppk] = v2;                                    // the next stage's packed right-hand side
+  }
 }
 
 // ----------------------------------------------------------------- K8
