@@ -178,8 +178,8 @@ gemslr_status gemslr_apply_precond(gemslr_ctx *ctx, const void *x_dev, void *y_d
  * function (up to summation order).  The SpMV reads A once for all columns; the
  * apply runs the triangular solves of up to GEMSLR_MAX_RHS columns in one
  * launch per stage (the columns share the factor stream), the E/W coupling per
- * column.  One GPU only (STATE with a communicator); INVALID_ARG for nrhs < 1
- * or ld < n_local. */
+ * column.  With several ranks (collective) the columns go one by one through the
+ * distributed spmv / apply; INVALID_ARG for nrhs < 1 or ld < n_local. */
 #define GEMSLR_MAX_RHS 8
 gemslr_status gemslr_spmv_multi(gemslr_ctx *ctx, const void *x_dev, void *y_dev, int nrhs, int64_t ld);
 gemslr_status gemslr_apply_precond_multi(gemslr_ctx *ctx, const void *x_dev, void *y_dev, int nrhs, int64_t ld);

@@ -536,7 +536,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
   if (S.reg.ok && cps_override <= 0 && tri_kernel == 0 && d.nblk > 0 &&
       reg_smem_bytes<D>(S.reg.ring, S.reg.max_block_slices, S.reg.imp_L + S.reg.imp_U, S.reg.plev_L + S.reg.plev_U,
                         S.reg.Q > 1) <= 232448 - 1024) {
-    static_assert(REG_BINFO == REG_BINFO_INTS, "binfo layout");
+    static_assert(REG_BINFO == REG_BINFO_INTS && REG_WN_SHIFT == REG_WN_SHIFT_DEV, "record layout");
     d.reg = true;
     d.reg_w = S.reg.W;
     d.reg_nw = reg_nw_for<D>(S.reg);
@@ -2525,7 +2525,9 @@ static gemslr_status multi_call(gemslr_ctx *c, Engine<T> &E, int which, const vo
   if (nrhs < 1 || ld < E.n) return fail(c, GEMSLR_ERR_INVALID_ARG, "nrhs < 1 or ld < n_local");
   const D *xi = static_cast<const D *>(x);
   D *yo = static_cast<D *>(y);
-  if (which == 0) {
+  if (which == 0 && E.dist) {                                     // several ranks: column by column (halo exchanges)
+    for (int q = 0; q < nrhs; ++q) E.spmv(xi + (size_t)q * ld, yo + (size_t)q * ld, 0, nullptr, nullptr);
+  } else if (which == 0) {
     E.spmv_multi(xi, yo, ld, nrhs);
   } else if (E.multi_ok()) {
     for (int c0 = 0; c0 < nrhs; c0 += GEMSLR_MAX_RHS)
@@ -2542,7 +2544,6 @@ gemslr_status gemslr_spmv_multi(gemslr_ctx *c, const void *x, void *y, int nrhs,
   gemslr_status st = need_device(c);
   if (st) return st;
   if (!x || !y || x == y) return fail(c, GEMSLR_ERR_INVALID_ARG, "null or aliased blocks");
-  if (c->comm.nranks > 1) return fail(c, GEMSLR_ERR_STATE, "several right-hand sides: one GPU only");
   return guarded(c, [&]() -> gemslr_status {
     return c->dtype == GEMSLR_F64 ? multi_call(c, *c->ed, 0, x, y, nrhs, ld) : multi_call(c, *c->ez, 0, x, y, nrhs, ld);
   });
@@ -2552,7 +2553,6 @@ gemslr_status gemslr_apply_precond_multi(gemslr_ctx *c, const void *x, void *y, 
   gemslr_status st = need_device(c);
   if (st) return st;
   if (!x || !y || x == y) return fail(c, GEMSLR_ERR_INVALID_ARG, "null or aliased blocks");
-  if (c->comm.nranks > 1) return fail(c, GEMSLR_ERR_STATE, "several right-hand sides: one GPU only");
   return guarded(c, [&]() -> gemslr_status {
     return c->dtype == GEMSLR_F64 ? multi_call(c, *c->ed, 1, x, y, nrhs, ld) : multi_call(c, *c->ez, 1, x, y, nrhs, ld);
   });

@@ -116,11 +116,19 @@ static int split_for(const std::vector<int64_t> &bl, const SetupOptions &opt, bo
   // 268 / 284 unsplit (15 warps either way) — the split only pays in fp64
   if (is_complex) return 1;
   const int64_t avg = rows / nb;
-  static const int qmax = getenv("GEMSLR_SPLIT_MAX") ? atoi(getenv("GEMSLR_SPLIT_MAX")) : 4;   // experiments
-  for (int Q = 4; Q >= 2; Q /= 2) {
+  // Measured (tools/split_cmp.py, level-0 DOWN / UP per apply): C5 (32 blocks of 60k rows,
+  // ~6 slices per level) Q = 4 228 / 236 us vs 281 / 299 unsplit (Q = 2: 267 / 282); C3 (64
+  // blocks of 30k rows, only Q = 2 fits) 194 / 198 vs 181 / 186; C2 (16 blocks of 15k rows)
+  // Q = 4 111 / 111, Q = 2 105 / 105 vs 98 / 99.  The split pays only for blocks whose levels
+  // carry many slices: Q = 4 with chunks of at least 12k rows (blocks >= 48k rows).
+  // (Experiments: GEMSLR_SPLIT_MAX, GEMSLR_SPLIT_MINROWS.)
+  static const int qmax = getenv("GEMSLR_SPLIT_MAX") ? atoi(getenv("GEMSLR_SPLIT_MAX")) : 4;
+  static const int64_t minrows = getenv("GEMSLR_SPLIT_MINROWS") ? atoll(getenv("GEMSLR_SPLIT_MINROWS")) : 12288;
+  const int qmin = getenv("GEMSLR_SPLIT_MAX") ? 2 : 4;
+  for (int Q = 4; Q >= qmin; Q /= 2) {
     if (Q > qmax) continue;
     const int fit = Q == 4 ? opt.sms - 16 : opt.sms;                // clusters of 4 leave a few SMs of each GPC idle
-    if ((int64_t)nb * Q <= fit && avg / Q >= 4096) return Q;
+    if ((int64_t)nb * Q <= fit && avg / Q >= minrows) return Q;
   }
   return 1;
 }

@@ -712,6 +712,8 @@ template <typename T> __host__ __device__ inline size_t reg_smem_bytes(int ring,
          al16((size_t)max_slices * 2) * (split ? 2 : 1);
 }
 constexpr int REG_BINFO = 16;            // ints per block in RegDev::binfo (= REG_BINFO_INTS)
+constexpr int REG_WN_SHIFT_DEV = 11;     // = REG_WN_SHIFT: slev = level | wn << 11
+constexpr int REG_LEV_MASK = (1 << REG_WN_SHIFT_DEV) - 1;
 
 // DSMEM hand-off of the split form: every exported value is an asynchronous
 // remote store (st.async) that completes its bytes on the consumer's mbarrier of
@@ -947,11 +949,39 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
         cid = cid == 15 ? 1 : cid + 1;
       }
     };
+    // Look-ahead: the old group (columns [0, wo): levels before the previous one,
+    // imports) is summed after the barrier two levels back, while the previous
+    // level still runs; after the last barrier only the new group (the 1-3 entries
+    // on the previous level) remains on the critical path.
+    auto solve_old = [&](const Buf &B, int wo) {
+      T a0 = B.rhs, a1 = dzero<T>(), a2 = dzero<T>(), a3 = dzero<T>();
+#pragma unroll
+      for (int e = 0; e < W; e += 4) {
+        if (e < wo) a0 -= B.val(e) * ring[B.slot(e)];
+        if (e + 1 < W && e + 1 < wo) a1 -= B.val(e + 1) * ring[B.slot(e + 1)];
+        if (e + 2 < W && e + 2 < wo) a2 -= B.val(e + 2) * ring[B.slot(e + 2)];
+        if (e + 3 < W && e + 3 < wo) a3 -= B.val(e + 3) * ring[B.slot(e + 3)];
+      }
+      return (a0 + a1) + (a2 + a3);
+    };
+    auto solve_new = [&](const Buf &B, int wo, T acc) {
+      T b1 = dzero<T>();
+#pragma unroll
+      for (int e = 0; e < W; ++e) {
+        if (e >= wo) {
+          if ((e & 1) == 0) acc -= B.val(e) * ring[B.slot(e)];
+          else b1 -= B.val(e) * ring[B.slot(e)];
+        }
+      }
+      acc = acc + b1;
+      if (upper) acc = acc * B.dg;
+      return acc;
+    };
     // x_i = (rhs_i - sum_j a_ij x_j) [/ u_ii]: W ring gathers, four partial sums
     auto solve = [&](const Buf &B, int s) {
       const bool tr = !SPLIT && kRegTrace && P.dbg && blockIdx.x == 0 && lane == 0 && s < 2048;
       long long *tp = tr ? P.dbg + 8 * (sw * 2048 + s) : nullptr;
-      if (tr) { tp[2] = clock64(); tp[6] = lvt[lvbase + s]; tp[7] = warp; tp[0] = tp[2]; }
+      if (tr) { tp[2] = clock64(); tp[6] = lvt[lvbase + s] & REG_LEV_MASK; tp[7] = warp; tp[0] = tp[2]; }
       if (tr) {
         const double pr = dabs2(B.val(0)) + dabs2(B.val(W - 1)) + (double)B.slot(0) + (double)B.slot(W - 1) + dabs2(B.rhs);
         tp[4] = clock64() + (pr != pr ? 1 : 0);
@@ -984,7 +1014,7 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
         while (cur < nxt - 1 && pass(false)) {}
       }
     };
-    auto level_of = [&](int t) { return t < ns ? (int)lvt[lvbase + t] : nlev; };
+    auto level_of = [&](int t) { return t < ns ? (int)(lvt[lvbase + t] & REG_LEV_MASK) : nlev; };
     // split: wait until the neighbour's exports this slice reads have landed (the
     // producer levels up to need - 1, monotone per warp); one acquire fence when any
     int rdy = -1;
@@ -1004,7 +1034,8 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
     auto export_ = [&](const Buf &B, int s_, const T &acc) {
       if constexpr (SPLIT) {
         if (B.exp >= 0)
-          st_async_cluster(rimp_sw + (unsigned)(B.exp * (int)sizeof(T)), acc, rmb_sw + (unsigned)lvt[lvbase + s_] * 8u);
+          st_async_cluster(rimp_sw + (unsigned)(B.exp * (int)sizeof(T)), acc,
+                           rmb_sw + (unsigned)(lvt[lvbase + s_] & REG_LEV_MASK) * 8u);
       }
     };
     // The global stores are read only after the sweep-transition barrier.
@@ -1047,15 +1078,18 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
     while (s < ns) {
       int nxt = level_of(s + NW);                                  // read before the barrier: off the critical path
       const long long tq0 = (str && s < 2048) ? clock64() : 0;
-      wait_level(lvt[lvbase + s]);
+      const int lva = lvt[lvbase + s], lv = lva & REG_LEV_MASK, wo = W - (lva >> REG_WN_SHIFT_DEV);
+      wait_level(lv - 1);                                          // the level two back is complete
       wait_imports(s);
+      const T p0 = solve_old(A, wo);
+      wait_level(lv);                                              // the previous level is complete
       const long long tq1 = (str && s < 2048) ? clock64() : 0;
-      const T a0 = solve(A, s);
+      const T a0 = solve_new(A, wo, p0);
       publish(A, s, a0);
       if (str && s < 2048) {
         const double pr = dabs2(a0);
         long long *q4 = sbase + 4 * s;
-        q4[0] = tq0; q4[1] = tq1; q4[2] = clock64() + (pr != pr ? 1 : 0); q4[3] = lvt[lvbase + s] | ((long long)ndt[lvbase + s] << 32);
+        q4[0] = tq0; q4[1] = tq1; q4[2] = clock64() + (pr != pr ? 1 : 0); q4[3] = (lvt[lvbase + s] & REG_LEV_MASK) | ((long long)ndt[lvbase + s] << 32);
       }
       if (SPLIT_EXPORT_FIRST) export_(A, s, a0);
       depart(nxt);
@@ -1067,15 +1101,18 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
         if (s >= ns) break;
         nxt = level_of(s + NW);
         const long long tr0 = (str && s < 2048) ? clock64() : 0;
-        wait_level(lvt[lvbase + s]);
+        const int lvb = lvt[lvbase + s], lv2 = lvb & REG_LEV_MASK, wo2 = W - (lvb >> REG_WN_SHIFT_DEV);
+        wait_level(lv2 - 1);
         wait_imports(s);
+        const T p1 = solve_old(B, wo2);
+        wait_level(lv2);
         const long long tr1 = (str && s < 2048) ? clock64() : 0;
-        const T a1 = solve(B, s);
+        const T a1 = solve_new(B, wo2, p1);
         publish(B, s, a1);
         if (str && s < 2048) {
           const double pr = dabs2(a1);
           long long *q4 = sbase + 4 * s;
-          q4[0] = tr0; q4[1] = tr1; q4[2] = clock64() + (pr != pr ? 1 : 0); q4[3] = lvt[lvbase + s] | ((long long)ndt[lvbase + s] << 32);
+          q4[0] = tr0; q4[1] = tr1; q4[2] = clock64() + (pr != pr ? 1 : 0); q4[3] = (lvt[lvbase + s] & REG_LEV_MASK) | ((long long)ndt[lvbase + s] << 32);
         }
         if (SPLIT_EXPORT_FIRST) export_(B, s, a1);
         depart(nxt);

@@ -247,7 +247,7 @@ void pack_pipe(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriP
 // greedy, 2.86 after this pass (GEMSLR_DEBUG_BANKS=1 prints it; ideal 2).
 // Returns {cost before, cost after}.
 template <typename T>
-static std::pair<int, int> refine_record(uint8_t *base, int W) {
+static std::pair<int, int> refine_record(uint8_t *base, int W, int wo) {
   const int VE = 16 / (int)sizeof(T), G = (int)(128 / sizeof(T)), PL = G;   // lanes per part
   const int NP = 32 / PL;
   T *val = reinterpret_cast<T *>(base);
@@ -293,7 +293,7 @@ static std::pair<int, int> refine_record(uint8_t *base, int W) {
             if (cnt[col[ci(e1, lane)] % G] < c[e1 * NP + h]) continue;
           }
           for (int e2 = 0; e2 < W; ++e2) {
-            if (e2 == e1) continue;
+            if (e2 == e1 || (e2 < wo) != (e1 < wo)) continue;        // look-ahead groups stay apart
             uint16_t &s1 = col[ci(e1, lane)], &s2 = col[ci(e2, lane)];
             if (s1 == s2) continue;
             std::swap(s1, s2);
@@ -323,6 +323,7 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
   P = RegPack<T>();
   P.Q = Q;
   const bool split = Q > 1;
+  static const bool lookahead = getenv("GEMSLR_NO_LOOKAHEAD") == nullptr;   // experiments
   const size_t nblk = blk.size() - 1;
   const size_t nb = nblk * (size_t)Q;                              // pack "blocks" (chunks)
   const int64_t R0 = blk.front(), NR = blk.back() - blk.front();
@@ -465,10 +466,12 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
             for (int lane = 0; lane < 32; ++lane) exp[lane] = -1;
           }
           rec_of[sweep][s] = rec;
-          if (v - lv0 > 65535) return;
-          P.slev.push_back((uint16_t)(v - lv0));
-          // entries of every lane with their ring slots
-          struct Ent { T v; uint16_t slot; };
+          if (v - lv0 >= (1 << REG_WN_SHIFT)) return;
+          // entries of every lane with their ring slots, split for the look-ahead:
+          // "new" = a dependency in the immediately preceding level of this chunk
+          // (needs that level's barrier), "old" = older levels and imports (ready after
+          // the barrier before it, so k_tri_reg sums them while the previous level runs)
+          struct Ent { T v; uint16_t slot; bool nw; };
           std::vector<Ent> ent[32];
           for (int lane = 0; lane < 32; ++lane) {
             const int32_t row = S.slice_row[(int64_t)s * 32 + lane];
@@ -482,17 +485,35 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
                 const int32_t ii = impmap[sweep][b].at(dep - (int32_t)R0);
                 const int32_t pslice = imp[sweep][b][ii].second;
                 need_pref = std::max(need_pref, sl_lev[sweep][pslice]);
-                ent[lane].push_back(Ent{S.val[g], (uint16_t)(R + (upper ? P.imp_L : 0) + ii)});
+                ent[lane].push_back(Ent{S.val[g], (uint16_t)(R + (upper ? P.imp_L : 0) + ii), false});
                 P.near++;
                 continue;
               }
               const int32_t pd = upper ? upos[dep - R0] : P.lpos[dep - R0];
               const int32_t q = pd - sb0 * 32;                  // block-relative position
-              if ((int64_t)send * 32 - 1 - q < R) { ent[lane].push_back(Ent{S.val[g], (uint16_t)(q & (R - 1))}); P.near++; }
+              const bool isnew = !lookahead || sl_lev[sweep][pd / 32] >= (v - lv0) - 1;
+              if ((int64_t)send * 32 - 1 - q < R) { ent[lane].push_back(Ent{S.val[g], (uint16_t)(q & (R - 1)), isnew}); P.near++; }
               else { P.far++; }
             }
           }
           if (split) P.sneed.push_back((uint16_t)(need_pref + 1));
+          // look-ahead groups: columns [0, wo) old, [wo, W) new; wn = the most new
+          // entries of a lane; a lane's old entries beyond wo join its new group
+          // (they fit: old + new <= W)
+          int wn = 0;
+          for (int lane = 0; lane < 32; ++lane) {
+            int c = 0;
+            for (const Ent &en : ent[lane]) c += en.nw ? 1 : 0;
+            wn = std::max(wn, c);
+          }
+          const int wo = W - wn;
+          std::vector<Ent> grp[2][32];
+          for (int lane = 0; lane < 32; ++lane) {
+            for (const Ent &en : ent[lane])
+              if (!en.nw && (int)grp[0][lane].size() < wo) grp[0][lane].push_back(en);
+              else grp[1][lane].push_back(en);
+          }
+          P.slev.push_back((uint16_t)((v - lv0) | (wn << REG_WN_SHIFT)));
           // Column e of the slice is one shared-memory gather of 32 lanes (8 or 16
           // bytes each); order each lane's entries (any order gives the same sum up
           // to rounding) so that every column spreads its distinct slots over the
@@ -511,7 +532,7 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
               }
               uint16_t slot = (uint16_t)(R - 1);
               T v = T(0);
-              auto &L = ent[lane];
+              auto &L = grp[e < wo ? 0 : 1][lane];
               if (!L.empty()) {
                 size_t best = 0;
                 int bc = 1 << 30;
@@ -582,7 +603,7 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
     long long cb = 0, ca = 0;
 #pragma omp parallel for schedule(dynamic, 256) reduction(+ : cb, ca)
     for (int64_t r = 0; r < P.nrec; ++r) {
-      const auto ba = refine_record<T>(P.data.data() + (size_t)r * P.rec_bytes, W);
+      const auto ba = refine_record<T>(P.data.data() + (size_t)r * P.rec_bytes, W, W - (P.slev[r] >> REG_WN_SHIFT));
       cb += ba.first;
       ca += ba.second;
     }

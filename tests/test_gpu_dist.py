@@ -64,6 +64,13 @@ def _worker(rank, world, port, q, case, bdir):
         ref = yo[iperm[s.perm]]
         res["apply"] = float(np.linalg.norm(yg - ref))
         res["apply_ref"] = float(np.linalg.norm(ref))
+        # several right-hand sides on the distributed path (column by column, NEXT-4)
+        r2 = P.rhs_vector(prob.n, prob.is_complex, 6)
+        X = torch.stack([torch.from_numpy(r[s.perm]), torch.from_numpy(r2[s.perm])]).to("cuda:0", dtype=dt)
+        Y = s.apply_precond_multi(X).cpu().numpy()
+        ref2 = Pc.apply(r2[st["perm"]])[iperm[s.perm]]
+        res["multi"] = float(max(np.linalg.norm(Y[0] - ref) / np.linalg.norm(ref),
+                                 np.linalg.norm(Y[1] - ref2) / np.linalg.norm(ref2)))
         out = s.solve(torch.from_numpy(b[s.perm]).to("cuda:0", dtype=dt), rtol=prm["rtol"], restart=prm["restart"])
         xg = out["x"].cpu().numpy()
         full = torch.zeros(prob.n, dtype=torch.complex128 if prob.is_complex else torch.float64)
@@ -108,6 +115,7 @@ def test_two_ranks_on_one_gpu(case, tmp_path):
         tot = np.sqrt(res[0]["apply"] ** 2 + res[1]["apply"] ** 2)
         ref = np.sqrt(res[0]["apply_ref"] ** 2 + res[1]["apply_ref"] ** 2)
         assert tot <= 1e-10 * ref, tot / ref
+        assert res[r]["multi"] <= 1e-10
         if k > 0:
             assert min(res[r]["k"]) >= 1
         assert res[r]["status"] == 0
@@ -118,12 +126,12 @@ def test_two_ranks_on_one_gpu(case, tmp_path):
 
 
 # ---------------------------------------------------------------- NCCL
-def _pair(prob, prm, tmp_path, comm):
+def _pair(prob, prm, tmp_path, comm, tri_split=0):
     import paper_2205_03224_b200 as gm
     import oracle
     from tests.bundle_io import Bundle
     s = gm.Solver(prob.rowptr, prob.colidx, prob.values, prm["levels"], prm["subdomains"], prm["rank"],
-                  ilu=prm["ilu"], coords=prob.coords, device=0, comm=comm)
+                  ilu=prm["ilu"], coords=prob.coords, device=0, comm=comm, tri_split=tri_split)
     B = Bundle(s.export(str(tmp_path / f"bundle_{comm}")))
     st = B.structure()
     Pc = oracle.Precond(prob, st, ilu=(oracle.ILU0 if prm["ilu"] == "ilu0" else oracle.ILUT, 1e-3, 10))
@@ -134,10 +142,11 @@ def _pair(prob, prm, tmp_path, comm):
     return s, st, Pc
 
 
-@pytest.mark.parametrize("name,dims,over", [("C3", (20, 18, 16), dict(subdomains=8, rank=6)),
-                                             ("C4", (16, 16, 14), dict(subdomains=8, rank=6)),
-                                             ("C5", (24, 24, 20), dict(subdomains=8, rank=4))])
-def test_nccl_one_rank_distributed_path(tmp_path, name, dims, over):
+@pytest.mark.parametrize("name,dims,over,split", [("C3", (20, 18, 16), dict(subdomains=8, rank=6), 0),
+                                                   ("C4", (16, 16, 14), dict(subdomains=8, rank=6), 0),
+                                                   ("C5", (24, 24, 20), dict(subdomains=8, rank=4), 0),
+                                                   ("C5", (28, 28, 24), dict(subdomains=4, rank=4), 4)])
+def test_nccl_one_rank_distributed_path(tmp_path, name, dims, over, split):
     """The distributed code path (k_ew + NCCL all-reduce of W^H r + k_waxpy, the last
     separator gathered by an NCCL all-reduce and solved replicated, Gram-Schmidt dots
     all-reduced, FGMRES iterations captured as CUDA graphs WITH their NCCL calls) on
@@ -147,7 +156,9 @@ def test_nccl_one_rank_distributed_path(tmp_path, name, dims, over):
     import oracle
     from synth import problems as P
     prob, b, xt, prm = P.make_config(name, dims=dims, **over)
-    s, st, Pc = _pair(prob, prm, tmp_path, "nccl1")
+    s, st, Pc = _pair(prob, prm, tmp_path, "nccl1", tri_split=split)
+    if split:
+        assert s.stats()["stages"][0]["stage"]["split"] > 1
     dt = s.torch_dtype
     for seed in (2, 3):
         r = P.rhs_vector(prob.n, prob.is_complex, seed)

@@ -218,11 +218,12 @@ def test_multiple_rhs_NEXT4(tmp_path, name, dims, over):
 @pytest.mark.parametrize("name,dims,over", [("C5", (24, 24, 20), dict(subdomains=8, rank=4)),
                                              ("C4", (16, 16, 14), dict(subdomains=8, rank=6)),
                                              ("C3", (20, 18, 16), dict(subdomains=8, rank=0))])
-def test_root_gmres_NEXT1(tmp_path, name, dims, over):
+@pytest.mark.parametrize("split", [1, 2])
+def test_root_gmres_NEXT1(tmp_path, name, dims, over, split):
     """Root-level inner GMRES on Ŝ_0 (Alg. 2 line 6, 3 steps as in P:L1073-1074): apply
     parity against the oracle's root GMRES, FGMRES iterations within ±1, true residual."""
     prob, b, xt, prm = P.make_config(name, dims=dims, **over)
-    s, B, st, Pc = make_pair(prob, prm, tmp_path, root_inner_its=3)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path, root_inner_its=3, tri_split=split)
     Pc.set_root_its(3)
     for seed in (2, 3):
         r = P.rhs_vector(prob.n, prob.is_complex, seed)
