@@ -297,6 +297,7 @@ struct StageDev {
   int reg_w = 0;           // record width W (4, 8, 10, 12 or 16)
   int reg_nw = 0;          // consumer warps of k_tri_reg (reg_nw_for)
   int reg_q = 1;           // split form: CTAs (a cluster) per block
+  int reg_la = 0;          // look-ahead new columns of the records (0 or REG_LA)
   RegDev<D> Rg{};
   int64_t reg_bytes = 0;   // record bytes of both sweeps
   const int *lrow = nullptr;       // per packed L position: the row (-1 padding), DOWN gather
@@ -536,7 +537,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
   if (S.reg.ok && cps_override <= 0 && tri_kernel == 0 && d.nblk > 0 &&
       reg_smem_bytes<D>(S.reg.ring, S.reg.max_block_slices, S.reg.imp_L + S.reg.imp_U, S.reg.plev_L + S.reg.plev_U,
                         S.reg.Q > 1) <= 232448 - 1024) {
-    static_assert(REG_BINFO == REG_BINFO_INTS && REG_WN_SHIFT == REG_WN_SHIFT_DEV, "record layout");
+    static_assert(REG_BINFO == REG_BINFO_INTS && REG_LA == REG_LA_DEV, "record layout");
     d.reg = true;
     d.reg_w = S.reg.W;
     d.reg_nw = reg_nw_for<D>(S.reg);
@@ -557,6 +558,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     d.xU = P.get<D>(std::max<int64_t>(S.reg.uslices * 32, 1));
     d.Rg.ring = S.reg.ring;
     d.reg_q = S.reg.Q;
+    d.reg_la = S.reg.la;
     d.Rg.Q = S.reg.Q;
     d.Rg.imp_L = S.reg.imp_L;
     d.Rg.imp_U = S.reg.imp_U;
@@ -1065,23 +1067,28 @@ static void launch_trisolve(Ctx *ctx, const StageDev<D> &S, int mode, const D *r
     };
     auto by_w = [&](auto nwc, auto nbc) {
       constexpr int NW = decltype(nwc)::value, NB = decltype(nbc)::value;
-      if (S.reg_q > 1) {                                           // split form: a cluster per block
-        switch (S.reg_w) {
-          case 4: go(k_tri_reg<D, 4, NW, NB, true>, NW); break;
-          case 8: go(k_tri_reg<D, 8, NW, NB, true>, NW); break;
-          case 10: go(k_tri_reg<D, 10, NW, NB, true>, NW); break;
-          case 12: go(k_tri_reg<D, 12, NW, NB, true>, NW); break;
-          default: go(k_tri_reg<D, 16, NW, NB, true>, NW); break;
+      auto by_la = [&](auto spc) {                                 // look-ahead (REG_LA new columns) or not
+        constexpr bool SP = decltype(spc)::value;
+        if (S.reg_la > 0) {
+          switch (S.reg_w) {
+            case 4: go(k_tri_reg<D, 4, NW, NB, SP, REG_LA_DEV>, NW); break;
+            case 8: go(k_tri_reg<D, 8, NW, NB, SP, REG_LA_DEV>, NW); break;
+            case 10: go(k_tri_reg<D, 10, NW, NB, SP, REG_LA_DEV>, NW); break;
+            case 12: go(k_tri_reg<D, 12, NW, NB, SP, REG_LA_DEV>, NW); break;
+            default: go(k_tri_reg<D, 16, NW, NB, SP, REG_LA_DEV>, NW); break;
+          }
+          return;
         }
-        return;
-      }
-      switch (S.reg_w) {
-        case 4: go(k_tri_reg<D, 4, NW, NB>, NW); break;
-        case 8: go(k_tri_reg<D, 8, NW, NB>, NW); break;
-        case 10: go(k_tri_reg<D, 10, NW, NB>, NW); break;
-        case 12: go(k_tri_reg<D, 12, NW, NB>, NW); break;
-        default: go(k_tri_reg<D, 16, NW, NB>, NW); break;
-      }
+        switch (S.reg_w) {
+          case 4: go(k_tri_reg<D, 4, NW, NB, SP>, NW); break;
+          case 8: go(k_tri_reg<D, 8, NW, NB, SP>, NW); break;
+          case 10: go(k_tri_reg<D, 10, NW, NB, SP>, NW); break;
+          case 12: go(k_tri_reg<D, 12, NW, NB, SP>, NW); break;
+          default: go(k_tri_reg<D, 16, NW, NB, SP>, NW); break;
+        }
+      };
+      if (S.reg_q > 1) by_la(std::true_type{});                    // split form: a cluster per block
+      else by_la(std::false_type{});
     };
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
@@ -2185,6 +2192,7 @@ std::string Engine<T>::stats_json() const {
            ", \"far\": " + std::to_string(S.far) + ", \"near\": " + std::to_string(S.nearc) +
            ", \"kernel\": \"" + (S.reg ? "reg" : S.pipe ? "pipe" : "level") + "\", \"reg_w\": " + std::to_string(S.reg_w) +
            ", \"split\": " + std::to_string(S.reg ? S.reg_q : 1) + ", \"reg_nw\": " + std::to_string(S.reg_nw) +
+           ", \"la\": " + std::to_string(S.reg ? S.reg_la : 0) +
            ", \"reg_bytes\": " + std::to_string(S.reg_bytes) + "}";
   };
   j += ", \"stages\": [";

@@ -712,8 +712,8 @@ template <typename T> __host__ __device__ inline size_t reg_smem_bytes(int ring,
          al16((size_t)max_slices * 2) * (split ? 2 : 1);
 }
 constexpr int REG_BINFO = 16;            // ints per block in RegDev::binfo (= REG_BINFO_INTS)
-constexpr int REG_WN_SHIFT_DEV = 11;     // = REG_WN_SHIFT: slev = level | wn << 11
-constexpr int REG_LEV_MASK = (1 << REG_WN_SHIFT_DEV) - 1;
+constexpr int REG_LA_DEV = 3;            // = REG_LA (look-ahead new columns)
+constexpr int REG_LEV_MASK = 0xffff;
 
 // DSMEM hand-off of the split form: every exported value is an asynchronous
 // remote store (st.async) that completes its bytes on the consumer's mbarrier of
@@ -786,7 +786,7 @@ struct RegBuf {
 #ifndef SPLIT_EXPORT_FIRST
 #define SPLIT_EXPORT_FIRST 0
 #endif
-template <typename T, int W, int NW, int NB, bool SPLIT = false>
+template <typename T, int W, int NW, int NB, bool SPLIT = false, int LA = 0>
 __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
                                                             const int *__restrict__ done) {
   pdl_launch();
@@ -953,25 +953,24 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
     // imports) is summed after the barrier two levels back, while the previous
     // level still runs; after the last barrier only the new group (the 1-3 entries
     // on the previous level) remains on the critical path.
-    auto solve_old = [&](const Buf &B, int wo) {
+    constexpr int WO = W - LA;                                     // old columns [0, WO), new [WO, W)
+    auto solve_old = [&](const Buf &B) {
       T a0 = B.rhs, a1 = dzero<T>(), a2 = dzero<T>(), a3 = dzero<T>();
 #pragma unroll
-      for (int e = 0; e < W; e += 4) {
-        if (e < wo) a0 -= B.val(e) * ring[B.slot(e)];
-        if (e + 1 < W && e + 1 < wo) a1 -= B.val(e + 1) * ring[B.slot(e + 1)];
-        if (e + 2 < W && e + 2 < wo) a2 -= B.val(e + 2) * ring[B.slot(e + 2)];
-        if (e + 3 < W && e + 3 < wo) a3 -= B.val(e + 3) * ring[B.slot(e + 3)];
+      for (int e = 0; e < WO; e += 4) {
+        a0 -= B.val(e) * ring[B.slot(e)];
+        if (e + 1 < WO) a1 -= B.val(e + 1) * ring[B.slot(e + 1)];
+        if (e + 2 < WO) a2 -= B.val(e + 2) * ring[B.slot(e + 2)];
+        if (e + 3 < WO) a3 -= B.val(e + 3) * ring[B.slot(e + 3)];
       }
       return (a0 + a1) + (a2 + a3);
     };
-    auto solve_new = [&](const Buf &B, int wo, T acc) {
+    auto solve_new = [&](const Buf &B, T acc) {
       T b1 = dzero<T>();
 #pragma unroll
-      for (int e = 0; e < W; ++e) {
-        if (e >= wo) {
-          if ((e & 1) == 0) acc -= B.val(e) * ring[B.slot(e)];
-          else b1 -= B.val(e) * ring[B.slot(e)];
-        }
+      for (int e = WO; e < W; ++e) {
+        if (((e - WO) & 1) == 0) acc -= B.val(e) * ring[B.slot(e)];
+        else b1 -= B.val(e) * ring[B.slot(e)];
       }
       acc = acc + b1;
       if (upper) acc = acc * B.dg;
@@ -1008,10 +1007,13 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
     // before nxt, the level of this warp's next slice (bar.arrive does not wait),
     // so the stores and the record loads that follow never delay a level; the
     // level right before nx's is synced on when nx is computed.
+    // (Look-ahead: the arrivals stop one level earlier — the level two before nxt is
+    // synced on, so the next slice's old group may read it.)
+    constexpr int DL = LA > 0 ? 2 : 1;
     auto depart = [&](int nxt) {
-      if (cur < nxt - 1 && pass(false)) {                          // the current level: straight-line arrival
+      if (cur < nxt - DL && pass(false)) {                         // the current level: straight-line arrival
 #pragma unroll 1
-        while (cur < nxt - 1 && pass(false)) {}
+        while (cur < nxt - DL && pass(false)) {}
       }
     };
     auto level_of = [&](int t) { return t < ns ? (int)(lvt[lvbase + t] & REG_LEV_MASK) : nlev; };
@@ -1078,13 +1080,20 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
     while (s < ns) {
       int nxt = level_of(s + NW);                                  // read before the barrier: off the critical path
       const long long tq0 = (str && s < 2048) ? clock64() : 0;
-      const int lva = lvt[lvbase + s], lv = lva & REG_LEV_MASK, wo = W - (lva >> REG_WN_SHIFT_DEV);
-      wait_level(lv - 1);                                          // the level two back is complete
-      wait_imports(s);
-      const T p0 = solve_old(A, wo);
-      wait_level(lv);                                              // the previous level is complete
+      const int lv = lvt[lvbase + s];
+      T a0;
+      if constexpr (LA > 0) {
+        wait_level(lv - 1);                                        // the level two back is complete
+        wait_imports(s);
+        const T p0 = solve_old(A);
+        wait_level(lv);                                            // the previous level is complete
+        a0 = solve_new(A, p0);
+      } else {
+        wait_level(lv);
+        wait_imports(s);
+        a0 = solve(A, s);
+      }
       const long long tq1 = (str && s < 2048) ? clock64() : 0;
-      const T a0 = solve_new(A, wo, p0);
       publish(A, s, a0);
       if (str && s < 2048) {
         const double pr = dabs2(a0);
@@ -1101,13 +1110,20 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
         if (s >= ns) break;
         nxt = level_of(s + NW);
         const long long tr0 = (str && s < 2048) ? clock64() : 0;
-        const int lvb = lvt[lvbase + s], lv2 = lvb & REG_LEV_MASK, wo2 = W - (lvb >> REG_WN_SHIFT_DEV);
-        wait_level(lv2 - 1);
-        wait_imports(s);
-        const T p1 = solve_old(B, wo2);
-        wait_level(lv2);
+        const int lv2 = lvt[lvbase + s];
+        T a1;
+        if constexpr (LA > 0) {
+          wait_level(lv2 - 1);
+          wait_imports(s);
+          const T p1 = solve_old(B);
+          wait_level(lv2);
+          a1 = solve_new(B, p1);
+        } else {
+          wait_level(lv2);
+          wait_imports(s);
+          a1 = solve(B, s);
+        }
         const long long tr1 = (str && s < 2048) ? clock64() : 0;
-        const T a1 = solve_new(B, wo2, p1);
         publish(B, s, a1);
         if (str && s < 2048) {
           const double pr = dabs2(a1);

@@ -154,13 +154,13 @@ struct PipePack {
 // run pipelined one hand-off apart instead of paying it per level.
 // Record extension: int32 exp[32] after rdiag (import index in the consumer's
 // area of this sweep, -1 none).
-// Look-ahead (round 2): a record's entries are in two groups, columns [0, W - wn) depend
-// only on levels before the previous one (and on imports), columns [W - wn, W) on the
-// previous level; k_tri_reg sums the first group after the barrier two levels back, while
-// the previous level still runs, and only the second after the last barrier.  slev
-// carries the record's level (low REG_WN_SHIFT bits: < 2048 levels per block, else the
-// stage takes another kernel) and wn (high bits, <= 16).
-constexpr int REG_WN_SHIFT = 11;
+// Look-ahead (round 2): with la = REG_LA the last la columns of every record hold the
+// entries on the previous level (at most la per row; "new"), the first W - la columns the
+// entries on older levels and the imports ("old"; a lane's surplus old entries fill its
+// unused new columns).  k_tri_reg sums the old columns after the barrier two levels back,
+// while the previous level still runs; after the last barrier only the new columns remain
+// on the critical path.  A stage with a row of more than la new entries keeps la = 0.
+constexpr int REG_LA = 3;
 constexpr int REG_RING_BYTES = 128 * 1024;     // solution window: 16384 doubles / 8192 complex
 constexpr int REG_BINFO_INTS = 16;             // + split: producer-L xexp offset, producer-L levels, same for U
 inline int reg_width(int w) { return w <= 4 ? 4 : w <= 8 ? 8 : w <= 10 ? 10 : w <= 12 ? 12 : w <= 16 ? 16 : 0; }
@@ -189,6 +189,7 @@ struct RegPack {
   // split form (Q > 1): import areas (entries, max over chunks), producer level
   // tables, per-record prefix-max of the producer level needed (+1, 0 = none)
   int Q = 1;
+  int la = 0;                                   // look-ahead new columns (0 or REG_LA)
   int imp_L = 0, imp_U = 0;                     // IL, IU
   int plev_L = 0, plev_U = 0;                   // max producer local levels (counter / xexp table sizes)
   std::vector<uint16_t> sneed;                  // per record

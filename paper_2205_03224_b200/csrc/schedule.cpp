@@ -392,6 +392,43 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
   P.ring = 1024;
   while (P.ring < need && P.ring < REG_RING_BYTES / (int)sizeof(T)) P.ring *= 2;
   const int R = P.ring;
+  // look-ahead (plan.hpp REG_LA): every row's entries on the previous level of its chunk
+  // (in-chunk dependencies only; imports are always ready before) must fit REG_LA columns
+  {
+    int maxnew = 0;
+    for (size_t b = 0; b < nb; ++b)
+      for (int sweep = 0; sweep < 2; ++sweep) {
+        const TriPack<T> &S = sweep ? Up : Lp;
+        for (int32_t v = S.blk_lev[b]; v < S.blk_lev[b + 1]; ++v)
+          for (int32_t sl = S.lev_slice[v]; sl < S.lev_slice[v + 1]; ++sl) {
+            const int w = (int)((S.slice_off[sl + 1] - S.slice_off[sl]) / 32);
+            for (int lane = 0; lane < 32; ++lane) {
+              int c = 0;
+              for (int e = 0; e < w; ++e) {
+                const int32_t dep = S.col[S.slice_off[sl] + 32 * e + lane];
+                if (dep < 0 || chunk[dep - R0] != (int32_t)b) continue;
+                const int32_t pd = sweep ? upos[dep - R0] : P.lpos[dep - R0];
+                if (sl_lev[sweep][pd / 32] >= (v - S.blk_lev[b]) - 1) c++;
+              }
+              maxnew = std::max(maxnew, c);
+            }
+          }
+      }
+    // Measured (tools/split_cmp.py, DOWN / UP per apply): the look-ahead shortens the
+    // per-level chain where levels carry 1-2 slices (C5 level 1 51.7 -> 47.5 us, C4 level
+    // 1 76 -> 70, level 2 23 -> 21) but costs where several slices per level contend for
+    // the shared-memory pipe (the two column groups constrain the bank spread of the
+    // gathers: C3 level 0 180 -> 199 us, C4 level 0 269 -> 313; C5's split level 0
+    // 227 -> 223): so only stages with fewer than 2 slices per level on average.
+    int64_t sl = 0, lv = 0;
+    for (size_t b = 0; b < nb; ++b) {
+      sl += (Lp.lev_slice[Lp.blk_lev[b + 1]] - Lp.lev_slice[Lp.blk_lev[b]]) +
+            (Up.lev_slice[Up.blk_lev[b + 1]] - Up.lev_slice[Up.blk_lev[b]]);
+      lv += (Lp.blk_lev[b + 1] - Lp.blk_lev[b]) + (Up.blk_lev[b + 1] - Up.blk_lev[b]);
+    }
+    const double K = lv > 0 ? (double)sl / (double)lv : 1.0;
+    P.la = (lookahead && maxnew <= REG_LA && W > REG_LA && K < 2.0) ? REG_LA : 0;
+  }
   // split: imports of every chunk and sweep (dependency rows in another chunk),
   // numbered in the order the consumer's records first need them
   std::vector<std::vector<std::pair<int32_t, int32_t>>> imp[2];   // per chunk: (stage row, producer slice)
@@ -466,7 +503,8 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
             for (int lane = 0; lane < 32; ++lane) exp[lane] = -1;
           }
           rec_of[sweep][s] = rec;
-          if (v - lv0 >= (1 << REG_WN_SHIFT)) return;
+          if (v - lv0 > 65535) return;
+          P.slev.push_back((uint16_t)(v - lv0));
           // entries of every lane with their ring slots, split for the look-ahead:
           // "new" = a dependency in the immediately preceding level of this chunk
           // (needs that level's barrier), "old" = older levels and imports (ready after
@@ -491,29 +529,21 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
               }
               const int32_t pd = upper ? upos[dep - R0] : P.lpos[dep - R0];
               const int32_t q = pd - sb0 * 32;                  // block-relative position
-              const bool isnew = !lookahead || sl_lev[sweep][pd / 32] >= (v - lv0) - 1;
+              const bool isnew = sl_lev[sweep][pd / 32] >= (v - lv0) - 1;
               if ((int64_t)send * 32 - 1 - q < R) { ent[lane].push_back(Ent{S.val[g], (uint16_t)(q & (R - 1)), isnew}); P.near++; }
               else { P.far++; }
             }
           }
           if (split) P.sneed.push_back((uint16_t)(need_pref + 1));
-          // look-ahead groups: columns [0, wo) old, [wo, W) new; wn = the most new
-          // entries of a lane; a lane's old entries beyond wo join its new group
-          // (they fit: old + new <= W)
-          int wn = 0;
-          for (int lane = 0; lane < 32; ++lane) {
-            int c = 0;
-            for (const Ent &en : ent[lane]) c += en.nw ? 1 : 0;
-            wn = std::max(wn, c);
-          }
-          const int wo = W - wn;
+          // look-ahead groups: columns [0, wo) old, [wo, W) new (wo = W - la); a lane's
+          // old entries beyond wo fill its unused new columns (old + new <= W)
+          const int wo = W - P.la;
           std::vector<Ent> grp[2][32];
           for (int lane = 0; lane < 32; ++lane) {
             for (const Ent &en : ent[lane])
-              if (!en.nw && (int)grp[0][lane].size() < wo) grp[0][lane].push_back(en);
+              if (P.la == 0 || (!en.nw && (int)grp[0][lane].size() < wo)) grp[0][lane].push_back(en);
               else grp[1][lane].push_back(en);
           }
-          P.slev.push_back((uint16_t)((v - lv0) | (wn << REG_WN_SHIFT)));
           // Column e of the slice is one shared-memory gather of 32 lanes (8 or 16
           // bytes each); order each lane's entries (any order gives the same sum up
           // to rounding) so that every column spreads its distinct slots over the
@@ -532,7 +562,7 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
               }
               uint16_t slot = (uint16_t)(R - 1);
               T v = T(0);
-              auto &L = grp[e < wo ? 0 : 1][lane];
+              auto &L = grp[P.la == 0 || e < wo ? 0 : 1][lane];
               if (!L.empty()) {
                 size_t best = 0;
                 int bc = 1 << 30;
@@ -603,7 +633,7 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
     long long cb = 0, ca = 0;
 #pragma omp parallel for schedule(dynamic, 256) reduction(+ : cb, ca)
     for (int64_t r = 0; r < P.nrec; ++r) {
-      const auto ba = refine_record<T>(P.data.data() + (size_t)r * P.rec_bytes, W, W - (P.slev[r] >> REG_WN_SHIFT));
+      const auto ba = refine_record<T>(P.data.data() + (size_t)r * P.rec_bytes, W, W - P.la);
       cb += ba.first;
       ca += ba.second;
     }
