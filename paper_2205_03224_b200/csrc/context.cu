@@ -1532,14 +1532,18 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
       }
     } else {
       // complex: lane groups (2 x 32 or 4 x 26 columns per row tile)
-      auto go3 = [&](auto kern, int rw) {
-        const int grid = grid_for((nn + 8 * rw - 1) / (8 * rw), 1);
+      auto go3 = [&](auto kern, int rw, int per_sm = 1) {
+        const int grid = grid_for((nn + 8 * rw - 1) / (8 * rw), per_sm);
         launch_pdl(kern, dim3(grid), dim3(256), 0, ctx->stream, nn, Vb, ldvv, ncols, wv, upd, dot, h_in, partial,
                    tickets + ticket, resv, doneflag);
       };
       if (ncols <= 48) done2 = false;                             // k_gs<2,6> measured faster here
       else if (ncols <= 64) go3(k_gs2g<D, 2, 32>, 16);
-      else if (ncols <= 104) go3(k_gs2g<D, 4, 26>, 8);
+      else if (ncols <= 104) {
+        static const int g8 = getenv("GEMSLR_GS2G") ? atoi(getenv("GEMSLR_GS2G")) : 4;
+        if (g8 == 8) go3(k_gs2g<D, 8, 13>, 4, 2);                   // 8 groups of 4 lanes, 2 CTAs per SM
+        else go3(k_gs2g<D, 4, 26>, 8);
+      }
       else done2 = false;
     }
   }

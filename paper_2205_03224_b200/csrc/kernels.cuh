@@ -2112,7 +2112,7 @@ __device__ inline void tbfly_n(T (&x)[RW], int sub) {
   }
 }
 template <typename T, int G, int C>
-__global__ void __launch_bounds__(256, 1) k_gs2g(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
+__global__ void __launch_bounds__(256, G >= 8 ? 2 : 1) k_gs2g(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols, T *w, int upd,
                                                 int dot, const T *__restrict__ h_in, T *__restrict__ partial,
                                                 unsigned *ticket, T *__restrict__ res, const int *__restrict__ done) {
   pdl_launch();
@@ -2297,8 +2297,11 @@ __global__ void __launch_bounds__(256) k_fgmres_scale(FgmDev<T> f, int m, int j,
       if (threadIdx.x == 0) { f.cs[j] = css[j]; f.sn[j] = sns[j]; }
     }
   }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    vnext[i] = dscale(w[i], sc);
+  // CTA 0 only does the Givens column (a chain of small dependent loads); the other
+  // CTAs scale, so the kernel ends at the later of the two instead of their sum
+  if (gridDim.x > 1 && blockIdx.x == 0) return;
+  const int64_t b0 = gridDim.x > 1 ? (int64_t)blockIdx.x - 1 : 0, nb = gridDim.x > 1 ? (int64_t)gridDim.x - 1 : 1;
+  for (int64_t i = b0 * blockDim.x + threadIdx.x; i < n; i += nb * blockDim.x) vnext[i] = dscale(w[i], sc);
 }
 
 // ----------------------------------------------------------------- NEXT-1 root GMRES helpers
