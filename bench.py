@@ -150,6 +150,16 @@ def algorithmic_bytes(stats, v, ld_iters, n):
     down = up = last = 0
     for st in stats["stages"]:
         S = st["stage"]
+        t = S.get("tail")
+        if t:
+            # tail form (DESIGN 6b): DOWN reads L (L_hh + L_t|h) and U_tt with the tail's
+            # diagonal, b1, writes t and z1 on the tail; UP reads L_tt, U (U_tt + U_h|t) with
+            # every diagonal, F_l, t, writes and reads u on the tail, writes y1
+            nz = t["nnz"]
+            down += (nz[0] + nz[1] + nz[2]) * (v + 4) + t["rows"] * v + 2 * S["rows"] * v + t["rows"] * v
+            up += (nz[4] + nz[2] + nz[3]) * (v + 4) + S["rows"] * v + st["nnzF"] * (v + 4) + 2 * S["rows"] * v \
+                + 2 * t["rows"] * v
+            continue
         fac = (S["nnz"] - S["rows"]) * (v + 4) + S["rows"] * v
         down += fac + 2 * S["rows"] * v
         up += fac + st["nnzF"] * (v + 4) + 5 * S["rows"] * v
@@ -283,7 +293,12 @@ def run_ours(args):
     # gather + DFMA chain + barrier hand-off, ~250 cycles at 1-2 slices per level).
     if dom.startswith("trisolve") and dom != "trisolve_last":
         try:
-            depth = sum(st["stage"]["depth_L"] + st["stage"]["depth_U"] for st in stats["stages"])
+            def _depth(g):
+                t = g["stage"].get("tail")
+                if t:
+                    return sum(t["depth_up" if dom == "trisolve_up" else "depth_down"])
+                return g["stage"]["depth_L"] + g["stage"]["depth_U"]
+            depth = sum(_depth(st) for st in stats["stages"])
             per_set = dd["ms_total"] * 1e3 / (dd["launches"] / max(len(stats["stages"]), 1))   # us per apply
             mhz = (clocks or {}).get("sm_mhz") or 1965.0
             roofline["latency"] = {"levels_per_apply": depth, "us_per_apply": round(per_set, 1),

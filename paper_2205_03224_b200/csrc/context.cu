@@ -313,6 +313,25 @@ struct StageDev {
   int64_t nchunks = 0, far = 0, nearc = 0;
   int64_t nnz = 0;         // real stored nonzeros (L + U incl. diagonal)
   int64_t padded = 0;      // stored entries incl. padding
+  // tail form (plan.hpp TailPack, DESIGN 6b) of the one-column apply's DOWN / UP
+  bool tail = false;
+  RegDev<D> TD{}, TU{};
+  int td_w = 0, td_nw = 0, td_la = 0, tu_w = 0, tu_nw = 0, tu_la = 0;
+  size_t td_smem = 0, tu_smem = 0;
+  const int *tlrow = nullptr;      // per DOWN L position: the row (-1 padding)
+  int64_t tnL = 0;                 // DOWN L positions
+  D *trhsL = nullptr;              // DOWN right-hand sides ([L_hh | L_t|h] order)
+  D *tT = nullptr;                 // t = L^-1 b1 (Ucat order)
+  D *tu = nullptr;                 // u = L_tt^-1 (F_l y2)_tail (U_tt order)
+  D *tz = nullptr;                 // z1 on the tail (U_tt order; E_l reads it)
+  D *trhsU = nullptr;              // (F_l y2)_tail in L_tt order (zero off the F_l rows)
+  const int *tfpos = nullptr;      // L_tt position of every row with F_l entries
+  const int *tfrow = nullptr;      // those rows (F_l row index)
+  int64_t tnf = 0;
+  int depth_tail[6] = {0, 0, 0, 0, 0, 0};   // L_hh, L_t|h, U_tt, L_tt, U_tt, U_h|t
+  int64_t tail_rows = 0, tail_bytes = 0;
+  int64_t tail_nnz[5] = {0, 0, 0, 0, 0};   // stored entries of L_hh, L_t|h, U_tt (no diagonal), U_h|t, L_tt
+  D *rhs_packed_buf() const { return tail ? trhsL : const_cast<D *>(Rg.rhsL); }
 };
 
 template <typename D>
@@ -483,8 +502,8 @@ static int reg_nw_for(const RegPack<T> &R) {
   int64_t sl = 0, lv = 0;
   for (int b = 0; b < nb; ++b) {
     const int32_t *bi = &R.binfo[(size_t)b * REG_BINFO_INTS];
-    sl += bi[1] + bi[4];
-    lv += bi[2] + bi[5];
+    sl += bi[1] + bi[4] + (R.nsweep == 3 ? bi[7] : 0);
+    lv += bi[2] + bi[5] + (R.nsweep == 3 ? bi[8] : 0);
   }
   const double K = lv > 0 ? (double)sl / (double)lv : 1.0;
   if (sizeof(D) == 8) {
@@ -566,8 +585,70 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
     d.Rg.plev_U = S.reg.plev_U;
     d.Rg.sneed = S.reg.Q > 1 ? P.upload<unsigned short>(S.reg.sneed, s) : nullptr;
     d.Rg.xexp = S.reg.Q > 1 ? P.upload<unsigned short>(S.reg.xexp, s) : nullptr;
+    d.Rg.xp = S.reg.xmode ? 1 : 0;
     d.reg_bytes = (int64_t)S.reg.data.size();
     if (!d.pipe) d.P.lpos = P.upload<int>(S.reg.lpos, s);
+  }
+  // tail form: only next to the one-CTA / split register kernel (the same record format)
+  const bool no_tail = getenv("GEMSLR_TAIL") && atoi(getenv("GEMSLR_TAIL")) != 1;   // 0 off, 2 order only
+  if (S.tail.ok && !no_tail && sizeof(D) == 8 && d.nblk > 0 && cps_override <= 0 && tri_kernel == 0) {
+    const TailPack<T> &TP = S.tail;
+    auto mk = [&](const RegPack<T> &R, RegDev<D> &G, int &w, int &nw, int &la, size_t &smem) {
+      G = RegDev<D>{};
+      G.data = P.upload<unsigned char>(R.data, s);
+      G.slev = P.upload<unsigned short>(R.slev, s);
+      G.max_slices = R.max_block_slices;
+      G.rec_bytes = (long long)R.rec_bytes;
+      G.binfo = P.upload<int>(R.binfo, s);
+      G.ring = R.ring;
+      G.Q = 1;
+      G.imp_L = R.imp_L;
+      G.xp = 1;
+      w = R.W;
+      nw = reg_nw_for<D>(R);
+      la = R.la;
+      smem = reg_smem_bytes<D>(R.ring, R.max_block_slices, R.imp_L, 0, false);
+      return smem <= 232448 - 1024;
+    };
+    bool ok = mk(TP.D, d.TD, d.td_w, d.td_nw, d.td_la, d.td_smem);
+    ok = mk(TP.U, d.TU, d.tu_w, d.tu_nw, d.tu_la, d.tu_smem) && ok;
+    if (ok) {
+      d.tail = true;
+      d.tnL = (int64_t)TP.lrow.size();
+      d.tlrow = P.upload<int>(TP.lrow, s);
+      const int64_t nU = (int64_t)TP.Utt.slice_row.size() + (int64_t)TP.Uht.slice_row.size();
+      d.trhsL = P.get<D>(std::max<int64_t>(d.tnL, 1));
+      CK(cudaMemsetAsync(d.trhsL, 0, std::max<int64_t>(d.tnL, 1) * sizeof(D), s));
+      d.tT = P.get<D>(std::max<int64_t>(nU, 1));
+      d.tu = P.get<D>(std::max<int64_t>(TP.nUtt, 1));
+      d.tz = P.get<D>(std::max<int64_t>(TP.nUtt, 1));
+      const int64_t nLtt = std::max<int64_t>((int64_t)TP.Ltt.slice_row.size(), 1);
+      d.trhsU = P.get<D>(nLtt);
+      CK(cudaMemsetAsync(d.trhsU, 0, nLtt * sizeof(D), s));
+      // DOWN: L_hh, L_t|h -> t (Ucat), U_tt -> z1 (U_tt order)
+      RegDev<D> &A = d.TD;
+      A.ra[0] = d.trhsL; A.roff[0] = 0; A.st[0] = d.tT; A.stm[0] = 0; A.upper[0] = 0;
+      A.ra[1] = d.trhsL; A.roff[1] = TP.nLhh; A.st[1] = d.tT; A.stm[1] = 0; A.upper[1] = 0;
+      A.ra[2] = d.tT; A.roff[2] = 0; A.st[2] = d.tz; A.stm[2] = 1; A.upper[2] = 1;
+      // UP: L_tt -> u, U_tt on t - u -> x, U_h|t on t -> x (x set per launch)
+      RegDev<D> &B = d.TU;
+      B.ra[0] = d.trhsU; B.roff[0] = 0; B.st[0] = d.tu; B.stm[0] = 0; B.upper[0] = 0;
+      B.ra[1] = d.tT; B.rb[1] = d.tu; B.roff[1] = 0; B.stm[1] = 0; B.upper[1] = 1;
+      B.ra[2] = d.tT; B.roff[2] = TP.nUtt; B.stm[2] = 0; B.upper[2] = 1;
+      d.depth_tail[0] = TP.Lhh.max_depth;
+      d.depth_tail[1] = TP.Lth.max_depth;
+      d.depth_tail[2] = TP.Utt.max_depth;
+      d.depth_tail[3] = TP.Ltt.max_depth;
+      d.depth_tail[4] = TP.Utt.max_depth;
+      d.depth_tail[5] = TP.Uht.max_depth;
+      d.tail_rows = TP.tail_rows;
+      d.tail_nnz[0] = TP.Lhh.nnz_real;
+      d.tail_nnz[1] = TP.Lth.nnz_real;
+      d.tail_nnz[2] = TP.Utt.nnz_real;
+      d.tail_nnz[3] = TP.Uht.nnz_real;
+      d.tail_nnz[4] = TP.Ltt.nnz_real;
+      d.tail_bytes = (int64_t)(TP.D.data.size() + TP.U.data.size());
+    }
   }
   if (S.reg.Q > 1 && !d.reg)                                       // chunks are not independent blocks
     throw Error{GEMSLR_ERR_INVALID_ARG, "split triangular solves need the register-prefetched kernel"};
@@ -743,6 +824,43 @@ void Engine<T>::upload(cudaStream_t s) {
         }
       }
     }
+    if (d.st.tail) {                                               // tail form: positions in its packs
+      const auto &Fh = plan.F[l], &Eh = plan.E[l];
+      const Stage<T> &S = plan.stage[l];
+      const TailPack<T> &TP = S.tail;
+      const int64_t R0 = S.blk.empty() ? 0 : S.blk.front();
+      auto at = [&](const std::vector<int32_t> &pos, int64_t lrow_) -> int32_t {
+        const int64_t row = lrow_ - R0;
+        return (row < 0 || row >= (int64_t)pos.size()) ? -1 : pos[row];
+      };
+      bool ok = true;
+      std::vector<int32_t> fpos, frow;
+      for (int64_t i = 0; i < Fh.n && ok; ++i) {
+        if (Fh.ptr[i + 1] == Fh.ptr[i]) continue;
+        fpos.push_back(at(TP.lttpos, d.o0 + i));
+        frow.push_back((int32_t)i);
+        ok = fpos.back() >= 0;
+      }
+      std::vector<int32_t> ecp(Eh.col.size()), sp(plan.hE[l].sidx.size());
+      for (size_t q = 0; q < Eh.col.size() && ok; ++q) {
+        if (Eh.col[q] >= n) { ecp[q] = kHaloE + (int32_t)(Eh.col[q] - n); continue; }
+        ecp[q] = at(TP.uttpos, Eh.col[q]);
+        ok = ecp[q] >= 0;
+      }
+      for (size_t q = 0; q < sp.size() && ok; ++q) {
+        sp[q] = at(TP.uttpos, plan.hE[l].sidx[q]);
+        ok = sp[q] >= 0;
+      }
+      if (ok) {
+        d.st.tfpos = P.upload<int>(fpos, s);
+        d.st.tfrow = P.upload<int>(frow, s);
+        d.st.tnf = (int64_t)fpos.size();
+        d.Ecol_p = P.upload<int32_t>(ecp, s);
+        d.esidx_p = P.upload<int32_t>(sp, s);
+      } else {
+        d.st.tail = false;
+      }
+    }
     hE[l] = upload_halo<D>(P, s, plan.hE[l]);
     hF[l] = upload_halo<D>(P, s, plan.hF[l]);
   }
@@ -760,16 +878,18 @@ void Engine<T>::upload(cudaStream_t s) {
       if (npk <= 0 || npk > d.s) continue;
       std::vector<int32_t> pos(npk);
       bool ok = true;
+      const std::vector<int32_t> &lp = nd.tail ? NS.tail.lcat : NS.reg.lpos;   // the stage's DOWN L positions
       for (int64_t i = 0; i < npk && ok; ++i) {
         // (the last stage numbers its rows from o_L: make_stage's relative bounds)
         const int64_t row = d.o1 + i - (l + 1 < L ? R0n : plan.lo[L] + R0n);
-        if (row < 0 || row >= (int64_t)NS.reg.lpos.size() || NS.reg.lpos[row] < 0) ok = false;
-        else pos[i] = NS.reg.lpos[row];
+        if (row < 0 || row >= (int64_t)lp.size() || lp[row] < 0) ok = false;
+        else pos[i] = lp[row];
       }
       if (!ok) continue;
       d.pkpos = P.upload<int>(pos, s);
       d.npk = npk;
-      CK(cudaMemsetAsync(const_cast<D *>(nd.Rg.rhsL), 0, std::max<int64_t>(nd.lslices * 32, 1) * sizeof(D), s));
+      if (nd.tail) CK(cudaMemsetAsync(nd.trhsL, 0, std::max<int64_t>(nd.tnL, 1) * sizeof(D), s));
+      else CK(cudaMemsetAsync(const_cast<D *>(nd.Rg.rhsL), 0, std::max<int64_t>(nd.lslices * 32, 1) * sizeof(D), s));
     }
   }
   if (dist) {
@@ -993,6 +1113,65 @@ struct FArgs {
   int64_t Fbase = 0, nloc = 0, nh = 0;
   const D *yh = nullptr, *yl = nullptr;
 };
+
+// Tail form of a level's DOWN / UP (plan.hpp TailPack, DESIGN 6b), one right-hand side:
+// DOWN packs b1 ([L_hh | L_t|h] order; or k_ewx already did), then one k_tri_reg<TAIL>
+// launch: t -> S.tT, z1 on the tail -> S.tz.  UP packs (F_l y2)_tail (k_pack_f), then
+// one launch: y1 -> x[I_l].
+template <typename D>
+static void launch_tail(Ctx *ctx, const StageDev<D> &S, bool down, const D *rhs, D *x, const FArgs<D> &fa,
+                        const int *doneflag, int kc, int lvl, bool rhs_packed) {
+  if (S.nblk <= 0 || S.rows == 0) return;
+  if constexpr (sizeof(D) != 8) {
+    throw Error{GEMSLR_ERR_STATE, "tail form: fp64 only"};
+  } else {
+    {
+      const Timed tt(ctx->prof, ctx->stream, KC_PACK);
+      if (down && !rhs_packed) {
+        launch_pdl(k_pack_gather<D>, dim3(grid_for((S.tnL + 255) / 256, 4), 1), dim3(256), 0, ctx->stream, S.tnL,
+                   S.tlrow, rhs, S.trhsL, doneflag, (int64_t)0, (int64_t)0);
+      } else if (!down && S.tnf > 0) {
+        const CsrDev<D> *F = fa.F;
+        launch_pdl(k_pack_f<D>, dim3(grid_for((S.tnf + 255) / 256, 4), 1), dim3(256), 0, ctx->stream, (int64_t)S.tnf,
+                   S.tfpos, S.tfrow, F->ptr, F->col, F->val, (const D *)x, (int64_t)fa.nloc, fa.yh, (int64_t)fa.nh, fa.yl,
+                   S.trhsU, doneflag, (int64_t)0, (int64_t)0, (int64_t)0, (const int *)nullptr, (D *)nullptr);
+      }
+    }
+    RegDev<D> Rg = down ? S.TD : S.TU;
+    if (!down) Rg.st[1] = Rg.st[2] = x;
+    const int w = down ? S.td_w : S.tu_w, nw = down ? S.td_nw : S.tu_nw, la = down ? S.td_la : S.tu_la;
+    const size_t smem = down ? S.td_smem : S.tu_smem;
+    Timed t(ctx->prof, ctx->stream, kc, lvl);
+    auto go = [&](auto kern) {
+      static std::set<const void *> attr;
+      if (attr.insert((const void *)kern).second)
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024));
+      launch_pdl(kern, dim3(S.nblk, 1), dim3(32 * nw), smem, ctx->stream, Rg, (int)TRI_DOWN, x, (D *)nullptr, doneflag);
+    };
+    auto by_w = [&](auto nwc, auto nbc, auto lac) {
+      constexpr int NW = decltype(nwc)::value, NB = decltype(nbc)::value, LA = decltype(lac)::value;
+      switch (w) {
+        case 4: go(k_tri_reg<D, 4, NW, NB, false, LA, true>); break;
+        case 8: go(k_tri_reg<D, 8, NW, NB, false, LA, true>); break;
+        case 10: go(k_tri_reg<D, 10, NW, NB, false, LA, true>); break;
+        case 12: go(k_tri_reg<D, 12, NW, NB, false, LA, true>); break;
+        default: go(k_tri_reg<D, 16, NW, NB, false, LA, true>); break;
+      }
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using ILA = std::integral_constant<int, REG_LA_DEV>;
+    if (nw == 23) {
+      if (la > 0) by_w(std::integral_constant<int, 23>{}, I1{}, ILA{});
+      else by_w(std::integral_constant<int, 23>{}, I1{}, I0{});
+    } else {
+      if (la > 0) by_w(std::integral_constant<int, 15>{}, I2{}, ILA{});
+      else by_w(std::integral_constant<int, 15>{}, I2{}, I0{});
+    }
+    CK(cudaGetLastError());
+  }
+}
 
 template <typename D>
 // xpm (one right-hand side, register kernel): DOWN writes the level's result to
@@ -1247,19 +1426,21 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     const D *src = (l == l0) ? in : r;
     // z1 = U_l^-1 L_l^-1 b1  -> out[I_l] (xpm: U-packed in d.st.xU, read by E_l and the UP)
     const bool xpm = d.Ecol_p != nullptr;
-    launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, l, 1, 0, xpm, packed);
+    if (d.st.tail) launch_tail(ctx, d.st, true, src, out, FArgs<D>{}, doneflag, KC_TRI_DOWN, l, packed);
+    else launch_trisolve(ctx, d.st, TRI_DOWN, src, out, tmp, FArgs<D>{}, doneflag, KC_TRI_DOWN, l, 1, 0, xpm, packed);
     packed = false;
-    const D *zsrc = xpm ? (const D *)d.st.xU : (const D *)out;
+    D *zp = d.st.tail ? d.st.tz : d.st.xU;                         // z1 in U-packed order (xpm)
+    const D *zsrc = xpm ? (const D *)zp : (const D *)out;
     const int32_t *ecol = xpm ? d.Ecol_p : d.E.col;
     const int64_t znloc = kHaloE;                                  // E's halo columns start there (U-packed ones may exceed n)
     if (d.s > 0 || dist) {
-      if (xpm) exchange(hE[l], d.st.xU, doneflag, nullptr, d.esidx_p);   // z1 entries of E_l's exterior columns
+      if (xpm) exchange(hE[l], zp, doneflag, nullptr, d.esidx_p);   // z1 entries of E_l's exterior columns
       else exchange(hE[l], out, doneflag);
       if (!dist && d.k > 0) {                                      // one cooperative launch: K6 + K7 + K8
         Timed t(ctx->prof, s, KC_EW);
         StageDev<D> &nst = (l + 1 < L) ? lev[l + 1].st : last;
         launch_ewx<D>(s, d.s, d.o1, d.E.ptr, ecol, d.E.val, zsrc, hE[l].rbuf, znloc, src, r, d.W, d.ldw, d.k, d.G,
-                      partial, tickets + 0, tvec, ewflag, doneflag, d.npk, d.pkpos, const_cast<D *>(nst.Rg.rhsL),
+                      partial, tickets + 0, tvec, ewflag, doneflag, d.npk, d.pkpos, nst.rhs_packed_buf(),
                       gtickets + l);
         packed = d.npk > 0;
         continue;
@@ -1279,7 +1460,7 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
         const int grid = grid_for((std::max<int64_t>(d.s, 1) + 255) / 256, 8);
         StageDev<D> &nst = (l + 1 < L) ? lev[l + 1].st : last;
         k_waxpy<D><<<grid, 256, 0, s>>>(d.s, d.o1, d.W, d.ldw, d.k, d.G, tvec, r, doneflag, d.npk, d.pkpos,
-                                        const_cast<D *>(nst.Rg.rhsL));
+                                        nst.rhs_packed_buf());
         packed = d.npk > 0;
         CK(cudaGetLastError());
       }
@@ -1311,8 +1492,9 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     fa.yh = hF[l].rbuf;
     fa.nh = hF[l].nrecv;
     fa.yl = yl_full;
-    launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP, l, 1, 0,
-                    d.Ecol_p != nullptr);
+    if (d.st.tail) launch_tail(ctx, d.st, false, (const D *)nullptr, out, fa, doneflag, KC_TRI_UP, l, false);
+    else launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP, l, 1, 0,
+                         d.Ecol_p != nullptr);
   }
 }
 
@@ -2197,7 +2379,19 @@ std::string Engine<T>::stats_json() const {
            ", \"kernel\": \"" + (S.reg ? "reg" : S.pipe ? "pipe" : "level") + "\", \"reg_w\": " + std::to_string(S.reg_w) +
            ", \"split\": " + std::to_string(S.reg ? S.reg_q : 1) + ", \"reg_nw\": " + std::to_string(S.reg_nw) +
            ", \"la\": " + std::to_string(S.reg ? S.reg_la : 0) +
-           ", \"reg_bytes\": " + std::to_string(S.reg_bytes) + "}";
+           ", \"reg_bytes\": " + std::to_string(S.reg_bytes) +
+           ", \"tail\": " + (S.tail ? std::string("{\"rows\": ") + std::to_string(S.tail_rows) + ", \"bytes\": " +
+                                       std::to_string(S.tail_bytes) + ", \"depth_down\": [" +
+                                       std::to_string(S.depth_tail[0]) + ", " + std::to_string(S.depth_tail[1]) + ", " +
+                                       std::to_string(S.depth_tail[2]) + "], \"depth_up\": [" +
+                                       std::to_string(S.depth_tail[3]) + ", " + std::to_string(S.depth_tail[4]) + ", " +
+                                       std::to_string(S.depth_tail[5]) + "], \"w\": [" + std::to_string(S.td_w) + ", " +
+                                       std::to_string(S.tu_w) + "], \"nw\": [" + std::to_string(S.td_nw) + ", " +
+                                       std::to_string(S.tu_nw) + "], \"la\": [" + std::to_string(S.td_la) + ", " +
+                                       std::to_string(S.tu_la) + "], \"nnz\": [" + std::to_string(S.tail_nnz[0]) + ", " +
+                                       std::to_string(S.tail_nnz[1]) + ", " + std::to_string(S.tail_nnz[2]) + ", " +
+                                       std::to_string(S.tail_nnz[3]) + ", " + std::to_string(S.tail_nnz[4]) + "]}"
+                                 : std::string("null")) + "}";
   };
   j += ", \"stages\": [";
   for (size_t l = 0; l < lev.size(); ++l) {
@@ -2403,6 +2597,12 @@ static gemslr_status do_setup(gemslr_ctx *c, std::unique_ptr<Engine<T>> &E, int6
   // kernel (tri_kernel 0, no cluster override); GEMSLR_SPLIT=1/2/4 forces it
   opt.split = (prm->tri_kernel != 0 || prm->cluster_ctas > 0) ? 1 : prm->tri_split;
   if (getenv("GEMSLR_SPLIT")) opt.split = atoi(getenv("GEMSLR_SPLIT"));
+  // tail form (DESIGN 6b): boundary rows last in every B_l and the tail sweeps; fp64 with
+  // the register kernel (GEMSLR_TAIL=0 keeps the plain order and sweeps; =2 the order only)
+  opt.tail = (std::is_same<T, double>::value && prm->tri_kernel == 0 && prm->cluster_ctas <= 0) ? 1 : 0;
+  if (opt.split > 1) opt.tail = 0;                                  // a forced split form keeps the plain order
+  if (getenv("GEMSLR_TAIL")) opt.tail = opt.tail && atoi(getenv("GEMSLR_TAIL")) != 0;
+  if (getenv("GEMSLR_TAIL_DIST")) opt.tail_dist = atoi(getenv("GEMSLR_TAIL_DIST"));   // experiments
   if (!c->host_only) opt.sms = num_sm();
   if (c->coord_dim > 0 && c->coords_src) {
     c->coords.assign(c->coords_src, c->coords_src + (size_t)n * c->coord_dim);

@@ -3,6 +3,8 @@
 // Â = Pᵀ A P, cut it into B_l blocks / E_l / F_l / C_last blocks
 // (P:L458-464), factor every block in parallel and
 // build the level-scheduled sweeps.
+#include <chrono>
+#include <cstdio>
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -134,17 +136,19 @@ static int split_for(const std::vector<int64_t> &bl, const SetupOptions &opt, bo
 }
 
 template <typename T>
-void make_stage(const std::vector<int64_t> &bl, const std::vector<Factor<T>> &fac, Stage<T> &S, int Q = 1) {
-  std::vector<int64_t> bounds;
+void make_stage(const std::vector<int64_t> &bl, const std::vector<Factor<T>> &fac, Stage<T> &S, int Q = 1,
+                const std::vector<int64_t> *tails = nullptr) {
+  std::vector<int64_t> bounds, tl;
   std::vector<Factor<T>> facs;
   for (size_t q = 0; q + 1 < bl.size(); ++q) {
     if (bl[q + 1] == bl[q]) continue;
     if (bounds.empty() || bounds.back() != bl[q]) bounds.push_back(bl[q]);
     bounds.push_back(bl[q + 1]);
     facs.push_back(fac[q]);
+    if (tails) tl.push_back((*tails)[q]);
   }
   if (bounds.empty()) bounds.push_back(bl.empty() ? 0 : bl[0]);
-  pack_stage(bounds, facs, S, Q);
+  pack_stage(bounds, facs, S, Q, tails && !facs.empty() ? &tl : nullptr);
 }
 
 }  // namespace
@@ -210,7 +214,13 @@ bool build_host_plan(int64_t n, const int64_t *rowptr, const int32_t *colidx, co
     return false;
   }
   Graph g = build_graph(n, rowptr, colidx);
+  const auto tq0 = std::chrono::steady_clock::now();
+  auto tdbg = [&](const char *what) {
+    if (getenv("GEMSLR_DEBUG_TAIL"))
+      fprintf(stderr, "setup %s %.2f s\n", what, std::chrono::duration<double>(std::chrono::steady_clock::now() - tq0).count());
+  };
   if (!build_structure(g, opt, plan.st, err)) return false;
+  tdbg("structure");
   const Structure &st = plan.st;
   plan.Ahat = permute(n, rowptr, colidx, vals, st);
   const Csr<T> &Ah = plan.Ahat;
@@ -349,11 +359,34 @@ bool build_host_plan(int64_t n, const int64_t *rowptr, const int32_t *colidx, co
     // local stage: owned blocks are contiguous in the local layout
     std::vector<int64_t> lb{plan.lo[l]};
     for (size_t t = 0; t < own_q.size(); ++t) lb.push_back(lb.back() + (bl[own_q[t] + 1] - bl[own_q[t]]));
-    make_stage(lb, own_fac, plan.stage[l], split_for(lb, opt, !std::is_same<T, double>::value));
+    // tail form (plan.hpp TailPack): a block's tail starts at its first row coupled to a
+    // later level (a column of E_l or a row of F_l); every row after it is in the tail
+    std::vector<int64_t> tails;
+    if (opt.tail) {
+      const int64_t a = st.o[l], e = st.o[l + 1];
+      std::vector<char> mark(e - a, 0);
+      for (int64_t i = a; i < e; ++i)                              // F_l: row i has a later column
+        for (int64_t p = Ah.ptr[i]; p < Ah.ptr[i + 1]; ++p)
+          if (Ah.col[p] >= e) { mark[i - a] = 1; break; }
+      for (int64_t j = e; j < n; ++j)                              // E_l: a later row has column i
+        for (int64_t p = Ah.ptr[j]; p < Ah.ptr[j + 1]; ++p)
+          if (Ah.col[p] >= a && Ah.col[p] < e) mark[Ah.col[p] - a] = 1;
+      for (size_t t = 0; t < own_q.size(); ++t) {
+        const int q = own_q[t];
+        int64_t f = bl[q + 1];
+        for (int64_t i = bl[q]; i < bl[q + 1]; ++i)
+          if (mark[i - a]) { f = i; break; }
+        tails.push_back(lb[t] + (f - bl[q]));
+      }
+    }
+    tdbg("factors");
+    make_stage(lb, own_fac, plan.stage[l], split_for(lb, opt, !std::is_same<T, double>::value),
+               opt.tail ? &tails : nullptr);
     plan.E[l] = local_rows(plan.lo[l + 1], nloc, st.o[l], st.o[l + 1], plan.hE[l], false);
     plan.F[l] = local_rows(plan.lo[l], plan.lo[l + 1], st.o[l + 1], n, plan.hF[l], G > 1);
   }
   // C_last: every rank factors and solves all blocks (replicated)
+  tdbg("stages");
   if (!factor_blocks(Ah, st.last, opt, sigma, plan.lastfac, "C_last", err)) return false;
   for (auto &f : plan.lastfac) plan.fac_nnz += f.L.nnz() + f.U.nnz();
   std::vector<int64_t> rel;

@@ -697,6 +697,16 @@ struct RegDev {
   int plev_L, plev_U;          // counter / expectation table sizes
   const unsigned short *sneed; // per record: producer level needed + 1 (0 none)
   const unsigned short *xexp;  // expected exporting slices per producer level
+  int xp;                      // one-CTA imports (RegPack::xmode): records carry exp[32]
+  // tail form (TAIL, plan.hpp TailPack): three sweeps, each with its right-hand side
+  // ra[pos + roff] (- rb[pos + roff]), pos = stage slice * 32 + lane, and its store:
+  // stm 0: st[out] (L sweeps: Ucat position; U sweeps: the row), 1: st[pos + roff]
+  const T *ra[3];
+  const T *rb[3];
+  T *st[3];
+  long long roff[3];
+  int upper[3];
+  int stm[3];
 };
 #ifdef GEMSLR_TRACE
 constexpr bool kRegTrace = true;         // clock64 trace of block 0 (tools/trace_reg.py; build with GEMSLR_TRACE=1)
@@ -786,7 +796,7 @@ struct RegBuf {
 #ifndef SPLIT_EXPORT_FIRST
 #define SPLIT_EXPORT_FIRST 0
 #endif
-template <typename T, int W, int NW, int NB, bool SPLIT = false, int LA = 0>
+template <typename T, int W, int NW, int NB, bool SPLIT = false, int LA = 0, bool TAIL = false>
 __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegDev<T> P, int mode, T *x, T *tmp,
                                                             const int *__restrict__ done) {
   pdl_launch();
@@ -805,7 +815,7 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
   T *ring = reinterpret_cast<T *>(smem);
   const int R = P.ring;
   const int IL = SPLIT ? P.imp_L : 0, PL = SPLIT ? P.plev_L : 0, PLU = SPLIT ? P.plev_L + P.plev_U : 0;
-  unsigned char *tail = smem + (size_t)(R + (SPLIT ? P.imp_L + P.imp_U : 0)) * sizeof(T) + 16;
+  unsigned char *tail = smem + (size_t)(R + P.imp_L + P.imp_U) * sizeof(T) + 16;   // (imports: 0 unless split / xp)
   // split: the import warp's progress, per sweep: producer levels whose values landed
   volatile int *ready = reinterpret_cast<volatile int *>(tail - 16);
   unsigned long long *mb = reinterpret_cast<unsigned long long *>(tail);       // split: one mbarrier per producer level
@@ -821,7 +831,7 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
   __syncthreads();
   const int *bi = bis;
   {                                                                // level table of the block's records (L then U)
-    const int f = bi[0], nl = bi[1] + bi[4];                       // U records follow the L records of the block
+    const int f = bi[0], nl = bi[1] + bi[4] + (TAIL ? bi[7] : 0);  // U records follow the L records of the block
     constexpr int U = 8;                                           // independent loads in flight per thread
     const int nt = blockDim.x;
     int i = tid;
@@ -888,15 +898,27 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
       }
     }
   } else {
-  const bool inplace = mode == TRI_UP && P.xU != nullptr;
+  const bool inplace = !TAIL && mode == TRI_UP && P.xU != nullptr;
   const size_t RB = (size_t)P.rec_bytes;
   using Buf = RegBuf<T, W>;
   constexpr int NV = Buf::NV, W8 = Buf::W8;
 #pragma unroll 1
-  for (int sw = 0; sw < 2; ++sw) {
-    const bool upper = sw == 1;
-    const int r0 = bi[3 * sw], ns = bi[3 * sw + 1], nlev = bi[3 * sw + 2], gbase = bi[10 + sw];
-    const int lvbase = upper ? bi[1] : 0;
+  for (int sw = 0; sw < (TAIL ? 3 : 2); ++sw) {
+    const bool upper = TAIL ? P.upper[sw] != 0 : sw == 1;
+    const int r0 = bi[3 * sw], ns = bi[3 * sw + 1], nlev = bi[3 * sw + 2], gbase = TAIL ? bi[9 + sw] : bi[10 + sw];
+    const int lvbase = TAIL ? (sw == 0 ? 0 : sw == 1 ? bi[1] : bi[1] + bi[4]) : (upper ? bi[1] : 0);
+    // tail form: this sweep's right-hand sides and store (uniform selects, no indexed parameter load)
+    const T *t_ra = nullptr, *t_rb = nullptr;
+    T *t_st = nullptr;
+    long long t_off = 0;
+    int t_stm = 0;
+    if constexpr (TAIL) {
+      t_ra = sw == 0 ? P.ra[0] : sw == 1 ? P.ra[1] : P.ra[2];
+      t_rb = sw == 0 ? P.rb[0] : sw == 1 ? P.rb[1] : P.rb[2];
+      t_st = sw == 0 ? P.st[0] : sw == 1 ? P.st[1] : P.st[2];
+      t_off = sw == 0 ? P.roff[0] : sw == 1 ? P.roff[1] : P.roff[2];
+      t_stm = sw == 0 ? P.stm[0] : sw == 1 ? P.stm[1] : P.stm[2];
+    }
     // Issues the loads of slice s; every address is arithmetic on s, so the
     // warp never waits here and reaches the next barrier right after its slice.
     auto load = [&](Buf &B, int s) {
@@ -910,8 +932,15 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
 #pragma unroll
       for (int j = 0; j < W8; ++j) B.c[j] = ld_na(cp + 32 * j);
       B.out = __ldg(op + lane);
-      if constexpr (SPLIT) B.exp = __ldg(reinterpret_cast<const int *>(op + 32 + 32 * (int)(sizeof(T) / 4)) + lane);
+      if constexpr (SPLIT || TAIL) B.exp = __ldg(reinterpret_cast<const int *>(op + 32 + 32 * (int)(sizeof(T) / 4)) + lane);
+      else B.exp = P.xp ? __ldg(reinterpret_cast<const int *>(op + 32 + 32 * (int)(sizeof(T) / 4)) + lane) : -1;
       const size_t ri = (size_t)(gbase + s) * 32 + lane;
+      if constexpr (TAIL) {                                        // written by earlier kernels or sweeps: L2
+        if (upper) B.dg = ld_nc(reinterpret_cast<const T *>(op + 32) + lane);
+        B.rhs = ld_cg(t_ra + ri + t_off);
+        if (t_rb) B.rhs = B.rhs - ld_cg(t_rb + ri + t_off);
+        return;
+      }
       if (upper) {
         B.dg = ld_nc(reinterpret_cast<const T *>(op + 32) + lane);
         B.rhs = ld_cg(P.mid + ri);                                 // written by this CTA's L sweep
@@ -1002,6 +1031,9 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
     };
     auto publish = [&](const Buf &B, int s, const T &acc) {
       if (B.out >= 0) ring[(s * 32 + lane) & (R - 1)] = acc;
+      if constexpr (!SPLIT) {                                      // imports: far / cross readers (xp, tail form)
+        if (B.exp >= 0) ring[R + B.exp] = acc;
+      }
     };
     // Done with the current level: arrive now at it and at every later level
     // before nxt, the level of this warp's next slice (bar.arrive does not wait),
@@ -1042,6 +1074,11 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
     };
     // The global stores are read only after the sweep-transition barrier.
     auto store = [&](const Buf &B, const T &acc, int s) {
+      if constexpr (TAIL) {
+        if (t_stm) t_st[(size_t)(gbase + s) * 32 + lane + t_off] = acc;
+        else if (B.out >= 0) t_st[B.out] = acc;
+        return;
+      }
       if (upper && P.xP) {                                         // coalesced: U-packed position of the row
         P.xP[(size_t)(gbase + s) * 32 + lane] = acc;
         return;
@@ -1142,7 +1179,7 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
     __threadfence_block();
     reg_sync_all<NW>();                                            // sweep transition: mid / tmp visible, ring free
   }
-  if (mode == TRI_UP && !inplace) {                                // y1 = z1 - U^-1 L^-1 F y2 (Alg. 2 l.9)
+  if (!TAIL && mode == TRI_UP && !inplace) {                       // y1 = z1 - U^-1 L^-1 F y2 (Alg. 2 l.9)
     constexpr int U = 8;                                           // 8 independent rows in flight per thread
     const int i0 = bi[8], i1 = bi[9];
     int i = i0 + tid;

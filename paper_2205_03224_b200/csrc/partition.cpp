@@ -269,6 +269,56 @@ bool build_structure(const Graph &g, const SetupOptions &opt, Structure &st, Err
         });
       }
     }
+    // Boundary rows last (a local reordering of B_l; DESIGN 6b): the rows of
+    // a block adjacent to a later level (E_l's columns, F_l's rows) go after its interior
+    // rows.  Since L is lower and U upper triangular, z1 at those rows then needs only
+    // the U sweep over them (the DOWN's U sweep shrinks to this tail) and L^-1 F_l y2 is
+    // zero before them (the UP's L sweep shrinks to it too; Alg. 2 is unchanged up to
+    // rounding, the oracle follows it literally).  The tail is coloured greedily (a
+    // colour per vertex, distinct from every tail vertex within opt.tail_dist tail edges,
+    // in the order above) and sorted by colour, which keeps the level-schedule depth of
+    // the tail sweeps small (C5 level 0, 32x32x64: U tail 95, L tail 14 levels).
+    if (opt.tail) {
+      std::vector<int32_t> colr(n, -1), seenv(n, -1);
+      for (auto &mem : members) {
+        std::vector<int32_t> head, tl;
+        for (int32_t v : mem) {
+          bool b = false;
+          for (int64_t q = g.ptr[v]; q < g.ptr[v + 1] && !b; ++q) b = insep[g.adj[q]] != 0;
+          (b ? tl : head).push_back(v);
+        }
+        if (tl.empty()) continue;
+        for (int32_t v : tl) colr[v] = -2;                         // tail, not yet coloured
+        std::vector<int32_t> fr, fr2, used;
+        for (int32_t v : tl) {
+          fr.assign(1, v);
+          seenv[v] = v;
+          used.clear();
+          for (int d = 0; d < opt.tail_dist && !fr.empty(); ++d) {
+            fr2.clear();
+            for (int32_t u : fr)
+              for (int64_t q = g.ptr[u]; q < g.ptr[u + 1]; ++q) {
+                const int32_t w = g.adj[q];
+                if (colr[w] == -1 || seenv[w] == v) continue;      // not in this tail, or seen
+                seenv[w] = v;
+                fr2.push_back(w);
+                if (colr[w] >= 0) used.push_back(colr[w]);
+              }
+            fr.swap(fr2);
+          }
+          std::sort(used.begin(), used.end());
+          int c = 0;
+          for (int32_t x : used)
+            if (x == c) ++c;
+            else if (x > c) break;
+          colr[v] = c;
+        }
+        std::stable_sort(tl.begin(), tl.end(), [&](int32_t a, int32_t b) { return colr[a] < colr[b]; });
+        for (int32_t v : tl) colr[v] = -1;
+        mem = head;
+        mem.insert(mem.end(), tl.begin(), tl.end());
+      }
+    }
     std::vector<int64_t> bl{pos};
     for (int q = 0; q < p; ++q) {
       for (int32_t v : members[q]) st.perm.push_back(v);

@@ -195,6 +195,38 @@ struct RegPack {
   std::vector<uint16_t> sneed;                  // per record
   std::vector<uint16_t> xexp;                   // per chunk and sweep: values exported per local level
   int64_t exports = 0;
+  int nsweep = 2;                               // 2: (L, U); 3: the tail form (binfo layout below)
+  bool xmode = false;                           // one-CTA imports: far / cross dependencies at R + i (exp)
+  std::vector<int64_t> sw_slices;               // slices of every sweep (stage-global)
+};
+
+// Tail form of a stage's sweeps (DESIGN 6b; requires every block's rows adjacent to a
+// later level to be its last rows, tails[b] on): with t = L^-1 b1 and ts the tail start,
+//   DOWN: L_hh (head rows), L_t|h (tail rows), U_tt (tail rows): t, and z1 on the tail
+//         only, which is all E_l reads (Alg. 2 l.3-4);
+//   UP:   L_tt on (F_l y2)_tail (u; zero on the head), U_tt and U_h|t on t - [0; u]:
+//         y1 = U^-1 (t - L^-1 F_l y2) = z1 - U^-1 L^-1 F_l y2 (Alg. 2 l.9).
+// Every one of these sweeps has a shallow DAG (C5 level 0: 337 + 14 + 95 and 14 + 95 +
+// 335 levels, against 360 + 456 per full sweep pair); all are exact (rounding only).
+// Record binfo layout (3 sweeps): [3k, 3k+1, 3k+2] first record, slices, levels of sweep
+// k; [9 + k] its first stage slice.  An entry of a row on a value of the other part
+// ("cross": L_t|h's head columns, U_h|t's tail columns) reads a shared-memory slot
+// R + i that the producing lane of an earlier sweep wrote (its record's exp field).
+// Positions: "Ucat" = [U_tt | U_h|t] packed order (t and u live there), L right-hand
+// sides of the DOWN in [L_hh | L_t|h] order.
+template <typename T>
+struct TailPack {
+  bool ok = false;
+  std::vector<int64_t> ts;                      // per block: tail start (absolute)
+  TriPack<T> Lhh, Lth, Utt, Uht, Ltt;
+  RegPack<T> D, U;                              // DOWN (Lhh, Lth, Utt), UP (Ltt, Utt, Uht)
+  int32_t nUtt = 0, nLhh = 0;                   // packed entries of U_tt, of L_hh
+  std::vector<int32_t> ucat;                    // per stage row: Ucat position
+  std::vector<int32_t> lcat;                    // per stage row: DOWN L position ([L_hh | L_t|h])
+  std::vector<int32_t> lrow;                    // per DOWN L position: the row (-1 padding)
+  std::vector<int32_t> uttpos;                  // per stage row: U_tt position (-1 off the tail)
+  std::vector<int32_t> lttpos;                  // per stage row: L_tt position (-1 off the tail)
+  int64_t tail_rows = 0;
 };
 
 template <typename T>
@@ -203,6 +235,7 @@ struct Stage {                                  // the blocks of one level (or o
   TriPack<T> Lp, Up;
   PipePack<T> pipe;
   RegPack<T> reg;
+  TailPack<T> tail;
 };
 
 // Neighbour exchange of one distributed operator: this rank
@@ -257,6 +290,8 @@ struct SetupOptions {
   const double *coords = nullptr;               // n x coord_dim (optional)
   int split = 0;                                // triangular-solve clusters per block: 0 auto, 1 off, 2/4 forced
   int sms = 148;                                // SMs of the device (auto split: blocks x Q must fit)
+  int tail = 1;                                 // boundary rows last in each B_l, tail sweeps (DESIGN 6b)
+  int tail_dist = 4;                            // tail colouring distance (measured: C5 its 63/64/65/64 at 1-4, fastest at 4)
 };
 
 // partition.cpp
@@ -269,7 +304,7 @@ template <typename T> bool ilut(const Csr<T> &B, double tau, int lfil, Factor<T>
 
 // schedule.cpp
 template <typename T> void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, Stage<T> &S,
-                                      int Q = 1);
+                                      int Q = 1, const std::vector<int64_t> *tails = nullptr);
 
 // hostplan.cpp
 template <typename T>

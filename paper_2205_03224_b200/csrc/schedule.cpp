@@ -9,6 +9,7 @@
 // level they are sorted ascending and packed 32 per slice (one row per lane),
 // entries column-major inside the slice so a warp's loads are coalesced.
 #include <algorithm>
+#include <chrono>
 #include <unordered_map>
 
 #include "plan.hpp"
@@ -17,12 +18,18 @@ namespace gemslr {
 
 namespace {
 
+size_t al16_h(size_t b) { return (b + 15) & ~(size_t)15; }
+
 // Q > 1 (split form, plan.hpp RegPack): block b is packed as Q chunks of
 // contiguous rows, each with the levels of the whole block's DAG in which it has
 // rows; "block" b Q + q of the pack is chunk q of block b.
+// Tail sweeps (DESIGN 6b): rsel = 1 keeps the head rows [0, ts_b) of every block, rsel = 2
+// the tail rows [ts_b, n_b).  An entry whose column lies in the other part ("cross": its
+// value comes from an earlier sweep of the launch) is kept when `cross` is set, else
+// dropped (it multiplies a zero); cross entries do not count for the levels.
 template <typename T>
 void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, bool upper, TriPack<T> &P,
-                int Q = 1) {
+                int Q = 1, int rsel = 0, const std::vector<int64_t> *ts = nullptr, bool cross = false) {
   P = TriPack<T>();
   P.blk_lev.push_back(0);
   P.lev_slice.push_back(0);
@@ -32,24 +39,29 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
     const Csr<T> &M = upper ? fac[b].U : fac[b].L;
     const int64_t n = M.n;
     const int64_t row0 = blk[b];
+    const int64_t tb = rsel ? std::min<int64_t>(std::max<int64_t>((*ts)[b], 0), n) : 0;
+    const int64_t i_lo = rsel == 2 ? tb : 0, i_hi = rsel == 1 ? tb : n;   // selected rows (and dependencies)
+    auto in_sel = [&](int64_t j) { return j >= i_lo && j < i_hi; };
     std::vector<int32_t> lev(n, 0);
     int32_t nlev = 0;
     if (!upper) {
-      for (int64_t i = 0; i < n; ++i) {
+      for (int64_t i = i_lo; i < i_hi; ++i) {
         int32_t v = 0;
-        for (int64_t p = M.ptr[i]; p < M.ptr[i + 1]; ++p) v = std::max(v, lev[M.col[p]] + 1);
+        for (int64_t p = M.ptr[i]; p < M.ptr[i + 1]; ++p)
+          if (in_sel(M.col[p])) v = std::max(v, lev[M.col[p]] + 1);
         lev[i] = v;
         nlev = std::max(nlev, v + 1);
       }
     } else {
-      for (int64_t i = n - 1; i >= 0; --i) {
+      for (int64_t i = i_hi - 1; i >= i_lo; --i) {
         int32_t v = 0;
-        for (int64_t p = M.ptr[i] + 1; p < M.ptr[i + 1]; ++p) v = std::max(v, lev[M.col[p]] + 1);
+        for (int64_t p = M.ptr[i] + 1; p < M.ptr[i + 1]; ++p)
+          if (in_sel(M.col[p])) v = std::max(v, lev[M.col[p]] + 1);
         lev[i] = v;
         nlev = std::max(nlev, v + 1);
       }
     }
-    if (n == 0) nlev = 0;
+    if (i_hi <= i_lo) nlev = 0;
     P.max_depth = std::max(P.max_depth, (int)nlev);
     std::vector<int32_t> ll;                                      // L levels (U packing order inside a level)
     if (upper) {
@@ -65,12 +77,12 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
     const int64_t c0 = n * q / Q, c1 = n * (q + 1) / Q;            // this chunk's rows
     // bucket rows by level (ascending row inside a level)
     std::vector<int64_t> cnt(nlev + 1, 0);
-    for (int64_t i = c0; i < c1; ++i) cnt[lev[i] + 1]++;
+    for (int64_t i = std::max(c0, i_lo); i < std::min(c1, i_hi); ++i) cnt[lev[i] + 1]++;
     for (int32_t v = 0; v < nlev; ++v) cnt[v + 1] += cnt[v];
-    std::vector<int64_t> rows(c1 - c0);
+    std::vector<int64_t> rows(cnt[nlev]);
     {
       std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
-      for (int64_t i = c0; i < c1; ++i) rows[pos[lev[i]]++] = i;
+      for (int64_t i = std::max(c0, i_lo); i < std::min(c1, i_hi); ++i) rows[pos[lev[i]]++] = i;
     }
     if (upper) {
       // Inside a U level, order the rows by their L level (ascending row within
@@ -90,7 +102,8 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
         int64_t width = 0;
         for (int64_t t = s0; t < s1; ++t) {
           const int64_t i = rows[t];
-          int64_t len = M.ptr[i + 1] - M.ptr[i] - (upper ? 1 : 0);
+          int64_t len = 0;
+          for (int64_t p = M.ptr[i] + (upper ? 1 : 0); p < M.ptr[i + 1]; ++p) len += (cross || in_sel(M.col[p])) ? 1 : 0;
           width = std::max(width, len);
         }
         const int64_t off = P.slice_off.back();
@@ -106,10 +119,12 @@ void pack_sweep(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
           const int64_t i = rows[t];
           P.slice_row.push_back((int32_t)(row0 + i));
           const int64_t pb = M.ptr[i] + (upper ? 1 : 0);
-          for (int64_t p = pb, e = 0; p < M.ptr[i + 1]; ++p, ++e) {
+          for (int64_t p = pb, e = 0; p < M.ptr[i + 1]; ++p) {
+            if (!cross && !in_sel(M.col[p])) continue;
             P.col[off + 32 * e + lane] = (int32_t)(row0 + M.col[p]);
             P.val[off + 32 * e + lane] = M.val[p];
             P.nnz_real++;
+            ++e;
           }
           if (upper) P.diag.push_back(M.val[M.ptr[i]]);
         }
@@ -319,37 +334,44 @@ static std::pair<int, int> refine_record(uint8_t *base, int W, int wo) {
 // Register-prefetched records of the two sweeps (RegPack, k_tri_reg).  Q > 1:
 // the split form (plan.hpp), with the chunks of pack_sweep(Q) as its "blocks".
 template <typename T>
-void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPack<T> &Up, RegPack<T> &P, int Q = 1) {
+// Tail form (DESIGN 6b): `sweeps` of any number (each L or U per `up`), Q = 1 only; `lout`
+// gives the L sweeps' output positions (per stage row) instead of the U sweep's.
+void pack_reg(const std::vector<int64_t> &blk, const std::vector<const TriPack<T> *> &SW, const std::vector<char> &up,
+              RegPack<T> &P, int Q = 1, const std::vector<int32_t> *lout = nullptr) {
   P = RegPack<T>();
   P.Q = Q;
+  const int NSW = (int)SW.size();
+  P.nsweep = NSW;
+  if (NSW != 2 && Q > 1) return;                                   // split form: the (L, U) pair only
+  if (NSW > 3) return;
   const bool split = Q > 1;
+  const TriPack<T> &Lp = *SW[0];
+  const TriPack<T> &Up = *SW[NSW - 1];
   static const bool lookahead = getenv("GEMSLR_NO_LOOKAHEAD") == nullptr;   // experiments
   const size_t nblk = blk.size() - 1;
   const size_t nb = nblk * (size_t)Q;                              // pack "blocks" (chunks)
   const int64_t R0 = blk.front(), NR = blk.back() - blk.front();
   P.lslices = (int64_t)Lp.slice_row.size() / 32;
   P.uslices = (int64_t)Up.slice_row.size() / 32;
-  for (const TriPack<T> *S : {&Lp, &Up})
+  for (int k = 0; k < NSW; ++k) P.sw_slices.push_back((int64_t)SW[k]->slice_row.size() / 32);
+  for (const TriPack<T> *S : SW)
     for (size_t s = 0; s + 1 < S->slice_off.size(); ++s)
       P.wmax = std::max(P.wmax, (int)((S->slice_off[s + 1] - S->slice_off[s]) / 32));
   P.W = reg_width(std::max(P.wmax, 1));
   if (P.W == 0) return;
   const int W = P.W, W8 = (W + 7) / 8, VE = 16 / (int)sizeof(T);
-  P.rec_bytes = reg_record_bytes<T>(W, split);
-  P.nrec = P.lslices + P.uslices;
-  P.data.assign((size_t)P.nrec * P.rec_bytes, 0);
-  std::vector<int32_t> upos(NR, -1);
-  P.lpos.assign(NR, -1);
-  for (int64_t s = 0; s < P.lslices; ++s)
-    for (int lane = 0; lane < 32; ++lane) {
-      const int32_t row = Lp.slice_row[s * 32 + lane];
-      if (row >= 0) P.lpos[row - R0] = (int32_t)(s * 32 + lane);
-    }
-  for (int64_t s = 0; s < P.uslices; ++s)
-    for (int lane = 0; lane < 32; ++lane) {
-      const int32_t row = Up.slice_row[s * 32 + lane];
-      if (row >= 0) upos[row - R0] = (int32_t)(s * 32 + lane);
-    }
+  P.nrec = 0;
+  for (int64_t v : P.sw_slices) P.nrec += v;
+  // packed position (stage slice * 32 + lane) of every row in each sweep
+  std::vector<std::vector<int32_t>> spos(NSW, std::vector<int32_t>(NR, -1));
+  for (int k = 0; k < NSW; ++k)
+    for (int64_t s = 0; s < P.sw_slices[k]; ++s)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int32_t row = SW[k]->slice_row[s * 32 + lane];
+        if (row >= 0) spos[k][row - R0] = (int32_t)(s * 32 + lane);
+      }
+  P.lpos = spos[0];
+  const std::vector<int32_t> &upos = spos[NSW - 1];
   // chunk of every stage row (the chunk's rows: pack_sweep's n q / Q split)
   std::vector<int32_t> chunk(NR, 0);
   for (size_t b = 0; b < nblk; ++b) {
@@ -358,9 +380,9 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
       for (int64_t i = n * q / Q; i < n * (q + 1) / Q; ++i) chunk[blk[b] - R0 + i] = (int32_t)(b * Q + q);
   }
   // slice -> (chunk, local level) of each sweep, for the producer side of imports
-  std::vector<int32_t> sl_chunk[2], sl_lev[2];
-  for (int sweep = 0; sweep < 2; ++sweep) {
-    const TriPack<T> &S = sweep ? Up : Lp;
+  std::vector<int32_t> sl_chunk[3], sl_lev[3];
+  for (int sweep = 0; sweep < NSW; ++sweep) {
+    const TriPack<T> &S = *SW[sweep];
     const int64_t ns = (int64_t)S.slice_row.size() / 32;
     sl_chunk[sweep].assign(ns, 0);
     sl_lev[sweep].assign(ns, 0);
@@ -375,30 +397,99 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
   // dependency distance (level end - dependency position)
   int64_t need = 1;
   for (size_t b = 0; b < nb; ++b)
-    for (int sweep = 0; sweep < 2; ++sweep) {
-      const TriPack<T> &S = sweep ? Up : Lp;
+    for (int sweep = 0; sweep < NSW; ++sweep) {
+      const TriPack<T> &S = *SW[sweep];
       const int32_t lv0 = S.blk_lev[b], lv1 = S.blk_lev[b + 1];
       const int32_t sb0 = S.lev_slice[lv0];
       for (int32_t v = lv0; v < lv1; ++v) {
         const int64_t send = S.lev_slice[v + 1] - sb0;
         for (int64_t g = S.slice_off[S.lev_slice[v]]; g < S.slice_off[S.lev_slice[v + 1]]; ++g) {
           const int32_t dep = S.col[g];
-          if (dep < 0 || chunk[dep - R0] != (int32_t)b) continue;
-          const int32_t q = (sweep ? upos[dep - R0] : P.lpos[dep - R0]) - sb0 * 32;
+          if (dep < 0 || chunk[dep - R0] != (int32_t)b || spos[sweep][dep - R0] < 0) continue;   // (cross: imports)
+          const int32_t q = spos[sweep][dep - R0] - sb0 * 32;
           need = std::max(need, send * 32 - q);
         }
       }
     }
   P.ring = 1024;
   while (P.ring < need && P.ring < REG_RING_BYTES / (int)sizeof(T)) P.ring *= 2;
+  // import mode: the tail form, or a one-CTA pack whose dependencies reach further back
+  // than the largest ring (a tail-ordered block's full sweeps)
+  const bool xmode = NSW == 3 || (!split && need > REG_RING_BYTES / (int)sizeof(T));
+  P.xmode = xmode;
+  const bool xf = split || xmode;                                  // records carry exp[32]
+  P.rec_bytes = reg_record_bytes<T>(W, xf);
+  P.data.assign((size_t)P.nrec * P.rec_bytes, 0);
+  // tail form: a dependency further back than the ring ("far") or on an earlier sweep
+  // ("cross") reads an import slot R + i that its producing lane writes (exp); R is
+  // chosen to minimise R + imports (the shared memory of the block's values)
+  auto prod_of = [&](int sweep, int32_t dep) {                     // the latest sweep <= `sweep` holding the row
+    for (int k = sweep; k >= 0; --k)
+      if (spos[k][dep - R0] >= 0) return k;
+    return -1;
+  };
+  auto xkey = [&](int ps, int32_t dep) { return (int64_t)ps * (NR + 1) + (dep - R0); };
+  // (producer sweep, dep row) -> widest window of its readers (-1: read by a later sweep,
+  // -2: not read); rows belong to one block, so the tables are stage-wide
+  std::vector<int64_t> dwin;
+  if (xmode) {
+    dwin.assign((size_t)NSW * (NR + 1), -2);
+    for (size_t b = 0; b < nb; ++b)
+      for (int sweep = 0; sweep < NSW; ++sweep) {
+        const TriPack<T> &S = *SW[sweep];
+        const int32_t lv0 = S.blk_lev[b], lv1 = S.blk_lev[b + 1];
+        const int32_t sb0 = S.lev_slice[lv0];
+        for (int32_t v = lv0; v < lv1; ++v) {
+          const int64_t send = S.lev_slice[v + 1] - sb0;
+          for (int64_t g = S.slice_off[S.lev_slice[v]]; g < S.slice_off[S.lev_slice[v + 1]]; ++g) {
+            const int32_t dep = S.col[g];
+            if (dep < 0) continue;
+            if (spos[sweep][dep - R0] < 0) {
+              const int ps = prod_of(sweep - 1, dep);
+              if (ps < 0) return;                                  // read but never computed
+              dwin[xkey(ps, dep)] = -1;
+              continue;
+            }
+            int64_t &w = dwin[xkey(sweep, dep)];
+            if (w == -2) w = 0;
+            if (w >= 0) w = std::max<int64_t>(w, send * 32 - (spos[sweep][dep - R0] - sb0 * 32));
+          }
+        }
+      }
+    int64_t maxsl = 0;                                             // level table entries of the largest block
+    for (size_t b = 0; b < nb; ++b) {
+      int64_t t = 0;
+      for (const TriPack<T> *S : SW) t += S->lev_slice[S->blk_lev[b + 1]] - S->lev_slice[S->blk_lev[b]];
+      maxsl = std::max(maxsl, t);
+    }
+    int best = -1;
+    int64_t bestc = 0;
+    for (int r = 1024; r <= REG_RING_BYTES / (int)sizeof(T); r *= 2) {
+      int64_t imp = 0;
+      for (size_t b = 0; b < nb; ++b) {
+        int64_t c = 0;
+        for (int k = 0; k < NSW; ++k)
+          for (int64_t i = blk[b] - R0; i < blk[b + 1] - R0; ++i) {
+            const int64_t w = dwin[xkey(k, (int32_t)(i + R0))];
+            c += (w == -1 || w > r) ? 1 : 0;
+          }
+        imp = std::max(imp, c);
+      }
+      const int64_t bytes = (r + imp) * (int64_t)sizeof(T) + 16 + (int64_t)al16_h((size_t)maxsl * 2);
+      if (r + imp > 65535 || bytes > 232448 - 1024 - 2048) continue;
+      if (best < 0 || r + imp <= bestc) { best = r; bestc = r + imp; }
+    }
+    if (best < 0) return;
+    P.ring = best;
+  }
   const int R = P.ring;
   // look-ahead (plan.hpp REG_LA): every row's entries on the previous level of its chunk
   // (in-chunk dependencies only; imports are always ready before) must fit REG_LA columns
   {
     int maxnew = 0;
     for (size_t b = 0; b < nb; ++b)
-      for (int sweep = 0; sweep < 2; ++sweep) {
-        const TriPack<T> &S = sweep ? Up : Lp;
+      for (int sweep = 0; sweep < NSW; ++sweep) {
+        const TriPack<T> &S = *SW[sweep];
         for (int32_t v = S.blk_lev[b]; v < S.blk_lev[b + 1]; ++v)
           for (int32_t sl = S.lev_slice[v]; sl < S.lev_slice[v + 1]; ++sl) {
             const int w = (int)((S.slice_off[sl + 1] - S.slice_off[sl]) / 32);
@@ -406,8 +497,8 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
               int c = 0;
               for (int e = 0; e < w; ++e) {
                 const int32_t dep = S.col[S.slice_off[sl] + 32 * e + lane];
-                if (dep < 0 || chunk[dep - R0] != (int32_t)b) continue;
-                const int32_t pd = sweep ? upos[dep - R0] : P.lpos[dep - R0];
+                if (dep < 0 || chunk[dep - R0] != (int32_t)b || spos[sweep][dep - R0] < 0) continue;
+                const int32_t pd = spos[sweep][dep - R0];
                 if (sl_lev[sweep][pd / 32] >= (v - S.blk_lev[b]) - 1) c++;
               }
               maxnew = std::max(maxnew, c);
@@ -422,9 +513,10 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
     // 227 -> 223): so only stages with fewer than 2 slices per level on average.
     int64_t sl = 0, lv = 0;
     for (size_t b = 0; b < nb; ++b) {
-      sl += (Lp.lev_slice[Lp.blk_lev[b + 1]] - Lp.lev_slice[Lp.blk_lev[b]]) +
-            (Up.lev_slice[Up.blk_lev[b + 1]] - Up.lev_slice[Up.blk_lev[b]]);
-      lv += (Lp.blk_lev[b + 1] - Lp.blk_lev[b]) + (Up.blk_lev[b + 1] - Up.blk_lev[b]);
+      for (const TriPack<T> *S : SW) {
+        sl += S->lev_slice[S->blk_lev[b + 1]] - S->lev_slice[S->blk_lev[b]];
+        lv += S->blk_lev[b + 1] - S->blk_lev[b];
+      }
     }
     const double K = lv > 0 ? (double)sl / (double)lv : 1.0;
     P.la = (lookahead && maxnew <= REG_LA && W > REG_LA && K < 2.0) ? REG_LA : 0;
@@ -457,6 +549,35 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
     }
     if ((int64_t)R + P.imp_L + P.imp_U > 65535) return;
   }
+  // tail form: the far and cross rows of every block get import slots, numbered in the
+  // order the consumers' records first need them; the producer is the latest sweep up to
+  // the consumer's holding the row
+  std::vector<int32_t> xmap;                                       // (producer sweep, row) -> index in its block
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> xprod;     // per block: (producer sweep, position)
+  auto is_imp = [&](size_t, int ps, int32_t dep) {
+    const int64_t w = dwin[xkey(ps, dep)];
+    return w == -1 || w > R;
+  };
+  if (xmode) {
+    xmap.assign((size_t)NSW * (NR + 1), -1);
+    xprod.resize(nb);
+    for (size_t b = 0; b < nb; ++b)
+      for (int sweep = 0; sweep < NSW; ++sweep) {
+        const TriPack<T> &S = *SW[sweep];
+        for (int64_t g = S.slice_off[S.lev_slice[S.blk_lev[b]]]; g < S.slice_off[S.lev_slice[S.blk_lev[b + 1]]]; ++g) {
+          const int32_t dep = S.col[g];
+          if (dep < 0) continue;
+          const int ps = sweep > 0 && spos[sweep][dep - R0] < 0 ? prod_of(sweep - 1, dep) : sweep;
+          if (ps < 0) return;                                      // read but never computed
+          if (!is_imp(b, ps, dep)) continue;
+          if (xmap[xkey(ps, dep)] >= 0) continue;
+          xmap[xkey(ps, dep)] = (int32_t)xprod[b].size();
+          xprod[b].push_back({ps, spos[ps][dep - R0]});
+        }
+      }
+    for (size_t b = 0; b < nb; ++b) P.imp_L = std::max(P.imp_L, (int)xprod[b].size());
+    if ((int64_t)R + P.imp_L > 65535) return;
+  }
   // per chunk and sweep: stage row -> import index (only rows imported by that chunk)
   std::vector<std::unordered_map<int32_t, int32_t>> impmap[2];
   if (split)
@@ -465,9 +586,118 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
       for (size_t b = 0; b < nb; ++b)
         for (size_t i = 0; i < imp[sweep][b].size(); ++i) impmap[sweep][b][imp[sweep][b][i].first] = (int32_t)i;
     }
-  std::vector<int64_t> rec_of[2];                                  // stage slice -> record
-  rec_of[0].assign(P.lslices, -1);
-  rec_of[1].assign(P.uslices, -1);
+  std::vector<int64_t> rec_of[3];                                  // stage slice -> record
+  for (int k = 0; k < NSW; ++k) rec_of[k].assign(P.sw_slices[k], -1);
+  // Records are numbered and their bookkeeping done in order; their contents are then
+  // filled in parallel (independent records).
+  struct Task { int64_t rec; int32_t b; int sweep; int32_t v, s, lv0, sb0, send; };
+  std::vector<Task> tasks;
+  tasks.reserve((size_t)P.nrec);
+  auto fill = [&](const Task &tk, int64_t &nearc, int64_t &farc) {
+    const int64_t rec = tk.rec;
+    const size_t b = (size_t)tk.b;
+    const int sweep = tk.sweep;
+    const int32_t v = tk.v, s = tk.s, lv0 = tk.lv0, sb0 = tk.sb0, send = tk.send;
+    const TriPack<T> &S = *SW[sweep];
+    const bool upper = up[sweep] != 0;
+    const int w = (int)((S.slice_off[s + 1] - S.slice_off[s]) / 32);
+    uint8_t *base = P.data.data() + (size_t)rec * P.rec_bytes;
+    T *val = reinterpret_cast<T *>(base);
+    uint16_t *col = reinterpret_cast<uint16_t *>(base + (size_t)W * 32 * sizeof(T));
+    int32_t *out = reinterpret_cast<int32_t *>(col + (size_t)W8 * 32 * 8);
+    T *rdiag = reinterpret_cast<T *>(out + 32);
+    if (xf) {
+      int32_t *exp = reinterpret_cast<int32_t *>(rdiag + 32);
+      for (int lane = 0; lane < 32; ++lane) exp[lane] = -1;
+    }
+    // entries of every lane with their ring slots, split for the look-ahead:
+    // "new" = a dependency in the immediately preceding level of this chunk
+    // (needs that level's barrier), "old" = older levels and imports (ready after
+    // the barrier before it, so k_tri_reg sums them while the previous level runs)
+    struct Ent { T v; uint16_t slot; bool nw; };
+    std::vector<Ent> ent[32];
+    for (int lane = 0; lane < 32; ++lane) {
+      const int32_t row = S.slice_row[(int64_t)s * 32 + lane];
+      out[lane] = row < 0 ? -1 : (upper ? row : lout ? (*lout)[row - R0] : upos[row - R0]);
+      rdiag[lane] = upper ? T(1) / S.diag[(int64_t)s * 32 + lane] : T(1);
+      for (int e = 0; e < w; ++e) {
+        const int64_t g = S.slice_off[s] + 32 * e + lane;
+        const int32_t dep = S.col[g];
+        if (dep < 0) continue;
+        if (split && chunk[dep - R0] != (int32_t)b) {         // an import (DSMEM from the neighbour chunk)
+          const int32_t ii = impmap[sweep][b].at(dep - (int32_t)R0);
+          const int32_t pslice = imp[sweep][b][ii].second;
+          (void)pslice;
+          ent[lane].push_back(Ent{S.val[g], (uint16_t)(R + (upper ? P.imp_L : 0) + ii), false});
+          nearc++;
+          continue;
+        }
+        if (NSW == 3 && spos[sweep][dep - R0] < 0) {           // cross: from an earlier sweep
+          ent[lane].push_back(Ent{S.val[g], (uint16_t)(R + xmap[xkey(prod_of(sweep - 1, dep), dep)]), false});
+          nearc++;
+          continue;
+        }
+        const int32_t pd = spos[sweep][dep - R0];
+        const int32_t q = pd - sb0 * 32;                  // block-relative position
+        const bool isnew = sl_lev[sweep][pd / 32] >= (v - lv0) - 1;
+        if (xmode && is_imp(b, sweep, dep)) {               // far: an import slot
+          ent[lane].push_back(Ent{S.val[g], (uint16_t)(R + xmap[xkey(sweep, dep)]), isnew});
+          nearc++;
+          continue;
+        }
+        if ((int64_t)send * 32 - 1 - q < R) { ent[lane].push_back(Ent{S.val[g], (uint16_t)(q & (R - 1)), isnew}); nearc++; }
+        else { farc++; }
+      }
+    }
+    // look-ahead groups: columns [0, wo) old, [wo, W) new (wo = W - la); a lane's
+    // old entries beyond wo fill its unused new columns (old + new <= W)
+    const int wo = W - P.la;
+    std::vector<Ent> grp[2][32];
+    for (int lane = 0; lane < 32; ++lane) {
+      for (const Ent &en : ent[lane])
+        if (P.la == 0 || (!en.nw && (int)grp[0][lane].size() < wo)) grp[0][lane].push_back(en);
+        else grp[1][lane].push_back(en);
+    }
+    // Column e of the slice is one shared-memory gather of 32 lanes (8 or 16
+    // bytes each); order each lane's entries (any order gives the same sum up
+    // to rounding) so that every column spreads its distinct slots over the
+    // bank groups: greedily give each lane the entry whose group is least
+    // used in the column so far.
+    // Counted per part of the warp the LDS serves in one pass (16 lanes for
+    // 8-byte slots, 8 for 16-byte; see refine_record).
+    const int G = (int)(128 / sizeof(T));                 // bank groups of one 128-byte wavefront
+    for (int e = 0; e < W; ++e) {
+      std::vector<int> cnt(G, 0);
+      std::vector<uint16_t> seen;
+      for (int lane = 0; lane < 32; ++lane) {
+        if (lane % G == 0) {                              // a new part of the warp
+          std::fill(cnt.begin(), cnt.end(), 0);
+          seen.clear();
+        }
+        uint16_t slot = (uint16_t)(R - 1);
+        T v = T(0);
+        auto &L = grp[P.la == 0 || e < wo ? 0 : 1][lane];
+        if (!L.empty()) {
+          size_t best = 0;
+          int bc = 1 << 30;
+          for (size_t k = 0; k < L.size(); ++k) {
+            const bool dup = std::find(seen.begin(), seen.end(), L[k].slot) != seen.end();
+            const int c = dup ? -1 : cnt[L[k].slot % G];          // a repeated slot is a broadcast
+            if (c < bc) { bc = c; best = k; }
+          }
+          slot = L[best].slot;
+          v = L[best].v;
+          L.erase(L.begin() + (long)best);
+        }
+        if (std::find(seen.begin(), seen.end(), slot) == seen.end()) {
+          seen.push_back(slot);
+          cnt[slot % G]++;
+        }
+        val[((e / VE) * 32 + lane) * VE + e % VE] = v;
+        col[((e / 8) * 32 + lane) * 8 + e % 8] = slot;
+      }
+    }
+  };
   int64_t rec = 0;
   for (size_t b = 0; b < nb; ++b) {
     int32_t info[REG_BINFO_INTS] = {0};
@@ -476,119 +706,54 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
     const int qq = (int)(b % (size_t)Q);
     info[8] = (int32_t)(blk[bk] + nbk * qq / Q);                   // this chunk's rows
     info[9] = (int32_t)(blk[bk] + nbk * (qq + 1) / Q);
-    for (int sweep = 0; sweep < 2; ++sweep) {
-      const TriPack<T> &S = sweep ? Up : Lp;
-      const bool upper = sweep == 1;
+    for (int sweep = 0; sweep < NSW; ++sweep) {
+      const TriPack<T> &S = *SW[sweep];
+      const bool upper = up[sweep] != 0;
       const int32_t lv0 = S.blk_lev[b], lv1 = S.blk_lev[b + 1];
       const int32_t sb0 = S.lev_slice[lv0];
       info[3 * sweep + 0] = (int32_t)rec;
       info[3 * sweep + 1] = S.lev_slice[lv1] - sb0;
       info[3 * sweep + 2] = lv1 - lv0;
-      info[6 + sweep] = (int32_t)P.lev_off.size();
-      info[10 + sweep] = sb0;
+      if (NSW == 2) {
+        info[6 + sweep] = (int32_t)P.lev_off.size();
+        info[10 + sweep] = sb0;
+      } else {
+        info[9 + sweep] = sb0;                                     // tail layout (plan.hpp)
+      }
       P.max_levels = std::max(P.max_levels, lv1 - lv0);
       int need_pref = -1;                                          // split: producer level needed so far
       for (int32_t v = lv0; v < lv1; ++v) {
         P.lev_off.push_back((int32_t)rec);
         const int32_t send = S.lev_slice[v + 1] - sb0;     // level end (block-relative slice)
         for (int32_t s = S.lev_slice[v]; s < S.lev_slice[v + 1]; ++s, ++rec) {
-          const int w = (int)((S.slice_off[s + 1] - S.slice_off[s]) / 32);
-          uint8_t *base = P.data.data() + (size_t)rec * P.rec_bytes;
-          T *val = reinterpret_cast<T *>(base);
-          uint16_t *col = reinterpret_cast<uint16_t *>(base + (size_t)W * 32 * sizeof(T));
-          int32_t *out = reinterpret_cast<int32_t *>(col + (size_t)W8 * 32 * 8);
-          T *rdiag = reinterpret_cast<T *>(out + 32);
-          if (split) {
-            int32_t *exp = reinterpret_cast<int32_t *>(rdiag + 32);
-            for (int lane = 0; lane < 32; ++lane) exp[lane] = -1;
-          }
           rec_of[sweep][s] = rec;
           if (v - lv0 > 65535) return;
           P.slev.push_back((uint16_t)(v - lv0));
-          // entries of every lane with their ring slots, split for the look-ahead:
-          // "new" = a dependency in the immediately preceding level of this chunk
-          // (needs that level's barrier), "old" = older levels and imports (ready after
-          // the barrier before it, so k_tri_reg sums them while the previous level runs)
-          struct Ent { T v; uint16_t slot; bool nw; };
-          std::vector<Ent> ent[32];
-          for (int lane = 0; lane < 32; ++lane) {
-            const int32_t row = S.slice_row[(int64_t)s * 32 + lane];
-            out[lane] = row < 0 ? -1 : (upper ? row : upos[row - R0]);
-            rdiag[lane] = upper ? T(1) / S.diag[(int64_t)s * 32 + lane] : T(1);
-            for (int e = 0; e < w; ++e) {
-              const int64_t g = S.slice_off[s] + 32 * e + lane;
+          if (split) {                                             // producer level of the imports read so far
+            const int w = (int)((S.slice_off[s + 1] - S.slice_off[s]) / 32);
+            for (int64_t g = S.slice_off[s]; g < S.slice_off[s] + 32 * w; ++g) {
               const int32_t dep = S.col[g];
-              if (dep < 0) continue;
-              if (split && chunk[dep - R0] != (int32_t)b) {         // an import (DSMEM from the neighbour chunk)
-                const int32_t ii = impmap[sweep][b].at(dep - (int32_t)R0);
-                const int32_t pslice = imp[sweep][b][ii].second;
-                need_pref = std::max(need_pref, sl_lev[sweep][pslice]);
-                ent[lane].push_back(Ent{S.val[g], (uint16_t)(R + (upper ? P.imp_L : 0) + ii), false});
-                P.near++;
-                continue;
-              }
-              const int32_t pd = upper ? upos[dep - R0] : P.lpos[dep - R0];
-              const int32_t q = pd - sb0 * 32;                  // block-relative position
-              const bool isnew = sl_lev[sweep][pd / 32] >= (v - lv0) - 1;
-              if ((int64_t)send * 32 - 1 - q < R) { ent[lane].push_back(Ent{S.val[g], (uint16_t)(q & (R - 1)), isnew}); P.near++; }
-              else { P.far++; }
+              if (dep < 0 || chunk[dep - R0] == (int32_t)b) continue;
+              auto it = impmap[sweep][b].find(dep - (int32_t)R0);
+              if (it == impmap[sweep][b].end()) return;
+              need_pref = std::max(need_pref, sl_lev[sweep][imp[sweep][b][it->second].second]);
             }
+            P.sneed.push_back((uint16_t)(need_pref + 1));
           }
-          if (split) P.sneed.push_back((uint16_t)(need_pref + 1));
-          // look-ahead groups: columns [0, wo) old, [wo, W) new (wo = W - la); a lane's
-          // old entries beyond wo fill its unused new columns (old + new <= W)
-          const int wo = W - P.la;
-          std::vector<Ent> grp[2][32];
-          for (int lane = 0; lane < 32; ++lane) {
-            for (const Ent &en : ent[lane])
-              if (P.la == 0 || (!en.nw && (int)grp[0][lane].size() < wo)) grp[0][lane].push_back(en);
-              else grp[1][lane].push_back(en);
-          }
-          // Column e of the slice is one shared-memory gather of 32 lanes (8 or 16
-          // bytes each); order each lane's entries (any order gives the same sum up
-          // to rounding) so that every column spreads its distinct slots over the
-          // bank groups: greedily give each lane the entry whose group is least
-          // used in the column so far.
-          // Counted per part of the warp the LDS serves in one pass (16 lanes for
-          // 8-byte slots, 8 for 16-byte; see refine_record).
-          const int G = (int)(128 / sizeof(T));                 // bank groups of one 128-byte wavefront
-          for (int e = 0; e < W; ++e) {
-            std::vector<int> cnt(G, 0);
-            std::vector<uint16_t> seen;
-            for (int lane = 0; lane < 32; ++lane) {
-              if (lane % G == 0) {                              // a new part of the warp
-                std::fill(cnt.begin(), cnt.end(), 0);
-                seen.clear();
-              }
-              uint16_t slot = (uint16_t)(R - 1);
-              T v = T(0);
-              auto &L = grp[P.la == 0 || e < wo ? 0 : 1][lane];
-              if (!L.empty()) {
-                size_t best = 0;
-                int bc = 1 << 30;
-                for (size_t k = 0; k < L.size(); ++k) {
-                  const bool dup = std::find(seen.begin(), seen.end(), L[k].slot) != seen.end();
-                  const int c = dup ? -1 : cnt[L[k].slot % G];          // a repeated slot is a broadcast
-                  if (c < bc) { bc = c; best = k; }
-                }
-                slot = L[best].slot;
-                v = L[best].v;
-                L.erase(L.begin() + (long)best);
-              }
-              if (std::find(seen.begin(), seen.end(), slot) == seen.end()) {
-                seen.push_back(slot);
-                cnt[slot % G]++;
-              }
-              val[((e / VE) * 32 + lane) * VE + e % VE] = v;
-              col[((e / 8) * 32 + lane) * 8 + e % 8] = slot;
-            }
-          }
+          tasks.push_back(Task{rec, (int32_t)b, sweep, v, s, lv0, sb0, send});
         }
       }
       P.lev_off.push_back((int32_t)rec);
     }
     P.binfo.insert(P.binfo.end(), info, info + REG_BINFO_INTS);
-    P.max_block_slices = std::max(P.max_block_slices, info[1] + info[4]);
+    P.max_block_slices = std::max(P.max_block_slices, info[1] + info[4] + (NSW == 3 ? info[7] : 0));
+  }
+  {
+    int64_t nearc = 0, farc = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(+ : nearc, farc)
+    for (int64_t t = 0; t < (int64_t)tasks.size(); ++t) fill(tasks[(size_t)t], nearc, farc);
+    P.near += nearc;
+    P.far += farc;
   }
   if (split) {
     // exports: the producer lane of every import, and per producer chunk and sweep
@@ -629,6 +794,18 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
       if (qq + 1 < Q) { info[14] = xoff[1][b + 1]; info[15] = Up.blk_lev[b + 2] - Up.blk_lev[b + 1]; }
     }
   }
+  if (xmode) {                                                    // producer lanes of the imports
+    for (size_t b = 0; b < nb; ++b)
+      for (size_t i = 0; i < xprod[b].size(); ++i) {
+        const int ps = xprod[b][i].first, pd = xprod[b][i].second;
+        const int64_t r = rec_of[ps][pd / 32];
+        uint8_t *base = P.data.data() + (size_t)r * P.rec_bytes;
+        int32_t *exp = reinterpret_cast<int32_t *>(base + (size_t)W * 32 * sizeof(T) + (size_t)W8 * 512 + 32 * 4 +
+                                                   32 * sizeof(T));
+        exp[pd % 32] = (int32_t)i;
+        P.exports++;
+      }
+  }
   {
     long long cb = 0, ca = 0;
 #pragma omp parallel for schedule(dynamic, 256) reduction(+ : cb, ca)
@@ -647,17 +824,78 @@ void pack_reg(const std::vector<int64_t> &blk, const TriPack<T> &Lp, const TriPa
 
 }  // namespace
 
+// Tail form of the sweeps (plan.hpp TailPack, DESIGN 6b), one CTA per block.
+template <typename T>
+void pack_tail(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, const std::vector<int64_t> &tails,
+               TailPack<T> &TP) {
+  TP = TailPack<T>();
+  const size_t nb = fac.size();
+  if (tails.size() != nb || nb == 0) return;
+  std::vector<int64_t> ts(nb);
+  for (size_t b = 0; b < nb; ++b) {
+    ts[b] = std::min(std::max(tails[b], blk[b]), blk[b + 1]) - blk[b];
+    TP.tail_rows += blk[b + 1] - blk[b] - ts[b];
+  }
+  TP.ts = tails;
+  pack_sweep(blk, fac, false, TP.Lhh, 1, 1, &ts);                 // head rows of L
+  pack_sweep(blk, fac, false, TP.Lth, 1, 2, &ts, true);           // tail rows of L (head columns: cross)
+  pack_sweep(blk, fac, true, TP.Utt, 1, 2, &ts);                  // tail rows of U
+  pack_sweep(blk, fac, true, TP.Uht, 1, 1, &ts, true);            // head rows of U (tail columns: cross)
+  pack_sweep(blk, fac, false, TP.Ltt, 1, 2, &ts);                 // tail rows of L, head columns dropped
+  const int64_t R0 = blk.front(), NR = blk.back() - blk.front();
+  auto posof = [&](const TriPack<T> &S, std::vector<int32_t> &pos, int32_t off) {
+    for (size_t q = 0; q < S.slice_row.size(); ++q)
+      if (S.slice_row[q] >= 0) pos[S.slice_row[q] - R0] = off + (int32_t)q;
+  };
+  const int32_t nUtt = (int32_t)TP.Utt.slice_row.size(), nLhh = (int32_t)TP.Lhh.slice_row.size();
+  TP.nUtt = nUtt;
+  TP.nLhh = nLhh;
+  TP.ucat.assign(NR, -1);
+  posof(TP.Utt, TP.ucat, 0);
+  posof(TP.Uht, TP.ucat, nUtt);
+  TP.lcat.assign(NR, -1);
+  posof(TP.Lhh, TP.lcat, 0);
+  posof(TP.Lth, TP.lcat, nLhh);
+  TP.uttpos.assign(NR, -1);
+  posof(TP.Utt, TP.uttpos, 0);
+  TP.lttpos.assign(NR, -1);
+  posof(TP.Ltt, TP.lttpos, 0);
+  TP.lrow = TP.Lhh.slice_row;
+  TP.lrow.insert(TP.lrow.end(), TP.Lth.slice_row.begin(), TP.Lth.slice_row.end());
+  const auto c0 = std::chrono::steady_clock::now();
+  pack_reg(blk, {&TP.Lhh, &TP.Lth, &TP.Utt}, {0, 0, 1}, TP.D, 1, &TP.ucat);
+  const auto c1 = std::chrono::steady_clock::now();
+  pack_reg(blk, {&TP.Ltt, &TP.Utt, &TP.Uht}, {0, 1, 1}, TP.U, 1, &TP.ucat);
+  if (getenv("GEMSLR_DEBUG_TAIL"))
+    fprintf(stderr, "pack_reg D %.2f s U %.2f s\n", std::chrono::duration<double>(c1 - c0).count(),
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - c1).count());
+  TP.ok = TP.D.ok && TP.U.ok;
+  if (getenv("GEMSLR_DEBUG_TAIL"))
+    for (const RegPack<T> *R : {&TP.D, &TP.U})
+      fprintf(stderr, "tail pack: ok %d ring %d imports %d W %d la %d far %lld records %lld max_block_slices %d\n",
+              (int)R->ok, R->ring, R->imp_L, R->W, R->la, (long long)R->far, (long long)R->nrec, R->max_block_slices);
+}
+
 // Q > 1: the split form (every block's sweeps over a Q-CTA cluster); when it
 // cannot be built (a dependency two chunks away, too many imports) the stage
 // falls back to Q / 2, down to the one-CTA form.  The split form has no TMA /
-// level-kernel variant (their blocks must be independent).
+// level-kernel variant (their blocks must be independent).  tails: the tail form
+// as well (one CTA per block).
 template <typename T>
-void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, Stage<T> &S, int Q) {
+void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &fac, Stage<T> &S, int Q,
+                const std::vector<int64_t> *tails) {
   S.blk = blk;
+  S.tail = TailPack<T>();
+  const auto t0 = std::chrono::steady_clock::now();
+  if (tails) pack_tail(blk, fac, *tails, S.tail);
+  if (getenv("GEMSLR_DEBUG_TAIL"))
+    fprintf(stderr, "pack_tail %.2f s\n", std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  // a tail-ordered block's tail rows read every chunk: no split form
+  if (S.tail.ok) Q = 1;
   for (; Q > 1; Q /= 2) {
     pack_sweep(blk, fac, false, S.Lp, Q);
     pack_sweep(blk, fac, true, S.Up, Q);
-    pack_reg(blk, S.Lp, S.Up, S.reg, Q);
+    pack_reg(blk, {&S.Lp, &S.Up}, {0, 1}, S.reg, Q);
     if (S.reg.ok) {
       S.pipe = PipePack<T>();
       return;
@@ -666,10 +904,15 @@ void pack_stage(const std::vector<int64_t> &blk, const std::vector<Factor<T>> &f
   pack_sweep(blk, fac, false, S.Lp);
   pack_sweep(blk, fac, true, S.Up);
   pack_pipe(blk, S.Lp, S.Up, S.pipe);
-  pack_reg(blk, S.Lp, S.Up, S.reg);
+  pack_reg(blk, {&S.Lp, &S.Up}, {0, 1}, S.reg);
+  if (getenv("GEMSLR_DEBUG_TAIL"))
+    fprintf(stderr, "full pack: ok %d ring %d imports %d xmode %d W %d\n", (int)S.reg.ok, S.reg.ring, S.reg.imp_L,
+            (int)S.reg.xmode, S.reg.W);
 }
 
-template void pack_stage<double>(const std::vector<int64_t> &, const std::vector<Factor<double>> &, Stage<double> &, int);
-template void pack_stage<zc>(const std::vector<int64_t> &, const std::vector<Factor<zc>> &, Stage<zc> &, int);
+template void pack_stage<double>(const std::vector<int64_t> &, const std::vector<Factor<double>> &, Stage<double> &, int,
+                                 const std::vector<int64_t> *);
+template void pack_stage<zc>(const std::vector<int64_t> &, const std::vector<Factor<zc>> &, Stage<zc> &, int,
+                             const std::vector<int64_t> *);
 
 }  // namespace gemslr
