@@ -508,6 +508,10 @@ static int reg_nw_for(const RegPack<T> &R) {
   const double K = lv > 0 ? (double)sl / (double)lv : 1.0;
   if (sizeof(D) == 8) {
     if (env == 15 || env == 23) return env;
+    // tail form of the deep stages (one CTA streams a whole level-0 block's records, the
+    // per-SM bytes in flight bound it): 31 warps, one buffer each, 64 registers (spill-free
+    // up to W = 12).  C5 level 0: DOWN / UP 235 / 253 -> 211 / 235 us per apply vs 23 warps.
+    if (R.nsweep == 3 && K >= 2.5 && R.W <= 12 && env != 23) return 31;
     // split chunks (C5 level 0 at Q = 4: K = 2.8): 23 warps measured 4 % faster than 15
     return K >= (R.Q > 1 ? 2.5 : 3.0) ? 23 : 15;
   }
@@ -1162,7 +1166,10 @@ static void launch_tail(Ctx *ctx, const StageDev<D> &S, bool down, const D *rhs,
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
     using ILA = std::integral_constant<int, REG_LA_DEV>;
-    if (nw == 23) {
+    if (nw == 31) {
+      if (la > 0) by_w(std::integral_constant<int, 31>{}, I1{}, ILA{});
+      else by_w(std::integral_constant<int, 31>{}, I1{}, I0{});
+    } else if (nw == 23) {
       if (la > 0) by_w(std::integral_constant<int, 23>{}, I1{}, ILA{});
       else by_w(std::integral_constant<int, 23>{}, I1{}, I0{});
     } else {
