@@ -938,7 +938,8 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
       if constexpr (TAIL) {                                        // written by earlier kernels or sweeps: L2
         if (upper) B.dg = ld_nc(reinterpret_cast<const T *>(op + 32) + lane);
         B.rhs = ld_cg(t_ra + ri + t_off);
-        if (t_rb) B.rhs = B.rhs - ld_cg(t_rb + ri + t_off);
+        // (subtracted at the solve: a use here would wait for every load just issued)
+        B.xo = t_rb ? ld_cg(t_rb + ri + t_off) : dzero<T>();
         return;
       }
       if (upper) {
@@ -985,6 +986,7 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
     constexpr int WO = W - LA;                                     // old columns [0, WO), new [WO, W)
     auto solve_old = [&](const Buf &B) {
       T a0 = B.rhs, a1 = dzero<T>(), a2 = dzero<T>(), a3 = dzero<T>();
+      if constexpr (TAIL) a1 = -B.xo;
 #pragma unroll
       for (int e = 0; e < WO; e += 4) {
         a0 -= B.val(e) * ring[B.slot(e)];
@@ -1017,6 +1019,7 @@ __global__ void __launch_bounds__(32 * (NW + (SPLIT ? 1 : 0)), 1) k_tri_reg(RegD
         tp[5] = clock64() + (q != q ? 1 : 0);
       }
       T acc = B.rhs, a1 = dzero<T>(), a2 = dzero<T>(), a3 = dzero<T>();
+      if constexpr (TAIL) a1 = -B.xo;
 #pragma unroll
       for (int e = 0; e < W; e += 4) {
         acc -= B.val(e) * ring[B.slot(e)];
