@@ -595,7 +595,7 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
   }
   // tail form: only next to the one-CTA / split register kernel (the same record format)
   const bool no_tail = getenv("GEMSLR_TAIL") && atoi(getenv("GEMSLR_TAIL")) != 1;   // 0 off, 2 order only
-  if (S.tail.ok && !no_tail && sizeof(D) == 8 && d.nblk > 0 && cps_override <= 0 && tri_kernel == 0) {
+  if (S.tail.ok && !no_tail && d.nblk > 0 && cps_override <= 0 && tri_kernel == 0) {
     const TailPack<T> &TP = S.tail;
     auto mk = [&](const RegPack<T> &R, RegDev<D> &G, int &w, int &nw, int &la, size_t &smem) {
       G = RegDev<D>{};
@@ -1126,9 +1126,7 @@ template <typename D>
 static void launch_tail(Ctx *ctx, const StageDev<D> &S, bool down, const D *rhs, D *x, const FArgs<D> &fa,
                         const int *doneflag, int kc, int lvl, bool rhs_packed) {
   if (S.nblk <= 0 || S.rows == 0) return;
-  if constexpr (sizeof(D) != 8) {
-    throw Error{GEMSLR_ERR_STATE, "tail form: fp64 only"};
-  } else {
+  {
     {
       const Timed tt(ctx->prof, ctx->stream, KC_PACK);
       if (down && !rhs_packed) {
@@ -1166,7 +1164,15 @@ static void launch_tail(Ctx *ctx, const StageDev<D> &S, bool down, const D *rhs,
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
     using ILA = std::integral_constant<int, REG_LA_DEV>;
-    if (nw == 31) {
+    if constexpr (sizeof(D) != 8) {                                // complex: 15 warps, one buffer (or 7, two)
+      if (nw == 15) {
+        if (la > 0) by_w(std::integral_constant<int, 15>{}, I1{}, ILA{});
+        else by_w(std::integral_constant<int, 15>{}, I1{}, I0{});
+      } else {
+        if (la > 0) by_w(std::integral_constant<int, 7>{}, I2{}, ILA{});
+        else by_w(std::integral_constant<int, 7>{}, I2{}, I0{});
+      }
+    } else if (nw == 31) {
       if (la > 0) by_w(std::integral_constant<int, 31>{}, I1{}, ILA{});
       else by_w(std::integral_constant<int, 31>{}, I1{}, I0{});
     } else if (nw == 23) {
@@ -2606,7 +2612,7 @@ static gemslr_status do_setup(gemslr_ctx *c, std::unique_ptr<Engine<T>> &E, int6
   if (getenv("GEMSLR_SPLIT")) opt.split = atoi(getenv("GEMSLR_SPLIT"));
   // tail form (DESIGN 6b): boundary rows last in every B_l and the tail sweeps; fp64 with
   // the register kernel (GEMSLR_TAIL=0 keeps the plain order and sweeps; =2 the order only)
-  opt.tail = (std::is_same<T, double>::value && prm->tri_kernel == 0 && prm->cluster_ctas <= 0) ? 1 : 0;
+  opt.tail = (prm->tri_kernel == 0 && prm->cluster_ctas <= 0) ? 1 : 0;
   if (opt.split > 1) opt.tail = 0;                                  // a forced split form keeps the plain order
   if (getenv("GEMSLR_TAIL")) opt.tail = opt.tail && atoi(getenv("GEMSLR_TAIL")) != 0;
   if (getenv("GEMSLR_TAIL_DIST")) opt.tail_dist = atoi(getenv("GEMSLR_TAIL_DIST"));   // experiments

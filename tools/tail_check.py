@@ -47,7 +47,7 @@ for name in [a for a in sys.argv[1:] if not a.startswith('--')] or ['C5']:
                 lr = B.lowrank(l)
                 if lr is not None:
                     Pc.set_lowrank(l, lr[0], lr[2])
-        r = P.rhs_vector(prob.n, False, 5)
+        r = P.rhs_vector(prob.n, prob.is_complex, 5)
         yg = s.apply_precond(torch.from_numpy(r).cuda()).cpu().numpy()     # both in the permuted order (as smoke())
         yo = Pc.apply(r)
         print('  apply parity rel err %.3e' % (np.linalg.norm(yg - yo) / np.linalg.norm(yo)))
