@@ -62,6 +62,8 @@ def lib():
         L.or_fgmres.argtypes = [C.c_int, i64, vp, vp, vp, vp, vp, vp, vp, C.c_double, C.c_int, C.c_int,
                                 C.POINTER(C.c_int), dp, C.c_int, C.POINTER(C.c_int), dp, C.c_int, dp]
         L.or_fgmres.restype = C.c_int
+        L.or_fgmres_dcgs2.argtypes = L.or_fgmres.argtypes
+        L.or_fgmres_dcgs2.restype = C.c_int
         _lib = L
     return _lib
 
@@ -251,8 +253,9 @@ class Precond:
 _PRECOND_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
 
 
-def fgmres(A, b, x0=None, M=None, rtol=1e-8, restart=30, maxit=1000, diag=False):
-    """c5: FGMRES(m) with CGS2 on natural-order A.
+def fgmres(A, b, x0=None, M=None, rtol=1e-8, restart=30, maxit=1000, diag=False, orth="cgs2"):
+    """c5: FGMRES(m) with CGS2 on natural-order A (orth="dcgs2": c5', the lagged
+    DCGS2 variant of reading Q38).
 
     M: None (identity), an oracle.Precond (applied as P M^{-1} Pᵀ), or a
     Python callable v -> z (e.g. a dense solve in the pins).
@@ -283,7 +286,10 @@ def fgmres(A, b, x0=None, M=None, rtol=1e-8, restart=30, maxit=1000, diag=False)
     hlen = C.c_int(0)
     fin = C.c_double(0)
     dg = np.zeros(3)
-    st = lib().or_fgmres(cplx, n, _p(rp), _p(ci), _p(v), fn, user, _p(b), _p(x), float(rtol), int(restart),
+    if orth not in ("cgs2", "dcgs2"):
+        raise ValueError(f"orth must be 'cgs2' or 'dcgs2', not {orth!r}")
+    fg = lib().or_fgmres if orth == "cgs2" else lib().or_fgmres_dcgs2
+    st = fg(cplx, n, _p(rp), _p(ci), _p(v), fn, user, _p(b), _p(x), float(rtol), int(restart),
                          int(maxit), C.byref(its), hist.ctypes.data_as(C.POINTER(C.c_double)), hcap,
                          C.byref(hlen), C.byref(fin), int(diag), dg.ctypes.data_as(C.POINTER(C.c_double)))
     del keep

@@ -19,6 +19,7 @@
 //   Precond::apply  Alg. 2 pGeMSLRSolve, single-pass, unrolled (c4)
 //   Precond::ghat   Ĝ_l = E_l U_l^-1 L_l^-1 F_l C_l^-1        (Q4)
 //   fgmres          FGMRES(m) with CGS2 + Givens               (c5; Q14/Q15)
+//   fgmres_dcgs2    the same with DCGS2 (lagged reorthogonalisation) (c5'; Q14/Q38)
 //
 // Pins: see tests/test_oracle_pins.py (closed forms, textbook special cases,
 // dense LU/Schur on tiny problems).  Nothing here is "parity unpinned".
@@ -675,6 +676,196 @@ FgmresOut<T> fgmres(const Csr<T> &A, precond_fn M, void *Muser, const T *b, T *x
   return out;
 }
 
+// ---- c5': FGMRES(m) with DCGS2 (reading Q38; Q14 admits a lagged variant when
+// both sides adopt it) ----------------------------------------------------------
+// Classical Gram-Schmidt applied twice, as CGS2, but the second projection of the
+// vector made at step j, and its normalisation, are delayed to step j + 1, where
+// they share the passes over the basis with step j + 1's first projection
+// (Swirydowicz, Langou, Ananthan, Yang, Thomas, "Low synchronization Gram-Schmidt
+// and GMRES algorithms", DCGS2-Arnoldi).  u_j is the not yet reorthogonalised,
+// unnormalised new vector (u_0 = r).  Step j:
+//   z_j = M(u_j) ; w = A z_j
+//   c = V_{0:j}^H u_j ; nu = u_j^H u_j ; a = V_{0:j}^H w ; mu = u_j^H w ; eta = ||w||
+//   alpha = sqrt(max(nu - ||c||^2, 0))                       (Pythagoras)
+//   column j-1 completed: Hraw[0:j, j-1] += c, Hraw[j, j-1] = alpha   (j = 0: g_0 = alpha)
+//   h_j = (mu - c^H a) / alpha
+//   v_j = (u_j - V_{0:j} c) / alpha
+//   u_{j+1} = w - V_{0:j} a - v_j h_j ; beta_j = ||u_{j+1}||
+//   Hraw[0:j, j] = a, Hraw[j, j] = h_j                       (completed at step j + 1)
+//   the cycle ends after step j when the residual estimate with H[j+1, j] = beta_j
+//   meets rtol, beta_j <= 1e-14 eta (breakdown), its reaches maxit, or j + 1 = m;
+//   then one more dot pass (c = V_{0:jend}^H u_jend, nu) completes the last column.
+// Each completed column gets the Givens rotations of c5 and one history entry.
+template <typename T>
+FgmresOut<T> fgmres_dcgs2(const Csr<T> &A, precond_fn M, void *Muser, const T *b, T *x,
+                          double rtol, int m, int maxit, bool diag) {
+  const int64_t n = A.n;
+  FgmresOut<T> out;
+  const double bnorm = nrm2(n, b);
+  if (bnorm == 0.0) {
+    std::fill(x, x + n, T(0));
+    out.hist.push_back(0.0);
+    return out;
+  }
+  double afro = 0.0;
+  for (int64_t p = 0; p < A.nnz(); ++p) afro += abs2(A.val[p]);
+  afro = std::sqrt(afro);
+  std::vector<T> r(n), w(n), V((size_t)n * (m + 1)), Z((size_t)n * m);
+  std::vector<T> H((size_t)(m + 1) * m), Hraw((size_t)(m + 1) * m), g(m + 1);
+  std::vector<double> cs(m);
+  std::vector<T> sn(m);
+  auto resid = [&]() {                                      // r = b - A x
+    spmv(A, x, r.data());
+#pragma omp parallel for schedule(static) if (n > 4096)
+    for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
+    return nrm2(n, r.data());
+  };
+  auto col = [&](std::vector<T> &M_, int j) { return M_.data() + (size_t)j * (m + 1); };
+  // Givens rotations of c5 on the completed column j (Hraw -> H), then rotation j
+  auto finish_column = [&](int j) {
+    T *Hj = col(H, j);
+    for (int i = 0; i <= j + 1; ++i) Hj[i] = col(Hraw, j)[i];
+    for (int i = 0; i < j; ++i) {
+      T p = Hj[i], q = Hj[i + 1];
+      Hj[i] = cs[i] * p + conjv(sn[i]) * q;
+      Hj[i + 1] = -sn[i] * p + cs[i] * q;
+    }
+    T a = Hj[j];
+    double bb = absval(Hj[j + 1]);
+    double aa = absval(a);
+    double c; T s;
+    if (bb == 0.0) { c = 1.0; s = T(0); }
+    else if (aa == 0.0) { c = 0.0; s = T(1); }
+    else {
+      double t = std::sqrt(aa * aa + bb * bb);
+      c = aa / t;
+      s = bb * conjv(a) / (aa * t);
+    }
+    cs[j] = c; sn[j] = s;
+    T p = Hj[j], q = Hj[j + 1];
+    Hj[j] = c * p + conjv(s) * q;
+    Hj[j + 1] = -s * p + c * q;
+    T gp = g[j], gq = g[j + 1];
+    g[j] = c * gp + conjv(s) * gq;
+    g[j + 1] = -s * gp + c * gq;
+    out.its += 1;
+    out.hist.push_back(absval(g[j + 1]) / bnorm);
+  };
+  // c = V_{0:j}^H u_j, nu = u_j^H u_j, alpha (u_j in column j of V)
+  auto reorth_coeffs = [&](int j, std::vector<T> &c, double &alpha) {
+    const T *u = V.data() + (size_t)j * n;
+    c.assign(j, T(0));
+    for (int i = 0; i < j; ++i) c[i] = dot(n, V.data() + (size_t)i * n, u);
+    const double nu = abs2(nrm2(n, u));
+    double cc = 0.0;
+    for (int i = 0; i < j; ++i) cc += abs2(c[i]);
+    alpha = std::sqrt(std::max(nu - cc, 0.0));
+  };
+  auto complete = [&](int j, const std::vector<T> &c, double alpha) {   // column j - 1 (j >= 1)
+    T *Hr = col(Hraw, j - 1);
+    for (int i = 0; i < j; ++i) Hr[i] += c[i];
+    Hr[j] = alpha;
+    finish_column(j - 1);
+  };
+  double beta = resid();
+  out.hist.push_back(beta / bnorm);
+  while (beta > rtol * bnorm && out.its < maxit) {
+    std::copy(r.begin(), r.end(), V.begin());                // u_0 = r
+    std::fill(g.begin(), g.end(), T(0));
+    std::fill(H.begin(), H.end(), T(0));
+    std::fill(Hraw.begin(), Hraw.end(), T(0));
+    int jend = 0;
+    for (int j = 0; j < m; ++j) {
+      T *uj = V.data() + (size_t)j * n;
+      T *zj = Z.data() + (size_t)j * n;
+      if (M) M(Muser, uj, zj); else std::copy(uj, uj + n, zj);   // z_j = M(u_j)
+      spmv(A, zj, w.data());                                      // w = A z_j
+      std::vector<T> c, a(j);
+      double alpha;
+      reorth_coeffs(j, c, alpha);                                 // the dots of the step's one pass
+      for (int i = 0; i < j; ++i) a[i] = dot(n, V.data() + (size_t)i * n, w.data());
+      const T mu = dot(n, uj, w.data());
+      const double eta = nrm2(n, w.data());
+      if (j == 0) g[0] = alpha;                                   // r = alpha v_0
+      else complete(j, c, alpha);
+      T ca = T(0);
+      for (int i = 0; i < j; ++i) ca += conjv(c[i]) * a[i];
+      const T hj = (mu - ca) / alpha;
+      T *un = V.data() + (size_t)(j + 1) * n;
+#pragma omp parallel for schedule(static) if (n > 4096)
+      for (int64_t q = 0; q < n; ++q) {                      // v_j, then u_{j+1} (per entry, i ascending)
+        T v = uj[q];
+        for (int i = 0; i < j; ++i) v -= V[(size_t)i * n + q] * c[i];
+        v = v / alpha;
+        T t = w[q];
+        for (int i = 0; i < j; ++i) t -= V[(size_t)i * n + q] * a[i];
+        t -= v * hj;
+        uj[q] = v;
+        un[q] = t;
+      }
+      const double bj = nrm2(n, un);
+      T *Hr = col(Hraw, j);
+      for (int i = 0; i < j; ++i) Hr[i] = a[i];
+      Hr[j] = hj;
+      // the estimate after column j with H[j+1, j] = beta_j (rotations 0..j-1 are final)
+      std::vector<T> t(Hr, Hr + j + 1);
+      for (int i = 0; i < j; ++i) {
+        T p = t[i], q = t[i + 1];
+        t[i] = cs[i] * p + conjv(sn[i]) * q;
+        t[i + 1] = -sn[i] * p + cs[i] * q;
+      }
+      const double tt = std::sqrt(abs2(t[j]) + bj * bj);
+      const double est = tt > 0.0 ? absval(g[j]) * bj / tt : absval(g[j]);
+      jend = j + 1;
+      if (est <= rtol * bnorm || bj <= 1e-14 * eta || out.its + 1 >= maxit) break;
+    }
+    {                                                         // complete column jend - 1
+      std::vector<T> c;
+      double alpha;
+      reorth_coeffs(jend, c, alpha);
+      complete(jend, c, alpha);
+    }
+    if (diag) {
+      for (int a = 0; a < jend; ++a)
+        for (int c = 0; c < jend; ++c) {
+          T d = dot(n, V.data() + (size_t)a * n, V.data() + (size_t)c * n);
+          out.max_orth = std::max(out.max_orth, absval(d - (a == c ? T(1) : T(0))));
+        }
+      // A Z_c = Σ_{i<=c+1} V_i Hraw_{i,c} for c < jend - 1 (v_{jend} is never formed)
+      const int ncheck = jend - 1;
+      if (ncheck > 0) {
+        double num = 0.0, zf = 0.0;
+        for (int c = 0; c < ncheck; ++c) {
+          const T *zc = Z.data() + (size_t)c * n;
+          spmv(A, zc, w.data());
+          for (int i = 0; i <= c + 1; ++i) {
+            const T *vi = V.data() + (size_t)i * n;
+            for (int64_t q = 0; q < n; ++q) w[q] -= vi[q] * Hraw[(size_t)c * (m + 1) + i];
+          }
+          num += abs2(nrm2(n, w.data()));
+          zf += abs2(nrm2(n, zc));
+        }
+        out.max_arnoldi = std::max(out.max_arnoldi, std::sqrt(num) / (afro * std::sqrt(zf)));
+      }
+    }
+    std::vector<T> y(jend);                                  // y = H^-1 g (c5)
+    for (int i = jend - 1; i >= 0; --i) {
+      T s = g[i];
+      for (int c = i + 1; c < jend; ++c) s -= H[(size_t)c * (m + 1) + i] * y[c];
+      y[i] = s / H[(size_t)i * (m + 1) + i];
+    }
+#pragma omp parallel for schedule(static) if (n > 4096)
+    for (int64_t q = 0; q < n; ++q)
+      for (int c = 0; c < jend; ++c) x[q] += Z[(size_t)c * n + q] * y[c];
+    const double est = out.hist.back();
+    beta = resid();
+    out.max_est_gap = std::max(out.max_est_gap, std::fabs(est - beta / bnorm));
+  }
+  out.final_relres = beta / bnorm;
+  out.status = (beta > rtol * bnorm) ? 1 : 0;
+  return out;
+}
+
 template <typename T>
 Csr<T> make_csr(int64_t n, const int64_t *rowptr, const int32_t *col, const void *val) {
   Csr<T> A;
@@ -1014,6 +1205,32 @@ int or_fgmres(int cplx, int64_t n, const int64_t *rowptr, const int32_t *col, co
   }
   Csr<double> A = make_csr<double>(n, rowptr, col, val);
   auto o = fgmres(A, M, Muser, static_cast<const double *>(b), static_cast<double *>(x), rtol, restart, maxit, want_diag != 0);
+  return fill(o);
+}
+
+// The same with DCGS2 (c5', reading Q38).
+int or_fgmres_dcgs2(int cplx, int64_t n, const int64_t *rowptr, const int32_t *col, const void *val,
+                    precond_fn M, void *Muser, const void *b, void *x, double rtol, int restart, int maxit,
+                    int *its, double *hist, int histcap, int *histlen, double *final_relres,
+                    int want_diag, double *diag) {
+  auto fill = [&](auto &o) {
+    *its = o.its;
+    int hl = (int)o.hist.size();
+    *histlen = hl;
+    for (int i = 0; i < hl && i < histcap; ++i) hist[i] = o.hist[i];
+    *final_relres = o.final_relres;
+    if (want_diag && diag) { diag[0] = o.max_orth; diag[1] = o.max_arnoldi; diag[2] = o.max_est_gap; }
+    return o.status;
+  };
+  if (cplx) {
+    Csr<zc> A = make_csr<zc>(n, rowptr, col, val);
+    auto o = fgmres_dcgs2(A, M, Muser, static_cast<const zc *>(b), static_cast<zc *>(x), rtol, restart, maxit,
+                          want_diag != 0);
+    return fill(o);
+  }
+  Csr<double> A = make_csr<double>(n, rowptr, col, val);
+  auto o = fgmres_dcgs2(A, M, Muser, static_cast<const double *>(b), static_cast<double *>(x), rtol, restart, maxit,
+                        want_diag != 0);
   return fill(o);
 }
 

@@ -451,6 +451,116 @@ def test_fgmres_dense_direct_solve_D1(cplx):
     assert np.all(np.diff(out["hist"][:31]) <= 1e-15)   # monotone within the first cycle
 
 
+# ---------------------------------------------------------------- FGMRES with DCGS2 (c5', Q38)
+def test_fgmres_dcgs2_identity_and_exact_preconditioner_one_iteration_D7():
+    A = sp.identity(30, format="csr")
+    b = rng(11).uniform(-1, 1, 30)
+    out = oracle.fgmres(A, b, rtol=1e-10, restart=10, orth="dcgs2")
+    assert out["its"] == 1 and np.allclose(out["x"], b, atol=1e-14)
+    for cplx in (False, True):
+        prob = P.helmholtz_shifted((5, 4, 3)) if cplx else P.convdiff_upwind((6, 5))
+        Ad = prob.scipy().toarray()
+        b = P.rhs_vector(prob.n, cplx, 4)
+        out = oracle.fgmres(prob.scipy(), b, M=lambda v: np.linalg.solve(Ad, v), rtol=1e-10, restart=10,
+                            orth="dcgs2")
+        assert out["its"] == 1
+        assert np.linalg.norm(Ad @ out["x"] - b) <= 1e-10 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_fgmres_dcgs2_dense_direct_solve_D1(cplx):
+    """The same closed-form checks as CGS2 (D1): solution against a dense solve, VᴴV = I and
+    the Arnoldi relation A Z = V H̄ to 1e-12 (north_star), estimate = explicit residual."""
+    prob = P.helmholtz_shifted((6, 6, 4)) if cplx else P.laplacian((32, 32))
+    A = prob.scipy()
+    b = P.rhs_vector(prob.n, cplx, 0)
+    rtol = 1e-8
+    out = oracle.fgmres(A, b, rtol=rtol, restart=30, maxit=3000, diag=True, orth="dcgs2")
+    assert out["status"] == 0
+    Ad = A.toarray()
+    xs = np.linalg.solve(Ad, b)
+    assert np.linalg.norm(Ad @ out["x"] - b) <= rtol * np.linalg.norm(b)
+    kappa = np.linalg.cond(Ad)
+    assert np.linalg.norm(out["x"] - xs) <= kappa * rtol * np.linalg.norm(xs)
+    assert out["orth"] <= 1e-12
+    assert out["arnoldi"] <= 1e-12
+    assert out["est_gap"] <= 1e-8
+    assert out["hist"][0] == pytest.approx(1.0)
+    assert np.all(np.diff(out["hist"][:31]) <= 1e-15)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
+def test_fgmres_history_is_the_least_squares_minimum_over_span_Z(cplx, orth):
+    """FGMRES: after k columns the residual estimate is
+    min_y ||b - A Z_k y|| / ||b||, Z_k the preconditioned vectors (any scaling: the span
+    counts).  A preconditioner that changes at every call (flexible) is recorded and the
+    minimum is recomputed by a dense least-squares solve — a dropped term, a sign or a
+    missing conjugate in the Hessenberg columns breaks the equality."""
+    prob = P.helmholtz_shifted((5, 4, 4)) if cplx else P.convdiff_upwind((9, 8))
+    A = prob.scipy()
+    Ad = A.toarray()
+    n = prob.n
+    b = P.rhs_vector(n, cplx, 6)
+    r = rng(21)
+    Zs = []
+
+    def M(v):                     # a different diagonal scaling at every call: flexible
+        d = 1.0 / (np.diag(Ad) * (1.0 + 0.5 * r.uniform(-1, 1, n)))
+        z = d * v
+        Zs.append(z.copy())
+        return z
+
+    m = 12
+    out = oracle.fgmres(A, b, M=M, rtol=1e-300, restart=m, maxit=m, orth=orth)
+    assert out["its"] == m
+    Z = np.array(Zs[:m]).T
+    bn = np.linalg.norm(b)
+    for k in range(1, m + 1):
+        AZ = Ad @ Z[:, :k]
+        y, *_ = np.linalg.lstsq(AZ, b, rcond=None)
+        best = np.linalg.norm(b - AZ @ y) / bn
+        assert out["hist"][k] == pytest.approx(best, rel=1e-7, abs=1e-14), (k, out["hist"][k], best)
+    x_ref = Z @ np.linalg.lstsq(Ad @ Z, b, rcond=None)[0]
+    assert np.linalg.norm(out["x"] - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
+def test_fgmres_orthonormal_basis_on_an_ill_conditioned_krylov_sequence(cplx, orth):
+    """north_star: ||VᴴV − I|| <= 1e-12.  Eigenvalues spread over 8 decades make the
+    Krylov vectors nearly dependent; one Gram–Schmidt pass then leaves ~1e-12 and worse,
+    the second (immediate in CGS2, delayed in DCGS2) brings it back to ~1e-15."""
+    n = 400
+    r = rng(3)
+    ev = np.logspace(-8, 0, n)
+    if cplx:
+        ev = ev * np.exp(1j * r.uniform(0, 0.3, n))
+    A = sp.diags([ev, 0.3 * ev[:-1]], [0, 1], format="csr")
+    b = r.uniform(-1, 1, n) + (1j * r.uniform(-1, 1, n) if cplx else 0)
+    out = oracle.fgmres(A, b, rtol=1e-300, restart=80, maxit=80, diag=True, orth=orth)
+    assert out["its"] == 80
+    assert out["orth"] <= 2e-14
+    assert out["arnoldi"] <= 1e-14
+
+
+def test_fgmres_dcgs2_matches_cgs2_iterations_with_gemslr():
+    """Both orthogonalisations are CGS applied twice; with the GeMSLR oracle as the
+    preconditioner they need the same number of iterations (±1) and reach rtol."""
+    prob = P.laplacian((16, 16, 8))
+    A = prob.scipy()
+    b = P.rhs_vector(prob.n, False, 0)
+    st = D.tiny_structure(A, prob.coords, 2, 4, nlast=4)
+    Pc = oracle.Precond(A, st, ilu=(oracle.ILUT, 1e-3, 10))
+    o1 = oracle.fgmres(A, b, M=Pc, rtol=1e-8, restart=20)
+    o2 = oracle.fgmres(A, b, M=Pc, rtol=1e-8, restart=20, orth="dcgs2")
+    assert o1["status"] == 0 and o2["status"] == 0
+    assert abs(o1["its"] - o2["its"]) <= 1
+    assert np.linalg.norm(A @ o2["x"] - b) <= 1e-8 * np.linalg.norm(b)
+    k = min(len(o1["hist"]), len(o2["hist"]))
+    assert np.allclose(o1["hist"][:k], o2["hist"][:k], rtol=1e-6, atol=1e-13)
+
+
 def test_fgmres_with_gemslr_oracle_converges_and_rank_helps():
     prob = P.laplacian((16, 16, 8))
     A = prob.scipy()

@@ -29,6 +29,12 @@ MUTATIONS = {
     "apply: t = G^T s": (
         "\n          for (int c = 0; c < kl; ++c) acc += G[l][c * kl + a] * sv[c];",
         "\n          for (int c = 0; c < kl; ++c) acc += G[l][a * kl + c] * sv[c];"),
+    "DCGS2: v_j not reorthogonalised (v_j = u_j / alpha)": (
+        "        for (int i = 0; i < j; ++i) v -= V[(size_t)i * n + q] * c[i];\n        v = v / alpha;",
+        "        v = v / alpha;"),
+    "DCGS2: u_{j+1} without the v_j h_j term": (
+        "        t -= v * hj;\n",
+        ""),
 }
 
 
