@@ -137,14 +137,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def algorithmic_bytes(stats, v, ld_iters, n):
+def algorithmic_bytes(stats, v, ld_iters, n, orth="cgs2", closing=()):
     """Algorithmic bytes per kernel class for the iterations executed.
 
     trisolve: every stored factor entry once (value v + int32 column 4), the U
     diagonal once, the right-hand side read and the solution written (2 v per row);
     the up sweep adds the F_l entries (v + 4) and the read-modify-write of y (2 v
     per row) plus the temporary (2 v per row).
-    gs: CGS2 pass j reads (j+1) basis columns + w (v per element) and passes 2-3 write w.
+    gs: CGS2 pass j reads (j+1) basis columns + w (v per element) and passes 2-3 write w;
+    DCGS2 step j: the dot pass reads j columns + u_j + w, the update pass reads j columns
+    + u_j + w and writes v_j and u_{j+1}; a cycle's closing dot pass reads j + 1 columns.
     """
     per = {}
     down = up = last = 0
@@ -180,7 +182,12 @@ def algorithmic_bytes(stats, v, ld_iters, n):
     per["waxpy"] = wax
     gs = 0
     for j in ld_iters:
-        gs += 3 * (j + 1) * n * v + 3 * n * v + 2 * n * v
+        if orth == "dcgs2":
+            gs += (2 * j + 6) * n * v
+        else:
+            gs += 3 * (j + 1) * n * v + 3 * n * v + 2 * n * v
+    for j in closing:
+        gs += (j + 1) * n * v
     per["gs_total"] = gs
     return per
 
@@ -205,6 +212,7 @@ def run_ours(args):
                   ilu=prm["ilu"], ilut_drop=prm["ilut_drop"], ilut_fill=prm["ilut_fill"], coords=prob.coords,
                   device=local, cluster_ctas=args.cluster_ctas)
     setup_s = time.time() - t0
+    s.set_orthogonalization(args.orth)
     stream = torch.cuda.current_stream()
     bd = s.to_local(torch.from_numpy(b).to(f"cuda:{local}", dtype=s.torch_dtype))
     K, W = args.steps, args.warmup
@@ -253,7 +261,8 @@ def run_ours(args):
     v = 16 if prob.is_complex else 8
     n = s.n_local
     iters_j = [j % restart for j in range(K)]
-    ab = algorithmic_bytes(stats, v, iters_j, n)
+    ab = algorithmic_bytes(stats, v, iters_j, n, args.orth,
+                           closing=[K % restart or restart] if args.orth == "dcgs2" else ())
     gb = {
         "trisolve_down": ab["trisolve_down"] * K, "trisolve_up": ab["trisolve_up"] * K,
         "trisolve_last": ab["trisolve_last"] * K, "spmv": ab["spmv"] * (K + 2),
@@ -334,6 +343,7 @@ def run_ours(args):
             s2 = gm.Solver(prob.rowptr, prob.colidx, prob.values, prm["levels"], prm["subdomains"], prm["rank"],
                            ilu=prm["ilu"], ilut_drop=prm["ilut_drop"], ilut_fill=prm["ilut_fill"], coords=prob.coords,
                            device=local, comm="nccl1")
+            s2.set_orthogonalization(args.orth)
             s2.solve(bd, rtol=1e-300, restart=restart, maxit=max(W, 1))
             torch.cuda.synchronize()
             a0 = s2.stats()["allreduces"]
@@ -351,7 +361,7 @@ def run_ours(args):
             dist_path = {"error": str(e)[:200]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(prob, prm, s, b, args.cpu_iters)
+        cpu = cpu_baseline(prob, prm, s, b, args.cpu_iters, args.orth)
     line = {
         "metric": METRIC, "value": round(ms_per, 4), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": round(ms_per, 4), "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
@@ -362,7 +372,8 @@ def run_ours(args):
                    "n": n, "nnz": prob.nnz, "levels": stats["levels"], "fill": round(stats["fill"], 3),
                    "parallelism": "1 GPU" if world == 1 else f"subdomain row partition over {world} GPUs (NCCL send/recv halos, all-reduce)",
                    "l2": "working set (~2.4 GB) > 126 MB L2; no flush",
-                   "setup_s": round(setup_s, 2), "timed_region": f"{K} FGMRES iterations (maxit=K, unreachable rtol)"},
+                   "setup_s": round(setup_s, 2), "timed_region": f"{K} FGMRES iterations (maxit=K, unreachable rtol)",
+                   "orth": args.orth},
         "cycle": cycle, "roofline": roofline, "kernels": per_kernel,
         "ms_per_step_profiled": round(ms_prof / out2["its"], 4),
         "profiled_note": "per-kernel CUDA events around every launch of a second identical K-iteration solve "
@@ -379,7 +390,7 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
-def cpu_baseline(prob, prm, s, b, iters):
+def cpu_baseline(prob, prm, s, b, iters, orth="cgs2"):
     """The oracle as it stands (C++ with OpenMP over independent work and fixed-order
     reductions), bounded sample: `iters` FGMRES iterations of the same workload on the
     same exported setup bundle, with all physical cores and with one thread."""
@@ -403,7 +414,7 @@ def cpu_baseline(prob, prm, s, b, iters):
         for nt, its in ((nth, iters), (1, max(iters // 2, 2))):
             oracle.set_threads(nt)
             t1 = time.perf_counter()
-            out = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=its)
+            out = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=its, orth=orth)
             res[nt] = (1e3 * (time.perf_counter() - t1) / out["its"], out["its"])
     return {"value": round(res[nth][0], 2), "unit": UNIT, "cores": nth, "kind": "oracle",
             "sample": f"{res[nth][1]} FGMRES iterations of the same {prob.n}-row workload on the same setup bundle "
@@ -430,15 +441,16 @@ def run_reference(args):
     D.arnoldi_lowrank(Pc, prm["rank"], seed=0)
     setup = time.perf_counter() - t0
     K, W = args.steps, args.warmup
-    oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=max(1, min(W, 1)))
+    oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=max(1, min(W, 1)), orth=args.orth)
     t1 = time.perf_counter()
-    out = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=K)
+    out = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=prm["restart"], maxit=K, orth=args.orth)
     dt = time.perf_counter() - t1
     val = 1e3 * dt / out["its"]
     line = {"impl": "reference", "metric": METRIC, "value": round(val, 2), "unit": UNIT, "n_gpus": args.gpus, "steps": out["its"],
             "warmup": W, "ms_per_step": round(val, 2), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded 7-pt Laplacian, b = A x_true)",
-            "config": {"workload": f"{name} per-GPU problem {prob.dims}", "n": prob.n, "setup_s": round(setup, 1)},
+            "config": {"workload": f"{name} per-GPU problem {prob.dims}", "n": prob.n, "setup_s": round(setup, 1),
+                       "orth": args.orth},
             "cpu_baseline": {"value": round(val, 2), "unit": UNIT, "cores": nth, "kind": "oracle", "cpu": info,
                              "sample": f"{out['its']} FGMRES iterations, oracle's own RCB structure, ILU and "
                                        f"one-cycle Arnoldi low rank (setup {setup:.0f}s excluded)"},
@@ -458,6 +470,8 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dist-path", action="store_true")
+    ap.add_argument("--orth", default="dcgs2", choices=["cgs2", "dcgs2"],
+                    help="FGMRES orthogonalisation: CGS2 (c5) or DCGS2 (c5', reading Q38), both sides")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -195,6 +195,16 @@ gemslr_status gemslr_solve(gemslr_ctx *ctx, const void *b_dev, void *x_dev, doub
                            int maxit, int *iterations, double *res_hist, int hist_cap, int *hist_len,
                            double *final_true_relres);
 
+/* Orthogonalisation of the solves that follow on this context (default 0):
+ * 0 = CGS2 (DESIGN.md c5, reading Q14): classical Gram-Schmidt applied twice at
+ *     every step, three passes over the Krylov basis;
+ * 1 = DCGS2 (c5', reading Q38): the same two projections with the second one and
+ *     the normalisation delayed to the next step, where they share its passes
+ *     (one dot pass + one update pass per step); z_j = M(u_j) of the not yet
+ *     normalised u_j, which flexible GMRES admits.
+ * Any other value: GEMSLR_ERR_INVALID_ARG.  No GPU work; the context keeps it. */
+gemslr_status gemslr_set_orthogonalization(gemslr_ctx *ctx, int orth);
+
 /* The same solve with HOST vectors in the ORIGINAL (natural) global order,
  * length n (global): the host->device copy, the permutation into the local
  * layout, the solve, the inverse permutation and the device->host copy all

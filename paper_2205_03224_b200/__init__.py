@@ -23,7 +23,7 @@ STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "INVALID_ARG", -2: "BAD_CSR", -3: "PA
           -5: "LOWRANK", -6: "STATE", -7: "CUDA", -8: "NCCL", -9: "OOM"}
 ABI_FUNCTIONS = ["gemslr_create", "gemslr_nccl_unique_id", "gemslr_create_dist", "gemslr_create_hostcomm", "gemslr_halo_plan", "gemslr_set_allocator", "gemslr_set_coordinates", "gemslr_setup", "gemslr_layout",
                  "gemslr_spmv", "gemslr_apply_precond", "gemslr_spmv_multi", "gemslr_apply_precond_multi",
-                 "gemslr_solve", "gemslr_solve_host", "gemslr_to_local",
+                 "gemslr_solve", "gemslr_set_orthogonalization", "gemslr_solve_host", "gemslr_to_local",
                  "gemslr_to_natural", "gemslr_export_setup", "gemslr_stats", "gemslr_profile", "gemslr_last_error",
                  "gemslr_destroy"]
 
@@ -78,6 +78,7 @@ def lib():
         L.gemslr_export_setup.argtypes = [vp, C.c_char_p]
         L.gemslr_stats.argtypes = [vp, C.c_char_p, C.c_size_t]
         L.gemslr_profile.argtypes = [vp, C.c_int, C.c_int]
+        L.gemslr_set_orthogonalization.argtypes = [vp, C.c_int]
         L.gemslr_last_error.argtypes = [vp]
         L.gemslr_last_error.restype = C.c_char_p
         L.gemslr_destroy.argtypes = [vp]
@@ -276,7 +277,17 @@ class Solver:
                     "apply_precond_multi")
         return Y
 
-    def solve(self, b, x0=None, rtol=1e-8, restart=50, maxit=1000):
+    def set_orthogonalization(self, orth):
+        """'cgs2' (c5, default) or 'dcgs2' (c5', reading Q38) for the solves that follow."""
+        code = {"cgs2": 0, "dcgs2": 1}.get(orth)
+        if code is None:
+            raise ValueError(f"orth must be 'cgs2' or 'dcgs2', not {orth!r}")
+        self._check(lib().gemslr_set_orthogonalization(self.h, code), "set_orthogonalization")
+        self.orth = orth
+
+    def solve(self, b, x0=None, rtol=1e-8, restart=50, maxit=1000, orth=None):
+        if orth is not None:
+            self.set_orthogonalization(orth)
         b = self._dev(b)
         x = self._vec().zero_() if x0 is None else self._dev(x0.clone())
         its, hl, fr = C.c_int(0), C.c_int(0), C.c_double(0)
@@ -285,8 +296,10 @@ class Solver:
                                             len(hist), C.byref(hl), C.byref(fr)), "solve")
         return dict(x=x, its=its.value, hist=hist[:hl.value].copy(), final_relres=fr.value, status=rc)
 
-    def solve_host(self, b, x0=None, rtol=1e-8, restart=50, maxit=1000, out=None):
+    def solve_host(self, b, x0=None, rtol=1e-8, restart=50, maxit=1000, out=None, orth=None):
         """End-to-end solve from host vectors in natural order (copies inside the call)."""
+        if orth is not None:
+            self.set_orthogonalization(orth)
         dt = np.complex128 if self.is_complex else np.float64
         b = np.ascontiguousarray(b, dtype=dt)
         x = out if out is not None else np.zeros(self.n, dtype=dt)

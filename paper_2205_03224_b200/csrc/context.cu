@@ -418,6 +418,7 @@ struct Engine {
   D *H = nullptr, *g = nullptr, *sn = nullptr, *ydev = nullptr;
   double *cs = nullptr, *dbl = nullptr, *hist = nullptr;
   int *ints = nullptr, *done = nullptr;
+  D *Hraw = nullptr, *dcs = nullptr;   // DCGS2: unrotated Hessenberg, [alpha, h_j, eta, beta_j^2]
   int hist_cap = 0;
   D *xb = nullptr, *bb = nullptr;   // host-path staging
   int *hflags = nullptr;             // pinned: done flag of every iteration of a cycle (async D2H)
@@ -426,6 +427,7 @@ struct Engine {
   int graph_m = -1;
   const D *graph_V = nullptr;
   const double *graph_hist = nullptr;  // captured k_fgmres_scale nodes write hist: a new buffer needs new graphs
+  int graph_orth = -1;
   cudaStream_t cap_stream = nullptr;
   ~Engine() {
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -465,12 +467,14 @@ struct Engine {
   void ensure_krylov(int m, int maxit);
   void gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv, int upd, int dot, const D *h_in, D *resv, int ticket, const int *doneflag);
   double norm(const D *x, int64_t nn, int ticket);
+  void dgs_step(int j, int m, int fin, const int *doneflag);
   void export_bundle(const std::string &dir) const;
   std::string stats_json() const;
 };
 
 struct Ctx {
   int device = -1;
+  int orth = 0;                      // FGMRES orthogonalisation: 0 CGS2 (c5), 1 DCGS2 (c5', reading Q38)
   cudaStream_t stream = nullptr;
   Comm comm;
   Allocator alloc;
@@ -1771,6 +1775,75 @@ void Engine<T>::gs_pass(const D *Vb, int64_t ldvv, int64_t nn, int ncols, D *wv,
   CK(cudaGetLastError());
 }
 
+// Step j of FGMRES with DCGS2 (c5', reading Q38): the dot pass over V_{0:j}, u_j = V_j
+// and w (its last CTA completes column j - 1), then the update pass forming v_j and
+// u_{j+1} = V_{j+1} (its last CTA takes the stopping decision).  fin: the closing dot
+// pass of a cycle (w = u_jend, column jend - 1 completed, no update).  Several ranks:
+// the dots and the norm are all-reduced between the passes and the two
+// scalar steps run as one-warp kernels after them.
+template <typename T>
+void Engine<T>::dgs_step(int j, int m, int fin, const int *doneflag) {
+  cudaStream_t st = ctx->stream;
+  FgmDev<D> f{done, ints, dbl, hist, H, g, cs, sn};
+  DcgDev<D> dd{f, Hraw, dcs};
+  const int fuse = dist ? 0 : 1;
+  D *u = V + (size_t)j * ldv;
+  {
+    Timed t(ctx->prof, st, KC_GS);
+    const D *wv = fin ? u : w;
+    // few columns: warp tiles holding every column of their rows (k_dgs_dotw); more:
+    // column groups of up to 32 (k_dgs_dot), the columns dealt to the groups in turn
+    auto gow = [&](auto kern, int tu, int per_sm, int nc) {
+      const int ncg = std::max(1, (j + nc - 1) / nc);
+      const int grid = grid_for((n + 256 * tu - 1) / (256 * tu), per_sm);
+      if ((size_t)(2 * j + 3) * grid > partial_cap) throw Error{GEMSLR_ERR_INVALID_ARG, "DCGS2 partial buffer"};
+      launch_pdl(kern, dim3(grid, ncg), dim3(256), 0, st, n, (const D *)V, ldv, j, (const D *)u, wv, partial,
+                 tickets + 13, res, doneflag, dd, m, fin, fuse);
+    };
+    // (measured on C5 / C4 cycles, ncu: warp tiles in column groups of 8 or 16 for every j
+    // re-read u and w per group and took 5.66 / 47.5 ms per cycle against 4.48 / 37.0 for
+    // this split; warp tiles up to 32 columns 5.08 / 38.6)
+    const int jw = sizeof(D) == 8 ? 16 : 8;                       // warp tiles up to jw columns
+    if constexpr (sizeof(D) == 8) {
+      if (j <= 8) gow(k_dgs_dotw<D, 8, 4>, 4, 2, 8);
+      else if (j <= jw) gow(k_dgs_dotw<D, 16, 2>, 2, 1, 16);
+    } else {
+      if (j <= jw) gow(k_dgs_dotw<D, 8, 2>, 2, 1, 8);
+    }
+    if (j > jw) {
+      constexpr int NPW = 4, TR = sizeof(D) == 8 ? 4 : 2;
+      const int ncg = std::max(1, (j + 8 * NPW - 1) / (8 * NPW));
+      const int64_t nsteps = (n + 32 * TR - 1) / (32 * TR);
+      const int nrb = (int)std::max<int64_t>(1, std::min<int64_t>(nsteps, (2 * num_sm() + ncg - 1) / ncg));
+      if ((size_t)(2 * j + 3) * nrb > partial_cap) throw Error{GEMSLR_ERR_INVALID_ARG, "DCGS2 partial buffer"};
+      launch_pdl(k_dgs_dot<D, NPW, TR>, dim3(nrb, ncg), dim3(256), 0, st, n, (const D *)V, ldv, j, (const D *)u, wv,
+                 partial, tickets + 13, res, doneflag, dd, m, fin, fuse);
+    }
+    CK(cudaGetLastError());
+  }
+  if (!fuse) {
+    allreduce(res, 2 * j + 3);
+    Timed t(ctx->prof, st, KC_FGM);
+    launch_pdl(k_dgs_col<D>, dim3(1), dim3(32), 0, st, dd, m, j, fin, (const D *)res, doneflag);
+    CK(cudaGetLastError());
+  }
+  if (fin) return;
+  {
+    Timed t(ctx->prof, st, KC_GS);
+    constexpr int RPT = 2;
+    const int grid = grid_for((n + 256 * RPT - 1) / (256 * RPT), sizeof(D) == 8 ? 3 : 2);   // resident CTAs (76 / 128 registers)
+    launch_pdl(k_dgs_upd<D, RPT>, dim3(grid), dim3(256), 0, st, n, V, ldv, j, (const D *)w, (const D *)res, partial,
+               tickets + 14, doneflag, dd, m, fuse);
+    CK(cudaGetLastError());
+  }
+  if (!fuse) {
+    allreduce(dcs + 3, 1);
+    Timed t(ctx->prof, st, KC_FGM);
+    launch_pdl(k_dgs_check<D>, dim3(1), dim3(32), 0, st, dd, m, j, (const D *)res, doneflag);
+    CK(cudaGetLastError());
+  }
+}
+
 template <typename T>
 double Engine<T>::norm(const D *x, int64_t nn, int ticket) {
   gs_pass(nullptr, 0, nn, 0, const_cast<D *>(x), 0, 0, nullptr, res, ticket, nullptr);
@@ -2076,6 +2149,8 @@ void Engine<T>::ensure_krylov(int m, int maxit) {
     dbl = P.get<double>(8);
     ints = P.get<int>(8);
     done = P.get<int>(2);
+    Hraw = P.get<D>((size_t)(m + 1) * m);
+    dcs = P.get<D>(4);
     kry_m = m;
   }
   if (hist_cap < maxit + 1) {
@@ -2116,18 +2191,22 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
   hh.push_back(beta / bnorm);
   double *dsc = dbl + 4;
   FgmDev<D> f{done, ints, dbl, hist, H, g, cs, sn};
+  const bool dcgs = ctx->orth == 1;
   while (beta > rtol * bnorm && its < maxit) {
     // V0 = r / beta ; g = (beta, 0, ...) ; state
     {
-      double hv[8] = {bnorm, rtol, 0, 0, 1.0 / beta, 0, 0, 0};
+      double hv[8] = {bnorm, rtol, 0, 0, dcgs ? 1.0 : 1.0 / beta, 0, 0, 0};   // DCGS2: u_0 = r
       int iv[4] = {0, its, maxit, 0};
       CK(cudaMemcpyAsync(dbl, hv, sizeof(hv), cudaMemcpyHostToDevice, s));
       CK(cudaMemcpyAsync(ints, iv, sizeof(iv), cudaMemcpyHostToDevice, s));
       CK(cudaMemsetAsync(done, 0, 2 * sizeof(int), s));
       std::vector<D> g0(m + 1, dzero<D>());
-      if constexpr (std::is_same<D, double>::value) g0[0] = beta; else g0[0] = D{beta, 0.0};
+      if (!dcgs) {                                                // DCGS2: g_0 = alpha from the first dot pass
+        if constexpr (std::is_same<D, double>::value) g0[0] = beta; else g0[0] = D{beta, 0.0};
+      }
       CK(cudaMemcpyAsync(g, g0.data(), (m + 1) * sizeof(D), cudaMemcpyHostToDevice, s));
       CK(cudaMemsetAsync(H, 0, (size_t)(m + 1) * m * sizeof(D), s));
+      if (dcgs) CK(cudaMemsetAsync(Hraw, 0, (size_t)(m + 1) * m * sizeof(D), s));
       Timed t(ctx->prof, s, KC_UTIL);
       k_scale<D><<<grid_for((n + 255) / 256, 4), 256, 0, s>>>(n, w, V, dsc, nullptr);
     }
@@ -2148,6 +2227,10 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
       D *zj = Z + (size_t)jj * ldv;
       apply_from(0, vj, zj, done);                                // Z_j = M^{-1} V_j
       spmv(zj, w, 0, nullptr, done);                              // w = A Z_j
+      if (dcgs) {                                                 // (DCGS2: V_j holds u_j)
+        dgs_step(jj, m, 0, done);
+        return;
+      }
       gs_pass(V, ldv, n, jj + 1, w, 0, 1, nullptr, res1, 7, done);  // h = V^H w, ||w||^2
       gs_pass(V, ldv, n, jj + 1, w, 1, 1, res1, res2, 8, done);     // w -= V h ; h2 = V^H w
       gs_pass(V, ldv, n, jj + 1, w, 1, 0, res2, res3, 9, done);     // w -= V h2 ; ||w||^2
@@ -2162,12 +2245,13 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
     // graphs on one GPU and over NCCL (its calls are captured with the kernels); the
     // host-staged backend synchronises inside its collectives and cannot be captured
     const bool use_graph = !no_graph && !ctx->comm.hostmode() && !ctx->prof.on;
-    if (use_graph && (graph_m != m || graph_V != V || graph_hist != hist)) {
+    if (use_graph && (graph_m != m || graph_V != V || graph_hist != hist || graph_orth != ctx->orth)) {
       for (auto &ge : graphs) if (ge) cudaGraphExecDestroy(ge);
       graphs.assign(m, nullptr);
       graph_m = m;
       graph_V = V;
       graph_hist = hist;
+      graph_orth = ctx->orth;
     }
     auto capture = [&](int jj) {                                 // capture on a private stream, replay on ours
       if (!cap_stream) CK(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
@@ -2236,8 +2320,13 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
     }
     CK(cudaStreamSynchronize(s));
     for (auto e : evs) cudaEventDestroy(e);
-    if (ctx->prof.on) ctx->prof.flush();
     int iv[4];
+    if (dcgs) {                                                   // the closing dot pass completes column jend - 1
+      CK(cudaMemcpy(iv, ints, sizeof(iv), cudaMemcpyDeviceToHost));
+      dgs_step(iv[0], m, 1, nullptr);
+      CK(cudaStreamSynchronize(s));
+    }
+    if (ctx->prof.on) ctx->prof.flush();
     CK(cudaMemcpy(iv, ints, sizeof(iv), cudaMemcpyDeviceToHost));
     const int jend = iv[0];
     const int its_new = iv[1];
@@ -2879,6 +2968,12 @@ gemslr_status gemslr_stats(const gemslr_ctx *c, char *json, size_t cap) {
 // trisolve launches into a device buffer of 4 * 4096 int64.
 extern "C" void gemslr_debug_trace(void *dev_buf) { g_tri_dbg = static_cast<long long *>(dev_buf); }
 extern "C" void gemslr_debug_trace_level(int level) { g_tri_dbg_level = level; }
+
+gemslr_status gemslr_set_orthogonalization(gemslr_ctx *c, int orth) {
+  if (!c || orth < 0 || orth > 1) return fail(c, GEMSLR_ERR_INVALID_ARG, "orth must be 0 (CGS2) or 1 (DCGS2)");
+  c->orth = orth;
+  return GEMSLR_OK;
+}
 
 gemslr_status gemslr_profile(gemslr_ctx *c, int enable, int reset) {
   if (!c) return GEMSLR_ERR_INVALID_ARG;

@@ -2344,6 +2344,429 @@ __global__ void __launch_bounds__(256) k_fgmres_scale(FgmDev<T> f, int m, int j,
   for (int64_t i = b0 * blockDim.x + threadIdx.x; i < n; i += nb * blockDim.x) vnext[i] = dscale(w[i], sc);
 }
 
+// ----------------------------------------------------------------- DCGS2 (c5', reading Q38)
+// FGMRES with the lagged CGS2 of the oracle's fgmres_dcgs2: step j holds the not yet
+// reorthogonalised, unnormalised u_j in column j of V (u_0 = r) and z_j = M(u_j).
+// ONE dot pass   [c, a, nu, mu, eta^2] = [V_{0:j}^H u_j, V_{0:j}^H w, u_j^H u_j, u_j^H w, w^H w]
+// (its last CTA completes column j - 1: alpha = sqrt(nu - |c|^2), Hraw[0:j, j-1] += c,
+// Hraw[j, j-1] = alpha, the Givens rotation of that column, and h_j = (mu - c^H a) / alpha),
+// then ONE update pass  v_j = (u_j - V c) / alpha (in place), u_{j+1} = w - V a - v_j h_j
+// into column j + 1, ||u_{j+1}||^2 (its last CTA takes the stopping decision with the
+// provisional H[j+1, j] = beta_j).  Two passes over the basis per iteration instead of
+// CGS2's three, and no separate scaling pass.
+template <typename T> __device__ inline double dre(T v);
+template <> __device__ inline double dre<double>(double v) { return v; }
+template <> __device__ inline double dre<cd>(cd v) { return v.x; }
+template <typename T> __device__ inline T dfrom(double v);
+template <> __device__ inline double dfrom<double>(double v) { return v; }
+template <> __device__ inline cd dfrom<cd>(double v) { return cd{v, 0.0}; }
+
+// dcs: [0] alpha, [1] h_j, [2] eta (as T), [3] ||u_{j+1}||^2 (reduced)
+template <typename T>
+struct DcgDev {
+  FgmDev<T> f;
+  T *Hraw;            // (m+1) x m column-major, unrotated
+  T *dcs;             // 4 scalars
+};
+
+// Column completion of step j (warp 0 of the calling CTA; the other threads return).
+// res = [c(j), a(j), nu, mu, eta^2] of the dot pass.  fin: the cycle's closing pass (no h_j).
+template <typename T>
+__device__ inline void dcgs_complete(DcgDev<T> d, int m, int j, int fin, const T *__restrict__ res) {
+  __shared__ T hc[GS_MAXC + 2], sns[GS_MAXC];
+  __shared__ double css[GS_MAXC];
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  FgmDev<T> &f = d.f;
+  double cc = 0.0;
+  T ca = dzero<T>();
+  T *Hr = d.Hraw + (int64_t)(j > 0 ? j - 1 : 0) * (m + 1);
+  for (int i = lane; i < j; i += 32) {
+    const T c = res[i];
+    cc += dabs2(c);
+    if (!fin) ca += dconj(c) * res[j + i];
+    const T h = Hr[i] + c;                                   // column j - 1 completed
+    Hr[i] = h;
+    hc[i] = h;
+    if (i < j - 1) { css[i] = f.cs[i]; sns[i] = f.sn[i]; }
+  }
+  cc = warp_sum(cc);
+  ca = warp_sum(ca);
+  const double nu = dre(res[2 * j]);
+  const double alpha = sqrt(fmax(nu - cc, 0.0));
+  __syncwarp();
+  if (lane == 0) {
+    if (j == 0) {
+      f.g[0] = dfrom<T>(alpha);                                // r = alpha v_0
+    } else {
+      const int jc = j - 1;
+      Hr[j] = dfrom<T>(alpha);
+      hc[j] = dfrom<T>(alpha);
+      for (int i = 0; i < jc; ++i) {                           // previous rotations
+        const T p = hc[i], q = hc[i + 1];
+        hc[i] = css[i] * p + dconj(sns[i]) * q;
+        hc[i + 1] = (-sns[i]) * p + css[i] * q;
+      }
+      const T a = hc[jc];
+      const double aa = sqrt(dabs2(a)), bb = alpha;
+      double c;
+      T s;
+      if (bb == 0.0) { c = 1.0; s = dzero<T>(); }
+      else if (aa == 0.0) { c = 0.0; s = dfrom<T>(1.0); }
+      else {
+        const double t = sqrt(aa * aa + bb * bb);
+        c = aa / t;
+        s = dscale(dconj(a), bb / (aa * t));
+      }
+      f.cs[jc] = c;
+      f.sn[jc] = s;
+      const T p = hc[jc], q = hc[jc + 1];
+      hc[jc] = c * p + dconj(s) * q;
+      hc[jc + 1] = (-s) * p + c * q;
+      const T gp = f.g[jc], gq = f.g[jc + 1];
+      f.g[jc] = c * gp + dconj(s) * gq;
+      f.g[jc + 1] = (-s) * gp + c * gq;
+      const int its = f.ints[1] + 1;
+      f.ints[1] = its;
+      f.hist[its] = sqrt(dabs2(f.g[jc + 1])) / f.dbl[0];
+    }
+    if (!fin) {
+      const T mu = res[2 * j + 1];
+      d.dcs[0] = dfrom<T>(alpha);
+      d.dcs[1] = dscale(mu - ca, 1.0 / alpha);                 // h_j = (mu - c^H a) / alpha
+      d.dcs[2] = dfrom<T>(sqrt(fmax(dre(res[2 * j + 2]), 0.0)));
+    }
+  }
+  __syncwarp();
+  if (j > 0) {
+    T *Hj = f.H + (int64_t)(j - 1) * (m + 1);
+    for (int i = lane; i <= j; i += 32) Hj[i] = hc[i];
+  }
+}
+
+// Stopping decision after the update pass of step j (warp 0): column j provisionally
+// [a, h_j] with H[j+1, j] = beta_j; the estimate |g_j| beta_j / sqrt(|t_j|^2 + beta_j^2)
+// after rotations 0..j-1 (the oracle's order), breakdown beta_j <= 1e-14 eta, maxit, m.
+template <typename T>
+__device__ inline void dcgs_check(DcgDev<T> d, int m, int j, const T *__restrict__ res) {
+  __shared__ T sns[GS_MAXC];
+  __shared__ double css[GS_MAXC];
+  __shared__ T ta[GS_MAXC];
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  FgmDev<T> &f = d.f;
+  T *Hr = d.Hraw + (int64_t)j * (m + 1);
+  for (int i = lane; i < j; i += 32) {
+    const T a = res[j + i];
+    Hr[i] = a;
+    ta[i] = a;
+    css[i] = f.cs[i];
+    sns[i] = f.sn[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const T hj = d.dcs[1];
+    Hr[j] = hj;
+    const double bj = sqrt(fmax(dre(d.dcs[3]), 0.0)), eta = dre(d.dcs[2]);
+    // t_j after rotations 0..j-1 (only the last entry matters)
+    T tj = j > 0 ? ta[0] : hj;
+    for (int i = 0; i < j; ++i) {
+      const T q = (i + 1 < j) ? ta[i + 1] : hj;
+      tj = (-sns[i]) * tj + css[i] * q;                          // rotated entry i + 1
+    }
+    const double tt = sqrt(dabs2(tj) + bj * bj);
+    const double gj = sqrt(dabs2(f.g[j]));
+    const double est = tt > 0.0 ? gj * bj / tt : gj;
+    f.ints[0] = j + 1;
+    if (est <= f.dbl[1] * f.dbl[0] || bj <= 1e-14 * eta || f.ints[1] + 1 >= f.ints[2] || j + 1 >= m) *f.done = 1;
+  }
+}
+
+// Dot pass of step j: grid (row blocks, ncg column groups); the columns are dealt to the
+// groups in turn (group cg: c = cg + ncg (w + 8a), so the groups differ by at most one
+// column); warp w owns the group's columns w + 8a, lanes the rows (TR per step, every load
+// of a step in flight).  Column group 0's warp 0 also forms nu, mu, eta^2.  fuse: the last CTA
+// completes column j - 1 (one GPU); else the caller all-reduces res and runs k_dgs_col.
+// Last-CTA tail of the dot passes: the partials of all CTAs reduced in CTA order into
+// res; fuse: column j - 1 completed by the same CTA.
+template <typename T>
+__device__ inline void dcgs_dot_tail(T *__restrict__ partial, int G, unsigned *ticket, T *__restrict__ res,
+                                     DcgDev<T> d, int m, int ncols, int fin, int fuse) {
+  __shared__ bool amlast;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) amlast = (atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1);
+  __syncthreads();
+  if (!amlast) return;
+  __threadfence();
+  reduce_partials(partial, G, 2 * ncols + 3, res);
+  if (threadIdx.x == 0) *ticket = 0;
+  if (!fuse) return;
+  __threadfence();
+  __syncthreads();
+  dcgs_complete(d, m, ncols, fin, res);
+}
+
+template <typename T, int NPW, int TR>
+__global__ void __launch_bounds__(256, 2) k_dgs_dot(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols,
+                                                    const T *__restrict__ u, const T *__restrict__ w,
+                                                    T *__restrict__ partial, unsigned *ticket, T *__restrict__ res,
+                                                    const int *__restrict__ done, DcgDev<T> d, int m, int fin, int fuse) {
+  pdl_launch();
+  pdl_wait();
+  if (done && *done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nrb = gridDim.x, cg = blockIdx.y;
+  T au[NPW], aw[NPW];
+#pragma unroll
+  for (int a = 0; a < NPW; ++a) { au[a] = dzero<T>(); aw[a] = dzero<T>(); }
+  double nu = 0.0, et = 0.0;
+  T mu = dzero<T>();
+  const bool scal = (cg == 0 && warp == 0);
+  const int ncg = gridDim.y;
+  const int64_t nsteps = (n + 32 * TR - 1) / (32 * TR);
+  for (int64_t step = blockIdx.x; step < nsteps; step += nrb) {
+    const int64_t base = step * 32 * TR + lane;
+    T vr[TR][NPW], ur[TR], wr[TR];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const int64_t i = base + 32 * r;
+      const bool ok = i < n;
+      ur[r] = ok ? ld_nc(u + i) : dzero<T>();
+      wr[r] = ok ? ld_nc(w + i) : dzero<T>();
+#pragma unroll
+      for (int a = 0; a < NPW; ++a) {
+        const int c = cg + ncg * (warp + 8 * a);
+        vr[r][a] = (ok && c < ncols) ? ld_nc(V + c * ldv + i) : dzero<T>();
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+#pragma unroll
+      for (int a = 0; a < NPW; ++a) {
+        const T cv = dconj(vr[r][a]);
+        au[a] += cv * ur[r];
+        aw[a] += cv * wr[r];
+      }
+      if (scal) {
+        nu += dabs2(ur[r]);
+        mu += dconj(ur[r]) * wr[r];
+        et += dabs2(wr[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NPW; ++a) {
+    const int c = cg + ncg * (warp + 8 * a);
+    const T su = warp_sum(au[a]), sw = warp_sum(aw[a]);
+    if (lane == 0 && c < ncols) {
+      partial[(int64_t)c * nrb + blockIdx.x] = su;
+      partial[(int64_t)(ncols + c) * nrb + blockIdx.x] = sw;
+    }
+  }
+  if (scal) {
+    nu = warp_sum(nu);
+    mu = warp_sum(mu);
+    et = warp_sum(et);
+    if (lane == 0) {
+      partial[(int64_t)(2 * ncols) * nrb + blockIdx.x] = dfrom<T>(nu);
+      partial[(int64_t)(2 * ncols + 1) * nrb + blockIdx.x] = mu;
+      partial[(int64_t)(2 * ncols + 2) * nrb + blockIdx.x] = dfrom<T>(et);
+    }
+  }
+  dcgs_dot_tail(partial, nrb, ticket, res, d, m, ncols, fin, fuse);
+}
+
+// Warp-tile form: lane i of a warp holds row 32 t + i of TU tiles with the NC columns of
+// its column group (blockIdx.y: columns [NC y, NC y + NC)), u and w (no load shared between
+// the warps, every value of TU tiles in flight); per-lane accumulators for the group's
+// 2 NC results (group 0: + nu, mu, eta^2), summed over the lanes, the warps and the CTAs
+// once at the end.  Groups > 0 re-read u and w (from L2 while the group waves overlap).
+template <typename T, int NC, int TU>
+__global__ void __launch_bounds__(256) k_dgs_dotw(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols,
+                                                  const T *__restrict__ u, const T *__restrict__ w,
+                                                  T *__restrict__ partial, unsigned *ticket, T *__restrict__ res,
+                                                  const int *__restrict__ done, DcgDev<T> d, int m, int fin, int fuse) {
+  pdl_launch();
+  pdl_wait();
+  if (done && *done) return;
+  __shared__ T red[8][2 * NC + 3];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T au[NC], aw[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) { au[c] = dzero<T>(); aw[c] = dzero<T>(); }
+  double nu = 0.0, et = 0.0;
+  T mu = dzero<T>();
+  const int64_t ntiles = (n + 31) / 32;
+  const int c0 = blockIdx.y * NC, ng = min(NC, ncols - c0);
+  const T *Vg = V + (int64_t)c0 * ldv;
+  for (int64_t t0 = ((int64_t)blockIdx.x * 8 + warp) * TU; t0 < ntiles; t0 += (int64_t)gridDim.x * 8 * TU) {
+    T v[TU][NC], ur[TU], wr[TU];
+#pragma unroll
+    for (int q = 0; q < TU; ++q) {
+      const int64_t r = (t0 + q) * 32 + lane;
+      const bool ok = r < n;
+      ur[q] = ok ? ld_nc(u + r) : dzero<T>();
+      wr[q] = ok ? ld_nc(w + r) : dzero<T>();
+#pragma unroll
+      for (int c = 0; c < NC; ++c) v[q][c] = (ok && c < ng) ? ld_nc(Vg + c * ldv + r) : dzero<T>();
+    }
+#pragma unroll
+    for (int q = 0; q < TU; ++q) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const T cv = dconj(v[q][c]);
+        au[c] += cv * ur[q];
+        aw[c] += cv * wr[q];
+      }
+      nu += dabs2(ur[q]);
+      mu += dconj(ur[q]) * wr[q];
+      et += dabs2(wr[q]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const T su = warp_sum(au[c]), sw = warp_sum(aw[c]);
+    if (lane == 0) { red[warp][c] = su; red[warp][NC + c] = sw; }
+  }
+  nu = warp_sum(nu);
+  mu = warp_sum(mu);
+  et = warp_sum(et);
+  if (lane == 0) {
+    red[warp][2 * NC] = dfrom<T>(nu);
+    red[warp][2 * NC + 1] = mu;
+    red[warp][2 * NC + 2] = dfrom<T>(et);
+  }
+  __syncthreads();
+  const int nl = 2 * ng + (blockIdx.y == 0 ? 3 : 0);            // this group's results
+  for (int e = tid; e < nl; e += blockDim.x) {
+    const int src = e < ng ? e : e < 2 * ng ? NC + (e - ng) : 2 * NC + (e - 2 * ng);
+    const int q = e < ng ? c0 + e : e < 2 * ng ? ncols + c0 + (e - ng) : 2 * ncols + (e - 2 * ng);
+    T t = dzero<T>();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][src];
+    partial[(int64_t)q * gridDim.x + blockIdx.x] = t;
+  }
+  dcgs_dot_tail(partial, (int)gridDim.x, ticket, res, d, m, ncols, fin, fuse);
+}
+
+template <typename T>
+__global__ void k_dgs_col(DcgDev<T> d, int m, int j, int fin, const T *__restrict__ res, const int *__restrict__ done) {
+  pdl_launch();
+  pdl_wait();
+  if (done && *done) return;
+  dcgs_complete(d, m, j, fin, res);
+}
+template <typename T>
+__global__ void k_dgs_check(DcgDev<T> d, int m, int j, const T *__restrict__ res, const int *__restrict__ done) {
+  pdl_launch();
+  pdl_wait();
+  if (done && *done) return;
+  dcgs_check(d, m, j, res);
+}
+
+// Update pass of step j: one thread per row (RPT rows, columns 8 at a time, all loads of a
+// chunk in flight): s1 = V c, s2 = V a, v_j = (u_j - s1) / alpha (in place in column j),
+// u_{j+1} = w - s2 - v_j h_j (column j + 1), ||u_{j+1}||^2 reduced in CTA order by the
+// last CTA (fuse: which then takes the stopping decision).
+template <typename T, int RPT>
+__global__ void __launch_bounds__(256) k_dgs_upd(int64_t n, T *V, int64_t ldv, int j, const T *__restrict__ w,
+                                                 const T *__restrict__ res, T *__restrict__ partial, unsigned *ticket,
+                                                 const int *__restrict__ done, DcgDev<T> d, int m, int fuse) {
+  pdl_launch();
+  pdl_wait();
+  if (done && *done) return;
+  __shared__ T sc[GS_MAXC], sa[GS_MAXC];
+  __shared__ double red[8];
+  __shared__ bool amlast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < j; i += blockDim.x) { sc[i] = res[i]; sa[i] = res[j + i]; }
+  const double ia = 1.0 / dre(d.dcs[0]);
+  const T hj = d.dcs[1];
+  __syncthreads();
+  T *u = V + (int64_t)j * ldv, *un = V + (int64_t)(j + 1) * ldv;
+  double nrm = 0.0;
+  const int64_t chunk = 256 * RPT;
+  for (int64_t b0 = (int64_t)blockIdx.x * chunk; b0 < n; b0 += (int64_t)gridDim.x * chunk) {
+    T uu[RPT], ww[RPT], s1[RPT], s2[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int64_t i = b0 + 256 * k + tid;
+      const bool ok = i < n;
+      uu[k] = ok ? u[i] : dzero<T>();
+      ww[k] = ok ? ld_nc(w + i) : dzero<T>();
+      s1[k] = dzero<T>();
+      s2[k] = dzero<T>();
+    }
+    int c = 0;
+    for (; c + 8 <= j; c += 8) {
+      T v[RPT][8];
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        const int64_t i = b0 + 256 * k + tid;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[k][q] = i < n ? ld_nc(V + (c + q) * ldv + i) : dzero<T>();
+      }
+#pragma unroll
+      for (int k = 0; k < RPT; ++k)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          s1[k] += v[k][q] * sc[c + q];
+          s2[k] += v[k][q] * sa[c + q];
+        }
+    }
+    if (c < j) {                                                  // the last 1..7 columns
+      T v[RPT][8];
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        const int64_t i = b0 + 256 * k + tid;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[k][q] = (i < n && c + q < j) ? ld_nc(V + (c + q) * ldv + i) : dzero<T>();
+      }
+#pragma unroll
+      for (int k = 0; k < RPT; ++k)
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (c + q < j) {
+            s1[k] += v[k][q] * sc[c + q];
+            s2[k] += v[k][q] * sa[c + q];
+          }
+    }
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int64_t i = b0 + 256 * k + tid;
+      if (i < n) {
+        const T vv = dscale(uu[k] - s1[k], ia);
+        const T t = ww[k] - s2[k] - vv * hj;
+        u[i] = vv;
+        un[i] = t;
+        nrm += dabs2(t);
+      }
+    }
+  }
+  nrm = warp_sum(nrm);
+  if (lane == 0) red[warp] = nrm;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += red[q];
+    partial[blockIdx.x] = dfrom<T>(s);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) amlast = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!amlast) return;
+  __threadfence();
+  reduce_partials(partial, (int)gridDim.x, 1, d.dcs + 3);
+  if (tid == 0) *ticket = 0;
+  if (!fuse) return;
+  __threadfence();
+  __syncthreads();
+  dcgs_check(d, m, j, res);
+}
+
 // ----------------------------------------------------------------- NEXT-1 root GMRES helpers
 // Start of the root-level inner GMRES (Alg. 2 line 6): beta = ||z2||
 // from the norm pass, the inner state reset, the inner done flag copied from the

@@ -174,6 +174,18 @@ def test_nccl_one_rank_distributed_path(tmp_path, name, dims, over, split):
     assert np.linalg.norm(b - oracle.spmv(prob, xg)) <= prm["rtol"] * np.linalg.norm(b)
     st2 = s.stats()
     assert st2["nranks"] == 1 and st2["allreduces"] > a0          # the all-reduces went through NCCL
+    # DCGS2 on the distributed path: dots and norm all-reduced between the passes, the
+    # column / stopping steps as one-warp kernels (captured with the NCCL calls)
+    a1 = st2["allreduces"]
+    out = s.solve(torch.from_numpy(b[st["perm"]]).to("cuda:0", dtype=dt), rtol=prm["rtol"], restart=prm["restart"],
+                  orth="dcgs2")
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"], orth="dcgs2")
+    assert out["status"] == 0 and abs(out["its"] - ref["its"]) <= 1, (out["its"], ref["its"])
+    h = min(len(out["hist"]), len(ref["hist"]))
+    assert np.allclose(out["hist"][:h], ref["hist"][:h], rtol=1e-6, atol=1e2 * prm["rtol"])
+    xg[st["perm"]] = out["x"].cpu().numpy()
+    assert np.linalg.norm(b - oracle.spmv(prob, xg)) <= prm["rtol"] * np.linalg.norm(b)
+    assert s.stats()["allreduces"] > a1
 
 
 def _nccl_worker(rank, world, port, q, case):

@@ -384,6 +384,58 @@ def test_gram_schmidt_every_column_count(tmp_path, cplx, restart):
     assert out["final_relres"] == pytest.approx(ref["final_relres"], rel=1e-7)
 
 
+@pytest.mark.parametrize("cplx,restart", [(False, 50), (False, 100), (True, 64), (True, 100)])
+def test_dcgs2_every_column_count(tmp_path, cplx, restart):
+    """DCGS2 (c5', reading Q38): one dot pass (column groups of 32) and one update pass
+    per step at 1..restart columns, fp64 and complex, against the oracle's fgmres_dcgs2
+    on the indefinite problems of the CGS2 test: same iteration count, histories equal to
+    1e-7 relative over a full cycle plus a restart (the closing dot pass of every cycle
+    completes its last column), the explicit residual and x."""
+    if cplx:
+        prob = P.helmholtz_shifted((16, 16, 14), omega2h2=1.0, damping=0.01)
+    else:
+        prob = P.laplacian_shifted((20, 20, 20), 0.6)
+    prm = dict(levels=2, subdomains=8, rank=4, ilu="ilut")
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    b = P.rhs_vector(prob.n, cplx, 0)
+    maxit = restart + 10
+    out = s.solve(to_dev(s, b[st["perm"]]), rtol=1e-300, restart=restart, maxit=maxit, orth="dcgs2")
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=restart, maxit=maxit, orth="dcgs2")
+    assert out["its"] == ref["its"] == maxit
+    h = np.asarray(ref["hist"])
+    assert len(out["hist"]) == len(h) == maxit + 1
+    assert h[restart] > 1e-6, "the problem converged too fast to exercise the late columns"
+    assert np.allclose(out["hist"], h, rtol=1e-7, atol=0), np.abs(out["hist"] / h - 1).max()
+    xg = np.empty(prob.n, dtype=b.dtype)
+    xg[st["perm"]] = out["x"].cpu().numpy()
+    assert rel(xg, ref["x"]) <= 1e-7
+    assert out["final_relres"] == pytest.approx(ref["final_relres"], rel=1e-7)
+    # switching back on the same context: CGS2 graphs are captured again and agree with c5
+    out2 = s.solve(to_dev(s, b[st["perm"]]), rtol=1e-300, restart=restart, maxit=12, orth="cgs2")
+    ref2 = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=restart, maxit=12)
+    assert np.allclose(out2["hist"], ref2["hist"], rtol=1e-7, atol=0)
+
+
+@pytest.mark.parametrize("name,dims,over", CASES)
+def test_dcgs2_solve_parity(tmp_path, name, dims, over):
+    """Solves to the config tolerance with DCGS2 on both sides: iterations within +-1 of
+    the oracle's fgmres_dcgs2, true residual <= rtol, histories while above the floor."""
+    prob, b, xt, prm = P.make_config(name, dims=dims, **over)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    perm = st["perm"]
+    out = s.solve(to_dev(s, b[perm]), rtol=prm["rtol"], restart=prm["restart"], maxit=1000, orth="dcgs2")
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"], maxit=1000, orth="dcgs2")
+    assert out["status"] == 0 and ref["status"] == 0
+    assert abs(out["its"] - ref["its"]) <= 1, (out["its"], ref["its"])
+    xg = np.empty(prob.n, dtype=prob.values.dtype)
+    xg[perm] = out["x"].cpu().numpy()
+    true_rel = np.linalg.norm(b - oracle.spmv(prob, xg)) / np.linalg.norm(b)
+    assert true_rel <= prm["rtol"]
+    assert out["final_relres"] == pytest.approx(true_rel, rel=1e-6, abs=1e-14)
+    h = min(len(out["hist"]), len(ref["hist"]))
+    assert np.allclose(out["hist"][:h], ref["hist"][:h], rtol=1e-6, atol=1e2 * prm["rtol"])
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
 def test_full_size_parity(tmp_path, name):
@@ -409,6 +461,14 @@ def test_full_size_parity(tmp_path, name):
     assert true_rel <= prm["rtol"], true_rel
     h = min(len(out["hist"]), len(ref["hist"]))
     assert np.allclose(out["hist"][:h], ref["hist"][:h], rtol=1e-6, atol=1e2 * prm["rtol"])
+    # the same solve with DCGS2 (c5', the orthogonalisation bench.py times) on both sides
+    out = s.solve(to_dev(s, b[perm]), rtol=prm["rtol"], restart=prm["restart"], maxit=1000, orth="dcgs2")
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"], maxit=1000, orth="dcgs2")
+    assert out["status"] == 0 and ref["status"] == 0
+    assert abs(out["its"] - ref["its"]) <= 1, (out["its"], ref["its"])
+    xg[perm] = out["x"].cpu().numpy()
+    true_rel = np.linalg.norm(b - oracle.spmv(prob, xg)) / np.linalg.norm(b)
+    assert true_rel <= prm["rtol"], true_rel
 
 
 @pytest.mark.parametrize("name,dims,over", [("C5", (32, 32, 24), dict(subdomains=4, rank=4)),
