@@ -320,6 +320,8 @@ struct StageDev {
   size_t td_smem = 0, tu_smem = 0;
   const int *tlrow = nullptr;      // per DOWN L position: the row (-1 padding)
   int64_t tnL = 0;                 // DOWN L positions
+  const int *tpos = nullptr;       // row -> its DOWN L position (-1: none), rows < ntpos (DCGS2 pre-packing)
+  int64_t ntpos = 0;
   D *trhsL = nullptr;              // DOWN right-hand sides ([L_hh | L_t|h] order)
   D *tT = nullptr;                 // t = L^-1 b1 (Ucat order)
   D *tu = nullptr;                 // u = L_tt^-1 (F_l y2)_tail (U_tt order)
@@ -443,7 +445,8 @@ struct Engine {
   void exchange(HaloDev<D> &h, const D *src, const int *doneflag, cudaStream_t comm_st = nullptr,
                 const int *sidx = nullptr);
   void allreduce(D *buf, size_t count);
-  void apply_from(int l0, const D *in, D *out, const int *doneflag);
+  void apply_from(int l0, const D *in, D *out, const int *doneflag, bool in_packed = false);
+  bool prepack_ok() const;
   // several right-hand sides (NEXT-4, one GPU): column-major n x nr blocks, leading dimension ld
   D *rM = nullptr, *tmpM = nullptr;
   int64_t multi_cap = 0;                                            // nr * ld of rM / tmpM
@@ -624,6 +627,15 @@ static StageDev<D> upload_stage(Pool &P, cudaStream_t s, const Stage<T> &S, int 
       d.tail = true;
       d.tnL = (int64_t)TP.lrow.size();
       d.tlrow = P.upload<int>(TP.lrow, s);
+      {
+        int64_t mx = -1;
+        for (int r : TP.lrow) mx = std::max<int64_t>(mx, r);
+        std::vector<int> inv((size_t)(mx + 1), -1);
+        for (size_t q = 0; q < TP.lrow.size(); ++q)
+          if (TP.lrow[q] >= 0) inv[(size_t)TP.lrow[q]] = (int)q;
+        d.ntpos = mx + 1;
+        if (d.ntpos > 0) d.tpos = P.upload<int>(inv, s);
+      }
       const int64_t nU = (int64_t)TP.Utt.slice_row.size() + (int64_t)TP.Uht.slice_row.size();
       d.trhsL = P.get<D>(std::max<int64_t>(d.tnL, 1));
       CK(cudaMemsetAsync(d.trhsL, 0, std::max<int64_t>(d.tnL, 1) * sizeof(D), s));
@@ -1413,10 +1425,18 @@ void Engine<T>::spmv(const D *x, D *y, int mode, const D *b, const int *doneflag
   CK(cudaGetLastError());
 }
 
+// DCGS2 pre-packing: the update pass of step j also writes u_{j+1} at its level-0 DOWN
+// positions, so step j + 1's apply skips k_pack_gather (tail form at level 0, single pass)
+template <typename T>
+bool Engine<T>::prepack_ok() const {
+  static const bool off = getenv("GEMSLR_NO_PREPACK") != nullptr;
+  return !off && !lev.empty() && root_its == 0 && lev[0].st.tail && lev[0].st.tpos != nullptr && lev[0].o0 == 0;
+}
+
 // Alg. 2, single pass, from level l0: input `in` and output `out`
 // are local vectors of which the local positions [lo_{l0}, n) are used.
 template <typename T>
-void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
+void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag, bool in_packed) {
   const int L = (int)lev.size();
   cudaStream_t s = ctx->stream;
   if (l0 == 0 && root_its > 0 && L > 0 && !dist) {                // Alg. 2 with GMRES at the root (NEXT-1)
@@ -1437,7 +1457,7 @@ void Engine<T>::apply_from(int l0, const D *in, D *out, const int *doneflag) {
     launch_trisolve(ctx, d.st, TRI_UP, (const D *)nullptr, out, tmp, fa, doneflag, KC_TRI_UP, 0);
     return;
   }
-  bool packed = false;                                             // this level's rhs already packed by k_ewx
+  bool packed = in_packed && l0 == 0 && prepack_ok();             // this level's rhs already packed (k_ewx / k_dgs_upd)
   for (int l = l0; l < L; ++l) {
     LevelDev<D> &d = lev[l];
     const D *src = (l == l0) ? in : r;
@@ -1810,14 +1830,22 @@ void Engine<T>::dgs_step(int j, int m, int fin, const int *doneflag) {
     } else {
       if (j <= jw) gow(k_dgs_dotw<D, 8, 2>, 2, 1, 8);
     }
-    if (j > jw) {
-      constexpr int NPW = 4, TR = sizeof(D) == 8 ? 4 : 2;
-      const int ncg = std::max(1, (j + 8 * NPW - 1) / (8 * NPW));
-      const int64_t nsteps = (n + 32 * TR - 1) / (32 * TR);
+    auto goc = [&](auto kern, int npw, int tr) {
+      const int ncg = std::max(1, (j + 8 * npw - 1) / (8 * npw));
+      const int64_t nsteps = (n + 32 * tr - 1) / (32 * tr);
       const int nrb = (int)std::max<int64_t>(1, std::min<int64_t>(nsteps, (2 * num_sm() + ncg - 1) / ncg));
       if ((size_t)(2 * j + 3) * nrb > partial_cap) throw Error{GEMSLR_ERR_INVALID_ARG, "DCGS2 partial buffer"};
-      launch_pdl(k_dgs_dot<D, NPW, TR>, dim3(nrb, ncg), dim3(256), 0, st, n, (const D *)V, ldv, j, (const D *)u, wv,
-                 partial, tickets + 13, res, doneflag, dd, m, fin, fuse);
+      launch_pdl(kern, dim3(nrb, ncg), dim3(256), 0, st, n, (const D *)V, ldv, j, (const D *)u, wv, partial,
+                 tickets + 13, res, doneflag, dd, m, fin, fuse);
+    };
+    if (j > jw) {
+      if constexpr (sizeof(D) == 8) {
+        // 33-48 columns in one group of 6 per warp (C5 cycle: 2.08 -> 1.86 ms of dot passes there)
+        if (j > 32 && j <= 48) goc(k_dgs_dot<D, 6, 4>, 6, 4);
+        else goc(k_dgs_dot<D, 4, 4>, 4, 4);
+      } else {
+        goc(k_dgs_dot<D, 4, 2>, 4, 2);
+      }
     }
     CK(cudaGetLastError());
   }
@@ -1832,8 +1860,10 @@ void Engine<T>::dgs_step(int j, int m, int fin, const int *doneflag) {
     Timed t(ctx->prof, st, KC_GS);
     constexpr int RPT = 2;
     const int grid = grid_for((n + 256 * RPT - 1) / (256 * RPT), sizeof(D) == 8 ? 3 : 2);   // resident CTAs (76 / 128 registers)
+    const bool pk = prepack_ok() && j + 1 < m;
     launch_pdl(k_dgs_upd<D, RPT>, dim3(grid), dim3(256), 0, st, n, V, ldv, j, (const D *)w, (const D *)res, partial,
-               tickets + 14, doneflag, dd, m, fuse);
+               tickets + 14, doneflag, dd, m, fuse, pk ? lev[0].st.tpos : (const int *)nullptr,
+               pk ? lev[0].st.ntpos : (int64_t)0, pk ? lev[0].st.trhsL : (D *)nullptr);
     CK(cudaGetLastError());
   }
   if (!fuse) {
@@ -2225,7 +2255,7 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
       cudaStream_t st = ctx->stream;
       D *vj = V + (size_t)jj * ldv;
       D *zj = Z + (size_t)jj * ldv;
-      apply_from(0, vj, zj, done);                                // Z_j = M^{-1} V_j
+      apply_from(0, vj, zj, done, dcgs && jj > 0);                // Z_j = M^{-1} V_j (DCGS2 j > 0: V_j pre-packed)
       spmv(zj, w, 0, nullptr, done);                              // w = A Z_j
       if (dcgs) {                                                 // (DCGS2: V_j holds u_j)
         dgs_step(jj, m, 0, done);

@@ -2583,7 +2583,7 @@ __global__ void __launch_bounds__(256, 2) k_dgs_dot(int64_t n, const T *__restri
 // 2 NC results (group 0: + nu, mu, eta^2), summed over the lanes, the warps and the CTAs
 // once at the end.  Groups > 0 re-read u and w (from L2 while the group waves overlap).
 template <typename T, int NC, int TU>
-__global__ void __launch_bounds__(256) k_dgs_dotw(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols,
+__global__ void __launch_bounds__(256, (NC <= 8 && NC * TU * sizeof(T) <= 256) ? 2 : 1) k_dgs_dotw(int64_t n, const T *__restrict__ V, int64_t ldv, int ncols,
                                                   const T *__restrict__ u, const T *__restrict__ w,
                                                   T *__restrict__ partial, unsigned *ticket, T *__restrict__ res,
                                                   const int *__restrict__ done, DcgDev<T> d, int m, int fin, int fuse) {
@@ -2668,11 +2668,13 @@ __global__ void k_dgs_check(DcgDev<T> d, int m, int j, const T *__restrict__ res
 // Update pass of step j: one thread per row (RPT rows, columns 8 at a time, all loads of a
 // chunk in flight): s1 = V c, s2 = V a, v_j = (u_j - s1) / alpha (in place in column j),
 // u_{j+1} = w - s2 - v_j h_j (column j + 1), ||u_{j+1}||^2 reduced in CTA order by the
-// last CTA (fuse: which then takes the stopping decision).
+// last CTA (fuse: which then takes the stopping decision).  pkdst: u_{j+1} also stored at
+// its level-0 DOWN positions pkpos[i] (rows i < npk), the next apply's packed rhs.
 template <typename T, int RPT>
 __global__ void __launch_bounds__(256) k_dgs_upd(int64_t n, T *V, int64_t ldv, int j, const T *__restrict__ w,
                                                  const T *__restrict__ res, T *__restrict__ partial, unsigned *ticket,
-                                                 const int *__restrict__ done, DcgDev<T> d, int m, int fuse) {
+                                                 const int *__restrict__ done, DcgDev<T> d, int m, int fuse,
+                                                 const int *__restrict__ pkpos, int64_t npk, T *__restrict__ pkdst) {
   pdl_launch();
   pdl_wait();
   if (done && *done) return;
@@ -2741,6 +2743,10 @@ __global__ void __launch_bounds__(256) k_dgs_upd(int64_t n, T *V, int64_t ldv, i
         u[i] = vv;
         un[i] = t;
         nrm += dabs2(t);
+        if (i < npk) {                                            // next apply's level-0 packed rhs
+          const int p = pkpos[i];
+          if (p >= 0) pkdst[p] = t;
+        }
       }
     }
   }
