@@ -1144,11 +1144,13 @@ static void launch_tail(Ctx *ctx, const StageDev<D> &S, bool down, const D *rhs,
   if (S.nblk <= 0 || S.rows == 0) return;
   {
     {
-      const Timed tt(ctx->prof, ctx->stream, KC_PACK);
+      // (profiler: a pack is timed and counted only when a kernel is launched)
       if (down && !rhs_packed) {
+        const Timed tt(ctx->prof, ctx->stream, KC_PACK);
         launch_pdl(k_pack_gather<D>, dim3(grid_for((S.tnL + 255) / 256, 4), 1), dim3(256), 0, ctx->stream, S.tnL,
                    S.tlrow, rhs, S.trhsL, doneflag, (int64_t)0, (int64_t)0);
       } else if (!down && S.tnf > 0) {
+        const Timed tt(ctx->prof, ctx->stream, KC_PACK);
         const CsrDev<D> *F = fa.F;
         launch_pdl(k_pack_f<D>, dim3(grid_for((S.tnf + 255) / 256, 4), 1), dim3(256), 0, ctx->stream, (int64_t)S.tnf,
                    S.tfpos, S.tfrow, F->ptr, F->col, F->val, (const D *)x, (int64_t)fa.nloc, fa.yh, (int64_t)fa.nh, fa.yl,

@@ -32,13 +32,13 @@ def launches(path, out):
         per.setdefault(lid, (k, {}))[1][m] = float(r[iv].replace(',', ''))
     # Iterations queued after the done flag run as no-ops (every kernel exits at
     # once; the host reads the flag 6 iterations late): an iteration ends with
-    # its k_fgmres_scale, which moves ~2 vectors when real; drop whole no-op
+    # its k_fgmres_scale (CGS2) or k_dgs_upd (DCGS2), which moves >= 2 vectors when real; drop whole no-op
     # iterations so shares and per-launch figures describe real work.
     items = list(per.items())
     keep, seg = [], []
     for lid, (k, m) in items:
         seg.append((lid, (k, m)))
-        if k.startswith('k_fgmres_scale'):
+        if k.startswith('k_fgmres_scale') or k.startswith('k_dgs_upd'):
             b = m.get('dram__bytes_read.sum', 0.0) + m.get('dram__bytes_write.sum', 0.0)
             if b >= 1e6 or 'dram__bytes_read.sum' not in m:
                 keep.extend(seg)
