@@ -1835,7 +1835,9 @@ void Engine<T>::dgs_step(int j, int m, int fin, const int *doneflag) {
     auto goc = [&](auto kern, int npw, int tr) {
       const int ncg = std::max(1, (j + 8 * npw - 1) / (8 * npw));
       const int64_t nsteps = (n + 32 * tr - 1) / (32 * tr);
-      const int nrb = (int)std::max<int64_t>(1, std::min<int64_t>(nsteps, (2 * num_sm() + ncg - 1) / ncg));
+      // every CTA of every group resident at once (2 per SM): a rounded-up count left one CTA
+      // for a second wave and doubled the pass at 3 column groups (C4, 65-96 columns)
+      const int nrb = (int)std::max<int64_t>(1, std::min<int64_t>(nsteps, (2 * num_sm()) / ncg));
       if ((size_t)(2 * j + 3) * nrb > partial_cap) throw Error{GEMSLR_ERR_INVALID_ARG, "DCGS2 partial buffer"};
       launch_pdl(kern, dim3(nrb, ncg), dim3(256), 0, st, n, (const D *)V, ldv, j, (const D *)u, wv, partial,
                  tickets + 13, res, doneflag, dd, m, fin, fuse);
@@ -1846,7 +1848,7 @@ void Engine<T>::dgs_step(int j, int m, int fin, const int *doneflag) {
         if (j > 32 && j <= 48) goc(k_dgs_dot<D, 6, 4>, 6, 4);
         else goc(k_dgs_dot<D, 4, 4>, 4, 4);
       } else {
-        goc(k_dgs_dot<D, 4, 2>, 4, 2);
+        goc(k_dgs_dot<D, 4, 2>, 4, 2);   // (TR = 4 or 8 columns per warp measured slower on C4)
       }
     }
     CK(cudaGetLastError());
@@ -1860,9 +1862,11 @@ void Engine<T>::dgs_step(int j, int m, int fin, const int *doneflag) {
   if (fin) return;
   {
     Timed t(ctx->prof, st, KC_GS);
-    constexpr int RPT = 2;
-    const int grid = grid_for((n + 256 * RPT - 1) / (256 * RPT), sizeof(D) == 8 ? 3 : 2);   // resident CTAs (76 / 128 registers)
     const bool pk = prepack_ok() && j + 1 < m;
+    // RPT = 2 rows per thread, all CTAs resident (80 / 128 registers); C5 cycle: RPT 1 / 4
+    // measured 5.05 / 4.73 ms against 4.69
+    constexpr int RPT = 2;
+    const int grid = grid_for((n + 256 * RPT - 1) / (256 * RPT), sizeof(D) == 8 ? 3 : 2);
     launch_pdl(k_dgs_upd<D, RPT>, dim3(grid), dim3(256), 0, st, n, V, ldv, j, (const D *)w, (const D *)res, partial,
                tickets + 14, doneflag, dd, m, fuse, pk ? lev[0].st.tpos : (const int *)nullptr,
                pk ? lev[0].st.ntpos : (int64_t)0, pk ? lev[0].st.trhsL : (D *)nullptr);

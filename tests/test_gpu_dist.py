@@ -82,6 +82,18 @@ def _worker(rank, world, port, q, case, bdir):
         res["true_rel"] = float(np.linalg.norm(b - oracle.spmv(prob, xs)) / np.linalg.norm(b))
         res["n_local"] = int(s.n_local)
         res["halo"] = s.stats()["halo_recv"]
+        # DCGS2 across the two ranks (reading Q38): the dots / norm all-reduced between the
+        # passes, the column and stopping steps as one-warp kernels; against the oracle's
+        # fgmres_dcgs2 with the gathered bundle
+        outd = s.solve(torch.from_numpy(b[s.perm]).to("cuda:0", dtype=dt), rtol=prm["rtol"], restart=prm["restart"],
+                       orth="dcgs2")
+        full.zero_()
+        full[torch.from_numpy(s.perm)] = torch.from_numpy(outd["x"].cpu().numpy())
+        dist.all_reduce(full)
+        res["its_d"] = outd["its"]
+        res["status_d"] = outd["status"]
+        res["true_rel_d"] = float(np.linalg.norm(b - oracle.spmv(prob, full.numpy())) / np.linalg.norm(b))
+        res["its_d_oracle"] = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"], orth="dcgs2")["its"]
         q.put((rank, res))
     except Exception as e:  # report, do not hang the parent
         import traceback
@@ -123,6 +135,9 @@ def test_two_ranks_on_one_gpu(case, tmp_path):
     rtol = P.CONFIGS[name]["rtol"]
     assert res[0]["its"] == res[1]["its"]
     assert res[0]["true_rel"] <= rtol
+    assert res[0]["its_d"] == res[1]["its_d"] and res[0]["status_d"] == 0
+    assert abs(res[0]["its_d"] - res[0]["its_d_oracle"]) <= 1, (res[0]["its_d"], res[0]["its_d_oracle"])
+    assert res[0]["true_rel_d"] <= rtol
 
 
 # ---------------------------------------------------------------- NCCL
@@ -213,6 +228,13 @@ def _nccl_worker(rank, world, port, q, case):
         dist.all_reduce(full)
         res.update(its=out["its"], status=out["status"],
                    true_rel=float(np.linalg.norm(b - oracle.spmv(prob, full.numpy())) / np.linalg.norm(b)))
+        outd = s.solve(torch.from_numpy(b[s.perm]).to(f"cuda:{rank}", dtype=dt), rtol=prm["rtol"],
+                       restart=prm["restart"], orth="dcgs2")                     # DCGS2 over NCCL (Q38)
+        full.zero_()
+        full[torch.from_numpy(s.perm)] = torch.from_numpy(outd["x"].cpu().numpy())
+        dist.all_reduce(full)
+        res.update(its_d=outd["its"], status_d=outd["status"],
+                   true_rel_d=float(np.linalg.norm(b - oracle.spmv(prob, full.numpy())) / np.linalg.norm(b)))
         q.put((rank, res))
     except Exception:
         import traceback
@@ -244,3 +266,5 @@ def test_two_ranks_nccl_two_gpus(case):
     from synth import problems as P
     assert res[0]["its"] == res[1]["its"]
     assert res[0]["true_rel"] <= P.CONFIGS[case[0]]["rtol"]
+    assert res[0]["its_d"] == res[1]["its_d"] and res[0]["status_d"] == 0
+    assert res[0]["true_rel_d"] <= P.CONFIGS[case[0]]["rtol"]
