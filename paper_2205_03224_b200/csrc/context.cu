@@ -1863,13 +1863,21 @@ void Engine<T>::dgs_step(int j, int m, int fin, const int *doneflag) {
   {
     Timed t(ctx->prof, st, KC_GS);
     const bool pk = prepack_ok() && j + 1 < m;
-    // RPT = 2 rows per thread, all CTAs resident (80 / 128 registers); C5 cycle: RPT 1 / 4
+    // RPT = 2 rows per thread, all CTAs resident; C5 cycle: RPT 1 / 4 with 8-column batches
     // measured 5.05 / 4.73 ms against 4.69
-    constexpr int RPT = 2;
-    const int grid = grid_for((n + 256 * RPT - 1) / (256 * RPT), sizeof(D) == 8 ? 3 : 2);
-    launch_pdl(k_dgs_upd<D, RPT>, dim3(grid), dim3(256), 0, st, n, V, ldv, j, (const D *)w, (const D *)res, partial,
-               tickets + 14, doneflag, dd, m, fuse, pk ? lev[0].st.tpos : (const int *)nullptr,
-               pk ? lev[0].st.ntpos : (int64_t)0, pk ? lev[0].st.trhsL : (D *)nullptr);
+    auto gou = [&](auto kern, int r, int per_sm) {
+      const int grid = grid_for((n + 256 * r - 1) / (256 * r), per_sm);
+      launch_pdl(kern, dim3(grid), dim3(256), 0, st, n, V, ldv, j, (const D *)w, (const D *)res, partial,
+                 tickets + 14, doneflag, dd, m, fuse, pk ? lev[0].st.tpos : (const int *)nullptr,
+                 pk ? lev[0].st.ntpos : (int64_t)0, pk ? lev[0].st.trhsL : (D *)nullptr);
+    };
+    // fp64: 2 rows x 16 columns per load batch, 2 CTAs per SM (124 registers); C5 cycle 4.50 ms
+    // against 4.68 with 8-column batches (3 CTAs per SM), 4.75 / 5.43 with one row x 16
+    if constexpr (sizeof(D) == 8) {
+      gou(k_dgs_upd<D, 2, 16>, 2, 2);
+    } else {
+      gou(k_dgs_upd<D, 2, 8>, 2, 2);
+    }
     CK(cudaGetLastError());
   }
   if (!fuse) {

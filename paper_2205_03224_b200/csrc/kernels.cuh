@@ -2670,7 +2670,7 @@ __global__ void k_dgs_check(DcgDev<T> d, int m, int j, const T *__restrict__ res
 // u_{j+1} = w - s2 - v_j h_j (column j + 1), ||u_{j+1}||^2 reduced in CTA order by the
 // last CTA (fuse: which then takes the stopping decision).  pkdst: u_{j+1} also stored at
 // its level-0 DOWN positions pkpos[i] (rows i < npk), the next apply's packed rhs.
-template <typename T, int RPT>
+template <typename T, int RPT, int CB = 8>
 __global__ void __launch_bounds__(256) k_dgs_upd(int64_t n, T *V, int64_t ldv, int j, const T *__restrict__ w,
                                                  const T *__restrict__ res, T *__restrict__ partial, unsigned *ticket,
                                                  const int *__restrict__ done, DcgDev<T> d, int m, int fuse,
@@ -2701,34 +2701,34 @@ __global__ void __launch_bounds__(256) k_dgs_upd(int64_t n, T *V, int64_t ldv, i
       s2[k] = dzero<T>();
     }
     int c = 0;
-    for (; c + 8 <= j; c += 8) {
-      T v[RPT][8];
+    for (; c + CB <= j; c += CB) {
+      T v[RPT][CB];
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         const int64_t i = b0 + 256 * k + tid;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[k][q] = i < n ? ld_nc(V + (c + q) * ldv + i) : dzero<T>();
+        for (int q = 0; q < CB; ++q) v[k][q] = i < n ? ld_nc(V + (c + q) * ldv + i) : dzero<T>();
       }
 #pragma unroll
       for (int k = 0; k < RPT; ++k)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < CB; ++q) {
           s1[k] += v[k][q] * sc[c + q];
           s2[k] += v[k][q] * sa[c + q];
         }
     }
-    if (c < j) {                                                  // the last 1..7 columns
-      T v[RPT][8];
+    if (c < j) {                                                  // the last 1..CB-1 columns
+      T v[RPT][CB];
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         const int64_t i = b0 + 256 * k + tid;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[k][q] = (i < n && c + q < j) ? ld_nc(V + (c + q) * ldv + i) : dzero<T>();
+        for (int q = 0; q < CB; ++q) v[k][q] = (i < n && c + q < j) ? ld_nc(V + (c + q) * ldv + i) : dzero<T>();
       }
 #pragma unroll
       for (int k = 0; k < RPT; ++k)
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < CB; ++q)
           if (c + q < j) {
             s1[k] += v[k][q] * sc[c + q];
             s2[k] += v[k][q] * sa[c + q];

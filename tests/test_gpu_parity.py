@@ -320,18 +320,40 @@ def test_zero_rhs_and_maxit(tmp_path):
     assert len(out["hist"]) == 8
 
 
-def test_solve_twice_with_growing_maxit(tmp_path):
+@pytest.mark.parametrize("restart,maxit", [(1, 6), (2, 7), (5, 1), (5, 3), (7, 21)])
+def test_dcgs2_degenerate_cycles(tmp_path, restart, maxit):
+    """DCGS2 (Q38) at the cycle edges: restart 1 (every step closes its cycle), a cycle cut
+    by maxit before its end, maxit = 1, whole cycles; zero right-hand side — histories and
+    iteration counts against the oracle's fgmres_dcgs2."""
+    prob, b, xt, prm = P.make_config("C2", dims=(10, 10, 10), subdomains=4, rank=3)
+    s, B, st, Pc = make_pair(prob, prm, tmp_path)
+    out = s.solve(to_dev(s, np.zeros(prob.n)), rtol=1e-8, restart=restart, orth="dcgs2")
+    assert out["its"] == 0 and out["status"] == 0 and torch.count_nonzero(out["x"]) == 0
+    out = s.solve(to_dev(s, b[st["perm"]]), rtol=1e-300, restart=restart, maxit=maxit, orth="dcgs2")
+    ref = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=restart, maxit=maxit, orth="dcgs2")
+    assert out["its"] == ref["its"] == maxit and out["status"] == 1
+    assert len(out["hist"]) == len(ref["hist"]) == maxit + 1
+    h = np.asarray(ref["hist"])
+    keep = h > 1e-10
+    assert np.allclose(out["hist"][keep], h[keep], rtol=1e-7, atol=0)
+    xg = np.empty(prob.n)
+    xg[st["perm"]] = out["x"].cpu().numpy()
+    assert rel(xg, ref["x"]) <= 1e-7
+
+
+@pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
+def test_solve_twice_with_growing_maxit(tmp_path, orth):
     """The FGMRES iteration graphs are captured once per (restart, basis, history buffer):
     a second solve with a larger maxit (a new history buffer) must re-capture them and
     report the full history (stale graphs wrote past the old buffer)."""
     prob, b, xt, prm = P.make_config("C5", dims=(24, 24, 20), subdomains=8, rank=4)
     s, B, st, Pc = make_pair(prob, prm, tmp_path)
     bd = to_dev(s, b[st["perm"]])
-    first = s.solve(bd, rtol=1e-300, restart=10, maxit=5)
+    first = s.solve(bd, rtol=1e-300, restart=10, maxit=5, orth=orth)
     assert first["its"] == 5 and len(first["hist"]) == 6
     for maxit in (37, 80):
-        out = s.solve(bd, rtol=1e-300, restart=10, maxit=maxit)
-        ref = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=10, maxit=maxit)
+        out = s.solve(bd, rtol=1e-300, restart=10, maxit=maxit, orth=orth)
+        ref = oracle.fgmres(prob, b, M=Pc, rtol=1e-300, restart=10, maxit=maxit, orth=orth)
         assert out["its"] == maxit and len(out["hist"]) == maxit + 1
         h = np.asarray(ref["hist"])
         keep = h > 1e-10            # above the rounding floor (the tail form sums in another order, DESIGN 6b)
