@@ -2319,7 +2319,10 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
     if (use_graph)                                                // all m iterations captured before the first runs
       for (int jj = 0; jj < m; ++jj)
         if (!graphs[jj]) capture(jj);
-    for (j = 0; j < m; ++j) {
+    // the iteration that reaches maxit is known here: nothing is queued after it (the
+    // done flag still ends the cycle earlier on convergence or breakdown)
+    const int jmax = std::min(m, maxit - its);
+    for (j = 0; j < jmax; ++j) {
       if (use_graph) {
         if (!graphs[j]) {                                         // (not reached: captured above)
           if (!cap_stream) CK(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
