@@ -1826,12 +1826,6 @@ void Engine<T>::dgs_step(int j, int m, int fin, const int *doneflag) {
     // re-read u and w per group and took 5.66 / 47.5 ms per cycle against 4.48 / 37.0 for
     // this split; warp tiles up to 32 columns 5.08 / 38.6)
     const int jw = sizeof(D) == 8 ? 16 : 8;                       // warp tiles up to jw columns
-    if constexpr (sizeof(D) == 8) {
-      if (j <= 8) gow(k_dgs_dotw<D, 8, 4>, 4, 2, 8);
-      else if (j <= jw) gow(k_dgs_dotw<D, 16, 2>, 2, 1, 16);
-    } else {
-      if (j <= jw) gow(k_dgs_dotw<D, 8, 2>, 2, 1, 8);
-    }
     auto goc = [&](auto kern, int npw, int tr) {
       const int ncg = std::max(1, (j + 8 * npw - 1) / (8 * npw));
       const int64_t nsteps = (n + 32 * tr - 1) / (32 * tr);
@@ -1842,9 +1836,17 @@ void Engine<T>::dgs_step(int j, int m, int fin, const int *doneflag) {
       launch_pdl(kern, dim3(nrb, ncg), dim3(256), 0, st, n, (const D *)V, ldv, j, (const D *)u, wv, partial,
                  tickets + 13, res, doneflag, dd, m, fin, fuse);
     };
+    if constexpr (sizeof(D) == 8) {
+      if (j <= 8) gow(k_dgs_dotw<D, 8, 4>, 4, 2, 8);
+      else if (j <= jw) gow(k_dgs_dotw<D, 16, 2>, 2, 1, 16);
+    } else {
+      if (j <= jw) gow(k_dgs_dotw<D, 8, 2>, 2, 1, 8);
+    }
     if (j > jw) {
       if constexpr (sizeof(D) == 8) {
         // 33-48 columns in one group of 6 per warp (C5 cycle: 2.08 -> 1.86 ms of dot passes there)
+        // (C5 cycle, dot passes: 8 rows per step with 4 or 2 columns per warp at 17-32 columns
+        // 1.36 / 1.33 ms against 1.29; 2 x 8 at 9-16 columns 0.40 against 0.42 for dotw<16>)
         if (j > 32 && j <= 48) goc(k_dgs_dot<D, 6, 4>, 6, 4);
         else goc(k_dgs_dot<D, 4, 4>, 4, 4);
       } else {
