@@ -228,12 +228,13 @@ def test_root_gmres_NEXT1(tmp_path, name, dims, over, split):
     for seed in (2, 3):
         r = P.rhs_vector(prob.n, prob.is_complex, seed)
         assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
-    out = s.solve(to_dev(s, b[st["perm"]]), rtol=prm["rtol"], restart=prm["restart"])
-    ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"])
-    assert out["status"] == 0 and abs(out["its"] - ref["its"]) <= 1, (out["its"], ref["its"])
-    xg = np.empty(prob.n, dtype=b.dtype)
-    xg[st["perm"]] = out["x"].cpu().numpy()
-    assert np.linalg.norm(b - oracle.spmv(prob, xg)) <= prm["rtol"] * np.linalg.norm(b)
+    for orth in ("cgs2", "dcgs2"):                  # (DCGS2: the outer level-0 pre-packing is off here)
+        out = s.solve(to_dev(s, b[st["perm"]]), rtol=prm["rtol"], restart=prm["restart"], orth=orth)
+        ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"], orth=orth)
+        assert out["status"] == 0 and abs(out["its"] - ref["its"]) <= 1, (orth, out["its"], ref["its"])
+        xg = np.empty(prob.n, dtype=b.dtype)
+        xg[st["perm"]] = out["x"].cpu().numpy()
+        assert np.linalg.norm(b - oracle.spmv(prob, xg)) <= prm["rtol"] * np.linalg.norm(b)
 
 
 def test_complex_shifted_ilu_NEXT3(tmp_path):
@@ -596,10 +597,11 @@ def test_tail_form(tmp_path, monkeypatch, name, dims, over):
         for seed in (2, 3):
             r = P.rhs_vector(prob.n, prob.is_complex, seed)
             assert rel(s.apply_precond(to_dev(s, r)).cpu().numpy(), Pc.apply(r)) <= TOL
-        out = s.solve(to_dev(s, b[st["perm"]]), rtol=prm["rtol"], restart=prm["restart"])
-        ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"])
-        assert out["status"] == 0 and abs(out["its"] - ref["its"]) <= 1, (out["its"], ref["its"])
-        xg = np.empty(prob.n)
-        xg[st["perm"]] = out["x"].cpu().numpy()
-        assert np.linalg.norm(b - oracle.spmv(prob, xg)) <= prm["rtol"] * np.linalg.norm(b)
+        for orth in ("cgs2", "dcgs2"):              # DCGS2: pre-packed level 0 in the tail form only
+            out = s.solve(to_dev(s, b[st["perm"]]), rtol=prm["rtol"], restart=prm["restart"], orth=orth)
+            ref = oracle.fgmres(prob, b, M=Pc, rtol=prm["rtol"], restart=prm["restart"], orth=orth)
+            assert out["status"] == 0 and abs(out["its"] - ref["its"]) <= 1, (orth, out["its"], ref["its"])
+            xg = np.empty(prob.n)
+            xg[st["perm"]] = out["x"].cpu().numpy()
+            assert np.linalg.norm(b - oracle.spmv(prob, xg)) <= prm["rtol"] * np.linalg.norm(b)
         s.close()
