@@ -425,6 +425,8 @@ struct Engine {
   D *xb = nullptr, *bb = nullptr;   // host-path staging
   int *hflags = nullptr;             // pinned: done flag of every iteration of a cycle (async D2H)
   int hflags_cap = 0;
+  char *hstage = nullptr;            // pinned: the cycle-end state (counters, history, H, g)
+  size_t hstage_cap = 0;
   std::vector<cudaGraphExec_t> graphs;   // FGMRES iteration j captured once (one GPU)
   int graph_m = -1;
   const D *graph_V = nullptr;
@@ -436,6 +438,7 @@ struct Engine {
     if (ev_join) cudaEventDestroy(ev_join);
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (hflags) cudaFreeHost(hflags);
+    if (hstage) cudaFreeHost(hstage);
     for (auto &ge : graphs) if (ge) cudaGraphExecDestroy(ge);
     if (cap_stream) cudaStreamDestroy(cap_stream);
   }
@@ -2220,7 +2223,21 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
   } nvtx_range;
   ensure_krylov(m, maxit);
   std::vector<double> hh;
-  const double bnorm = norm(b, n, 6);
+  // ||b||, r = b - A x and ||r|| with one round trip (slot 4 of res is free here)
+  double bnorm, beta;
+  {
+    D *rn = res + 3 * (GS_MAXC + 2);
+    gs_pass(nullptr, 0, n, 0, const_cast<D *>(b), 0, 0, nullptr, rn, 6, nullptr);
+    spmv(x, w, 1, b, nullptr);
+    gs_pass(nullptr, 0, n, 0, w, 0, 0, nullptr, rn + 1, 6, nullptr);
+    D h2[2];
+    CK(cudaMemcpyAsync(h2, rn, 2 * sizeof(D), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double v0, v1;
+    if constexpr (std::is_same<D, double>::value) { v0 = h2[0]; v1 = h2[1]; } else { v0 = h2[0].x; v1 = h2[1].x; }
+    bnorm = std::sqrt(std::max(v0, 0.0));
+    beta = std::sqrt(std::max(v1, 0.0));
+  }
   int its = 0;
   if (bnorm == 0.0) {
     k_fill<D><<<grid_for((n + 255) / 256, 4), 256, 0, s>>>(n, x, dzero<D>());
@@ -2231,9 +2248,6 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
     CK(cudaStreamSynchronize(s));
     return GEMSLR_OK;
   }
-  // r = b - A x
-  spmv(x, w, 1, b, nullptr);
-  double beta = norm(w, n, 6);
   hh.push_back(beta / bnorm);
   double *dsc = dbl + 4;
   FgmDev<D> f{done, ints, dbl, hist, H, g, cs, sn};
@@ -2367,26 +2381,53 @@ int Engine<T>::solve(const D *b, D *x, double rtol, int m, int maxit, int *its_o
         if (((volatile int *)hflags)[j - kLag]) break;
       }
     }
-    CK(cudaStreamSynchronize(s));
-    for (auto e : evs) cudaEventDestroy(e);
-    int iv[4];
+    if (hstage_cap < 64) {
+      if (hstage) cudaFreeHost(hstage);
+      hstage = nullptr;
+      if (cudaMallocHost(&hstage, 4096) != cudaSuccess) throw Error{GEMSLR_ERR_OOM, "pinned staging"};
+      hstage_cap = 4096;
+    }
     if (dcgs) {                                                   // the closing dot pass completes column jend - 1
-      CK(cudaMemcpy(iv, ints, sizeof(iv), cudaMemcpyDeviceToHost));
-      dgs_step(iv[0], m, 1, nullptr);
+      int *jh = reinterpret_cast<int *>(hstage);
+      CK(cudaMemcpyAsync(jh, ints, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      dgs_step(jh[0], m, 1, nullptr);
+    } else {
       CK(cudaStreamSynchronize(s));
     }
-    if (ctx->prof.on) ctx->prof.flush();
-    CK(cudaMemcpy(iv, ints, sizeof(iv), cudaMemcpyDeviceToHost));
-    const int jend = iv[0];
-    const int its_new = iv[1];
-    std::vector<double> hcyc(its_new - its);
-    if (its_new > its) CK(cudaMemcpy(hcyc.data(), hist + its + 1, (its_new - its) * sizeof(double), cudaMemcpyDeviceToHost));
-    for (double v : hcyc) hh.push_back(v);
+    for (auto e : evs) cudaEventDestroy(e);
+    if (ctx->prof.on) {
+      CK(cudaStreamSynchronize(s));
+      ctx->prof.flush();
+    }
+    // the cycle's state in one round trip: counters, history entries, H and g into a
+    // pinned staging buffer on the solver stream
+    const size_t offH = 64 + (((size_t)m + 1) * sizeof(double) + 63) / 64 * 64;
+    const size_t need = offH + ((size_t)(m + 1) * m + m + 1) * sizeof(D);
+    if (hstage_cap < need) {
+      if (hstage) cudaFreeHost(hstage);
+      hstage = nullptr;
+      if (cudaMallocHost(&hstage, need) != cudaSuccess) throw Error{GEMSLR_ERR_OOM, "pinned staging"};
+      hstage_cap = need;
+    }
+    int *iv_h = reinterpret_cast<int *>(hstage);
+    double *hist_h = reinterpret_cast<double *>(hstage + 64);
+    const T *Hh = reinterpret_cast<const T *>(hstage + offH);
+    const T *gh = Hh + (size_t)(m + 1) * m;
+    const int hcnt = std::max(0, std::min(m, hist_cap - its));    // hist[its + 1 .. its + m] (within the buffer)
+    CK(cudaMemcpyAsync(iv_h, ints, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (hcnt > 0) CK(cudaMemcpyAsync(hist_h, hist + its + 1, hcnt * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hstage + offH, H, (size_t)(m + 1) * m * sizeof(D), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hstage + offH + (size_t)(m + 1) * m * sizeof(D), g, (m + 1) * sizeof(D), cudaMemcpyDeviceToHost,
+                       s));
+    CK(cudaStreamSynchronize(s));
+    const int jend = iv_h[0];
+    const int its_new = iv_h[1];
+    if (its_new - its > hcnt) throw Error{GEMSLR_ERR_CUDA, "history beyond the staged entries"};
+    for (int q = 0; q < its_new - its; ++q) hh.push_back(hist_h[q]);
     its = its_new;
     // y = H[0:jend,0:jend]^{-1} g  (upper triangular after the rotations; host)
-    std::vector<T> Hh((size_t)(m + 1) * m), gh(m + 1), y(jend);
-    CK(cudaMemcpy(Hh.data(), H, Hh.size() * sizeof(D), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(gh.data(), g, gh.size() * sizeof(D), cudaMemcpyDeviceToHost));
+    std::vector<T> y(jend);
     for (int i = jend - 1; i >= 0; --i) {
       T acc = gh[i];
       for (int c = i + 1; c < jend; ++c) acc -= Hh[(size_t)c * (m + 1) + i] * y[c];
