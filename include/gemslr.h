@@ -185,8 +185,9 @@ gemslr_status gemslr_spmv_multi(gemslr_ctx *ctx, const void *x_dev, void *y_dev,
 gemslr_status gemslr_apply_precond_multi(gemslr_ctx *ctx, const void *x_dev, void *y_dev, int nrhs, int64_t ld);
 
 /* solve(b, x0, tol, restart) -> (x, iterations, residual history): right-
- * preconditioned FGMRES(restart) with CGS2 (DESIGN.md readings
- * Q14/Q15).  b_dev: device, local permuted layout; x_dev: in x0, out x.
+ * preconditioned FGMRES(restart) with CGS2, or DCGS2 after
+ * gemslr_set_orthogonalization(ctx, 1) (DESIGN.md readings
+ * Q14/Q15/Q38).  b_dev: device, local permuted layout; x_dev: in x0, out x.
  * res_hist (host, may be NULL): relative residual estimates |g_{j+1}|/||b||,
  * entry 0 = initial; *hist_len = number written (<= hist_cap).
  * final_true_relres (may be NULL): ||b - A x||/||b|| recomputed explicitly.
