@@ -137,3 +137,19 @@ def test_host_only_context_refuses_device_calls():
     s = host_solver(prob, 1, 2)
     rc = gm.lib().gemslr_apply_precond(s.h, None, None)
     assert rc in (-1, -6)
+
+
+def test_orthogonalization_setter():
+    """gemslr_set_orthogonalization: 0 (CGS2) and 1 (DCGS2, reading Q38) accepted on any
+    context, anything else INVALID_ARG; the binding maps the names and rejects others."""
+    prob = P.laplacian((6, 6))
+    s = host_solver(prob, 1, 2)
+    assert gm.lib().gemslr_set_orthogonalization(s.h, 0) == 0
+    assert gm.lib().gemslr_set_orthogonalization(s.h, 1) == 0
+    assert gm.lib().gemslr_set_orthogonalization(s.h, 2) == -1
+    assert gm.lib().gemslr_set_orthogonalization(s.h, -1) == -1
+    assert gm.lib().gemslr_set_orthogonalization(None, 1) == -1
+    s.set_orthogonalization("dcgs2")
+    assert s.orth == "dcgs2"
+    with pytest.raises(ValueError):
+        s.set_orthogonalization("mgs")
