@@ -37,17 +37,36 @@ MUTATIONS = {
         ""),
 }
 
+# Rounding-level variants: the same algorithm in exact arithmetic (c = V^H u_j is zero there,
+# so every term below vanishes); they only change what the reorthogonalisation does with
+# the rounding left by the first projection, and no pin of exact mathematics can see them.
+# Reported, not required to be caught (Q38).
+EQUIVALENT = {
+    "DCGS2: alpha = ||u_j|| (no Pythagoras correction)": (
+        "    alpha = std::sqrt(std::max(nu - cc, 0.0));",
+        "    alpha = std::sqrt(std::max(nu, 0.0));"),
+    "DCGS2: h_j = mu / alpha (c^H a dropped)": (
+        "      const T hj = (mu - ca) / alpha;",
+        "      const T hj = mu / alpha;"),
+    "DCGS2: column j - 1 not completed with c": (
+        "    for (int i = 0; i < j; ++i) Hr[i] += c[i];\n    Hr[j] = alpha;",
+        "    Hr[j] = alpha;"),
+}
+
 
 def run():
     orig = open(SRC).read()
     bad = []
     try:
-        for name, (a, b) in MUTATIONS.items():
+        for name, (a, b) in list(MUTATIONS.items()) + list(EQUIVALENT.items()):
             assert orig.count(a) == 1, f"mutation anchor not unique: {name}"
             open(SRC, "w").write(orig.replace(a, b))
             r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", os.path.join(ROOT, "tests", "test_oracle_pins.py")],
                                cwd=ROOT, capture_output=True, text=True)
             caught = r.returncode != 0
+            if name in EQUIVALENT:
+                print(f"{'caught' if caught else 'not caught'} (rounding-level variant, exact-arithmetic equivalent): {name}")
+                continue
             print(f"{'caught' if caught else 'MISSED'}: {name}")
             if not caught:
                 bad.append(name)
