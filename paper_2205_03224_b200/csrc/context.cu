@@ -1834,6 +1834,7 @@ void Engine<T>::dgs_step(int j, int m, int fin, const int *doneflag) {
       const int64_t nsteps = (n + 32 * tr - 1) / (32 * tr);
       // every CTA of every group resident at once (2 per SM): a rounded-up count left one CTA
       // for a second wave and doubled the pass at 3 column groups (C4, 65-96 columns)
+      // (3 CTAs per SM at 80 registers measured slower: 1.73 against 1.58 ms per C5 cycle)
       const int nrb = (int)std::max<int64_t>(1, std::min<int64_t>(nsteps, (2 * num_sm()) / ncg));
       if ((size_t)(2 * j + 3) * nrb > partial_cap) throw Error{GEMSLR_ERR_INVALID_ARG, "DCGS2 partial buffer"};
       launch_pdl(kern, dim3(nrb, ncg), dim3(256), 0, st, n, (const D *)V, ldv, j, (const D *)u, wv, partial,
