@@ -35,6 +35,13 @@ sys.path.insert(0, ROOT)
 from synth import problems as P  # noqa: E402
 
 METRIC = "FGMRES solve-phase ms/iteration (HBM GB/s fraction in roofline)"
+# the operator and right-hand side of each BASELINE config (synth/problems.py CONFIGS)
+_OPER = {"C1": "2D 5-pt Poisson", "C2": "3D 7-pt Laplacian", "C3": "3D upwind convection-diffusion beta=(20,20,20)",
+         "C4": "3D complex shifted Helmholtz omega^2 h^2=0.1", "C5": "3D 7-pt Laplacian"}
+_DATA = {"C1": "seeded 5-pt Poisson, b uniform[-1,1]", "C2": "seeded 7-pt Laplacian, b = A x_true",
+         "C3": "seeded upwind convection-diffusion, b uniform[-1,1]",
+         "C4": "seeded complex shifted Helmholtz, b uniform[-1,1] + i uniform[-1,1]",
+         "C5": "seeded 7-pt Laplacian, b = A x_true"}
 UNIT = "ms/iteration"
 
 
@@ -365,8 +372,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(ms_per, 4), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": round(ms_per, 4), "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-        "dtype": "c128" if prob.is_complex else "f64", "data": "synthetic (seeded 7-pt Laplacian, b = A x_true)",
-        "config": {"workload": f"{name}: 3D 7-pt Laplacian {prob.dims[0]}x{prob.dims[1]}x{prob.dims[2]} per GPU, "
+        "dtype": "c128" if prob.is_complex else "f64", "data": f"synthetic ({_DATA[name]})",
+        "config": {"workload": f"{name}: {_OPER[name]} {'x'.join(str(d) for d in prob.dims)} per GPU, "
                                f"l_ev={prm['levels']}, p={prm['subdomains']}, {prm['ilu'].upper()}(1e-3,10), "
                                f"rank={prm['rank']}, restart={restart}",
                    "n": n, "nnz": prob.nnz, "levels": stats["levels"], "fill": round(stats["fill"], 3),
@@ -448,7 +455,7 @@ def run_reference(args):
     val = 1e3 * dt / out["its"]
     line = {"impl": "reference", "metric": METRIC, "value": round(val, 2), "unit": UNIT, "n_gpus": args.gpus, "steps": out["its"],
             "warmup": W, "ms_per_step": round(val, 2), "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded 7-pt Laplacian, b = A x_true)",
+            "vs_baseline": None, "dtype": "c128" if prob.is_complex else "f64", "data": f"synthetic ({_DATA[name]})",
             "config": {"workload": f"{name} per-GPU problem {prob.dims}", "n": prob.n, "setup_s": round(setup, 1),
                        "orth": args.orth},
             "cpu_baseline": {"value": round(val, 2), "unit": UNIT, "cores": nth, "kind": "oracle", "cpu": info,
